@@ -1,0 +1,25 @@
+"""cvsr ORACLE -- plain fp64 CPU reference of the sliced-reconciliation hot path.
+
+TEST INFRASTRUCTURE ONLY: only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import it.
+It imports nothing from the CUDA package ``paper_2108_08418_b200`` and shares
+no code with it.
+
+Parity-pin status per function:
+  quantise, slice_bits, syndrome  -- pinned (definition, brute force, invariants)
+  llr_slice, llr_biawgn           -- pinned (closed forms, Monte Carlo, normalisation)
+  bp_decode, bp_trace             -- pinned (tree exactness vs brute-force marginals,
+                                     Hamming ML statistics, SPC/repetition closed forms,
+                                     sign symmetry, (3,6) threshold trend)
+  reconcile                       -- pinned (composition: reduces to the pinned parts;
+                                     noiseless limit; MC posterior of the LLR feed)
+  analysis.*                      -- pinned to the paper's printed/derived values
+                                     (gamma, I_AB, A, C_Finite, beta identities);
+                                     delta* and slice capacities: parity unpinned vs
+                                     paper (the paper prints no value)
+"""
+from . import analysis  # noqa: F401
+from .oracle import (  # noqa: F401
+    build, bp_decode, bp_trace, llr_biawgn, llr_slice, quantise, reconcile, slice_bits,
+    syndrome, num_threads,
+)
