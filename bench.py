@@ -1,0 +1,339 @@
+#!/usr/bin/env python3
+"""Benchmark: sliced reconciliation throughput on B200 (driver contract).
+
+A step = one pass of the whole hot path over one
+batch of synthetic input resident in HBM: Bob quantises y and computes the
+syndromes of the coded slices (packed bits of disclosed slices); Alice runs
+the multi-stage conditional-LLR + BP reconciliation of every frame.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl cvsr|reference]
+
+N > 1 runs under torchrun, one rank per GPU; frames are sharded (weak
+scaling, per-GPU work fixed); the only collective is the final NCCL
+all_reduce of statistics and MAX of elapsed time (north star).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "reconciled bits/sec at 1/2/4/8 B200; FER and efficiency β at paper SNR"
+UNIT = "bits/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cvsr", choices=["cvsr", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--frames", type=int, default=0, help="frames per GPU (0 = config default)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = f"/tmp/cvsr_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_workload(cfg_name: str):
+    from cvsr_inputs import configs
+    cfg = configs.CONFIGS[cfg_name]
+    return cfg, cfg.build_codes()
+
+
+# ---------------------------------------------------------------- oracle legs (CPU)
+
+def oracle_sample(cfg, codes_l, frames: int, first_frame: int = 0):
+    """Bounded sample of the workload on the host: the oracle (as it stands) runs
+    Bob (quantise + syndromes) and Alice (reconcile) on `frames` frames."""
+    import oracle
+    from cvsr_inputs import awgn
+    x, y = awgn.quadratures(frames, cfg.n, cfg.gamma, seed=awgn.DATA_SEED + 7, first_frame=first_frame)
+    t0 = time.perf_counter()
+    lab = oracle.quantise(cfg.edges(), y)
+    synd = [oracle.slice_bits(lab, j) if c is None else oracle.syndrome(c, lab, j) for j, c in enumerate(codes_l)]
+    _, ok, _ = oracle.reconcile(codes_l, cfg.order, cfg.edges(), cfg.sigma_n, x, synd, cfg.max_iter)
+    dt = time.perf_counter() - t0
+    return int(ok.sum()) * cfg.m * cfg.n, dt, int(ok.sum())
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    cfg, codes_l = build_workload(args.config)
+    cores = oracle.num_threads()
+    frames = max(2, min(cores, 16))
+    for _ in range(args.warmup):
+        oracle_sample(cfg, codes_l, frames)
+    bits_total, t_total = 0, 0.0
+    for s in range(args.steps):
+        b, dt, _ = oracle_sample(cfg, codes_l, frames, first_frame=s * frames)
+        bits_total += b
+        t_total += dt
+    v = bits_total / t_total
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: m={cfg.m} slices, N_R={cfg.n}, gamma={cfg.gamma}",
+                       "frames_per_step": frames, "sample": True},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{frames} frames x N_R={cfg.n} per step (bounded sample of {cfg.name})"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- CUDA leg
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from cvsr_inputs.awgn import torch_quadratures
+    from paper_2108_08418_b200 import cvsr
+    from paper_2108_08418_b200.pipeline import SRPipeline
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    cfg, codes_l = build_workload(args.config)
+    F = args.frames or cfg.frames
+    n = cfg.n
+    stream = torch.cuda.current_stream(device)
+    pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, device, cfg.max_iter, cfg.q_max,
+                      stream)
+    # rank r owns frames [r F, (r+1) F): per-frame-chunk seeding => identical data for any GPU count
+    x, y = torch_quadratures(F, n, cfg.gamma, device, first_frame=rank * F)
+    torch.cuda.synchronize()
+
+    # untimed reference run for statistics (the batch is identical every step)
+    st = pipe.step(x, y, want_stats=True)
+    undetected = pipe.count_errors()[1]
+    bits_per_step = st["bits_reconciled"]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        pipe.step(x, y)
+    barrier()
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    l0 = pipe.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        pipe.step(x, y)
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = (pipe.launches() - l0) // args.steps
+    t_ms = ev0.elapsed_time(ev1)
+
+    # roofline pass: same steps with per-kernel CUDA events on the launching stream
+    prof = None
+    if not args.no_profile:
+        cvsr.cvsr_ctx_set_profiling(pipe.ctx, True)
+        cvsr.cvsr_ctx_kernel_times(pipe.ctx)  # reset
+        for _ in range(args.steps):
+            pipe.step(x, y)
+        prof = cvsr.cvsr_ctx_kernel_times(pipe.ctx)
+        cvsr.cvsr_ctx_set_profiling(pipe.ctx, False)
+
+    # end-to-end pass: pinned host inputs copied in, results copied out, every step
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        yh = y.cpu().pin_memory()
+        lab_h = torch.empty((F, n), dtype=torch.uint8).pin_memory()
+        ok_h = torch.empty((F,), dtype=torch.uint8).pin_memory()
+        xd, yd = torch.empty_like(x), torch.empty_like(y)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            xd.copy_(xh, non_blocking=True)
+            yd.copy_(yh, non_blocking=True)
+            pipe.step(xd, yd)
+            lab_h.copy_(pipe.label_alice, non_blocking=True)
+            ok_h.copy_(pipe.frame_ok, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        e2e = {"ms": e0.elapsed_time(e1), "h2d": 2 * F * n * 4, "d2h": F * n + F}
+
+    # ---- reduce over ranks (the only collective: statistics + max time)
+    sums = torch.tensor([bits_per_step, st["frames"], st["frames_ok"], undetected] + st["iters_sum"] +
+                        st["edge_iters"], dtype=torch.float64, device=device)
+    tmax = torch.tensor([t_ms, e2e["ms"] if e2e else 0.0], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    sums = sums.cpu().numpy()
+    tmax = tmax.cpu().numpy()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        pipe.close()
+        return
+    m = cfg.m
+    bits_step, frames_all, ok_all, undet = sums[0], sums[1], sums[2], sums[3]
+    iters_sum = sums[4:4 + m]
+    edge_iters = sums[4 + m:4 + 2 * m]
+    ms_step = tmax[0] / args.steps
+    value = bits_step / (ms_step * 1e-3)
+    fer = 1.0 - ok_all / frames_all
+
+    # beta (equation: beta) with the realised rates R_j = 1 - M_j/N_R
+    from oracle import analysis  # host-side analysis only (fp64 formulas), not the hot path
+    rates = [c.rate if c is not None else 0.0 for c in codes_l]
+    pi_my, _ = analysis.entropies(cfg.gamma, m, cfg.delta)
+    beta = analysis.beta(pi_my, m, rates, cfg.gamma)
+
+    peak, peak_src = measured_peaks()
+    roofline = None
+    extra = {}
+    if prof:
+        E = [c.n_edges if c is not None else 0 for c in codes_l]
+        cn_ms, cn_n = prof["cn"]
+        vn_ms, vn_n = prof["vn"]
+        # algorithmic bytes: per edge-iteration the CN half must read the V2C
+        # message and write the C2V message (8 B); per variable-iteration the VN half reads L (4 B).
+        # Units processed = this rank's sum over coded slices of E_j * D_j (edge-iterations).
+        edge_it_rank = float(sum(st["edge_iters"]))
+        var_it_rank = float(sum(st["iters_sum"][j] * n for j in range(m) if codes_l[j] is not None))
+        cn_bytes = 8.0 * edge_it_rank
+        ach = cn_bytes * args.steps / (cn_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "traffic": None, "kernel": "k_cn (check-node pass, fused syndrome test)",
+                    "launches_per_step": cn_n / args.steps, "avg_launch_us": 1e3 * cn_ms / max(cn_n, 1),
+                    "bytes_per_launch": cn_bytes / max(cn_n / args.steps, 1), "peak_source": peak_src,
+                    "share_of_step": cn_ms / args.steps / ms_step}
+        it_bytes = 8.0 * edge_it_rank + 4.0 * var_it_rank
+        it_ach = it_bytes * args.steps / ((cn_ms + vn_ms) * 1e-3) / 1e9
+        extra["roofline_bp_iteration"] = {
+            "bound": "hbm", "achieved": it_ach, "peak": peak, "unit": "GB/s", "frac": it_ach / peak,
+            "note": "whole flooding iteration (k_cn + k_vn): algorithmic 8 B/edge + 4 B/var per iteration",
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()}}
+    ops = 7.0 * float(edge_iters.sum())  # eq: EP, E_j = 7 G per iteration
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle
+        cores = oracle.num_threads()
+        frames_s = max(2, min(cores, 16))
+        b, dt, okc = oracle_sample(cfg, codes_l, frames_s)
+        cpu = {"value": b / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{frames_s} frames x N_R={n} of {cfg.name} (quantise+syndromes+reconcile), "
+                         f"{dt:.1f} s wall, {okc} ok"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {m}-slice SR, N_R={n}, gamma={cfg.gamma} (SNR {10*np.log10(cfg.gamma):.1f} dB), "
+                               f"codes {[('disclosed' if c is None else f'R={c.rate:.3f}') for c in codes_l]}",
+                   "frames_per_gpu": F, "symbols_per_gpu": F * n, "max_iter": cfg.max_iter,
+                   "l2": "inputs and message arena > L2 (no flush needed)", "parallelism": f"frames sharded x{world}"},
+        "fer": fer, "beta": beta, "undetected_frames": int(undet),
+        "mean_iters": [float(iters_sum[j] / max(frames_all, 1)) for j in range(m)],
+        "symbols_per_s": frames_all * n / (ms_step * 1e-3),
+        "decoded_slice_bits_per_s": frames_all * n * sum(c is not None for c in codes_l) / (ms_step * 1e-3),
+        "paper_ops_per_s": ops / (ms_step * 1e-3),
+        "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+        "gpu_launches": int(launches),
+        "e2e": ({"value": bits_step / (tmax[1] / args.steps * 1e-3), "unit": UNIT,
+                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                 "ms_per_step": tmax[1] / args.steps} if e2e else None),
+        **extra,
+    }
+    print(json.dumps(line), flush=True)
+    pipe.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,212 @@
+/*
+ * cvsr.h -- C ABI of the B200-native sliced-reconciliation hot path
+ * (Ai & Malaney, arXiv 2108.08418; "PAPER.md" = the paper's text).
+ *
+ * The library (paper_2108_08418_b200/libcvsr.so, sm_100a) implements the
+ * data-parallel hot path named by BASELINE.json's north star and scoped by
+ * Gray-labelled constant-step quantisation (Bob), slice
+ * syndromes (Bob), per-slice LLRs conditioned on already-known slices
+ * (Alice), and syndrome-based flooding sum-product BP over many independent
+ * LDPC sub-blocks ("frames") with per-frame early termination.
+ *
+ * Conventions (apply to every entry point unless stated):
+ *  - Ownership.  Every data buffer argument is CALLER-OWNED DEVICE memory of
+ *    the context's device (e.g. a torch tensor's data_ptr()), except where a
+ *    parameter is documented "host".  The library owns only cvsr_ctx (stream
+ *    handle + a grow-only scratch arena) and cvsr_code (immutable after load).
+ *  - Asynchrony.  Calls validate their arguments on the host, enqueue kernels
+ *    on the context stream and return; outputs are valid after the stream
+ *    (or cvsr_ctx_sync) completes.  Entry points that fill a host struct
+ *    (cvsr_reconcile with stats_out != NULL, cvsr_count_errors) synchronise.
+ *  - Errors.  The return status is the only error channel.  Argument and
+ *    shape validation happens before any launch, so on a validation error
+ *    nothing is written.  Asynchronous CUDA faults are sticky and reported
+ *    as CVSR_ECUDA by the next call or by cvsr_ctx_sync.  Non-convergence of
+ *    a frame is never an error; it is reported through flags.
+ *    cvsr_last_error() returns a thread-local message for the last failure.
+ *  - Threading.  A cvsr_ctx is single-threaded.  A cvsr_code is read-only
+ *    and may be shared by contexts on the same device.
+ *  - Determinism.  Results are bit-identical for any batch size, frame order
+ *    and GPU count: no floating-point atomics on any path.
+ *  - Layouts.  "frame-major" arrays are [frames][n] row-major.  Packed bit
+ *    vectors put bit i at bit (i mod 32) of 32-bit word floor(i/32); a
+ *    vector of B bits occupies ceil(B/32) words per frame; padding bits are
+ *    0 on output and ignored on input.  Labels are uint8 Gray codes with bit
+ *    j = slice j and bit 0 the LSB (PAPER.md:114 footnote "the least
+ *    significant bit is l_0").
+ */
+#ifndef CVSR_H
+#define CVSR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CVSR_ABI_VERSION 1
+
+typedef int32_t cvsr_status;
+#define CVSR_OK 0
+#define CVSR_EINVAL (-1)  /* bad argument value / null pointer                 */
+#define CVSR_ESHAPE (-2)  /* inconsistent sizes                                */
+#define CVSR_ENOMEM (-3)  /* device or host allocation failed                  */
+#define CVSR_ECUDA  (-4)  /* CUDA runtime error (sticky for asynchronous faults)*/
+#define CVSR_ECODE  (-5)  /* malformed parity-check matrix                     */
+
+typedef struct cvsr_ctx cvsr_ctx;
+typedef struct cvsr_code cvsr_code;
+
+/* Thread-local message describing the last non-OK status ("" if none). */
+const char *cvsr_last_error(void);
+/* Returns CVSR_ABI_VERSION of the loaded library. */
+int32_t cvsr_abi_version(void);
+
+/* ------------------------------------------------------------- context */
+/* Create a context on CUDA device `device`; `cuda_stream` is a cudaStream_t
+ * (NULL = the legacy default stream).  The stream is borrowed, not owned. */
+cvsr_status cvsr_ctx_create(int32_t device, void *cuda_stream, cvsr_ctx **out);
+/* Re-point the context at another borrowed stream of the same device. */
+cvsr_status cvsr_ctx_set_stream(cvsr_ctx *ctx, void *cuda_stream);
+/* Wait for all work on the context stream; surfaces asynchronous faults. */
+cvsr_status cvsr_ctx_sync(cvsr_ctx *ctx);
+/* Number of kernels this context has launched so far (diagnostics/bench). */
+int64_t cvsr_ctx_launch_count(const cvsr_ctx *ctx);
+void cvsr_ctx_destroy(cvsr_ctx *ctx);
+/* Diagnostics: when enabled, the BP scheduler brackets its launches with CUDA
+ * events on the context stream, per kernel class: 0 = check-node pass (k_cn),
+ * 1 = variable-node pass (k_vn), 2 = initialisation (conditional LLR + first
+ * V2C write), 3 = control (status/retire).  cvsr_ctx_kernel_times
+ * synchronises, returns device milliseconds and launch counts per class in
+ * HOST arrays ms_out[4], launches_out[4], and resets the accumulators. */
+cvsr_status cvsr_ctx_set_profiling(cvsr_ctx *ctx, int32_t enable);
+cvsr_status cvsr_ctx_kernel_times(cvsr_ctx *ctx, double *ms_out, int64_t *launches_out);
+
+/* ------------------------------------------------------------- code H_j */
+/* Load a parity-check matrix H (n_checks x n_vars) given as HOST CSR by
+ * check: row_ptr[n_checks+1] (row_ptr[0] = 0, non-decreasing), col_idx[E]
+ * (0 <= col < n_vars, no duplicate within a row).  G = E non-zeros
+ * (PAPER.md:189).  The arrays are copied; the library builds the device
+ * CSR + CSC + edge-permutation layout (SURVEY.md §1 layer B1).
+ * Errors: CVSR_EINVAL (null/negative), CVSR_ECODE (malformed rows, empty
+ * variable columns are allowed), CVSR_ENOMEM, CVSR_ECUDA. */
+cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, const int32_t *row_ptr,
+                           const int32_t *col_idx, cvsr_code **out);
+/* host outputs; any may be NULL */
+cvsr_status cvsr_code_info(const cvsr_code *code, int32_t *n_vars, int32_t *n_checks, int64_t *n_edges);
+void cvsr_code_free(cvsr_code *code);
+
+/* ------------------------------------------------------------- Bob */
+/* Constant-step quantiser M(.) (PAPER.md:114 step 1): m in
+ * [1,8]; edges[0 .. 2^m-2] strictly ascending fp32 bin edges (reading A-3:
+ * integer multiples of the step, symmetric about 0; outer bins unbounded).
+ * Passed by host pointer. */
+typedef struct {
+    int32_t m;
+    float edges[255];
+} cvsr_quantiser;
+
+/* label[i] = g(b), b = #{k : y[i] >= edges[k]}, g(b) = b ^ (b >> 1) (Gray
+ * labelling).  Bit-exact (fp32 comparisons only; ties go to the
+ * upper bin).  y: float[count] (any layout), label_out: uint8[count].
+ * Inputs must be finite (NaN is undefined). */
+cvsr_status cvsr_quantise(cvsr_ctx *ctx, const cvsr_quantiser *q, const float *y, int64_t count,
+                          uint8_t *label_out);
+
+/* Slice S_j = bit j of each label (PAPER.md:114 step 2), packed:
+ * label uint8[frames][n] -> bits_out uint32[frames][ceil(n/32)]. */
+cvsr_status cvsr_slice_bits(cvsr_ctx *ctx, const uint8_t *label, int32_t frames, int32_t n, int32_t slice_j,
+                            uint32_t *bits_out);
+
+/* Syndrome s_j = H_j S_j over GF(2) (PAPER.md:89, PAPER.md:114 steps 2-3):
+ * label uint8[frames][n_vars] -> synd_out uint32[frames][ceil(n_checks/32)]. */
+cvsr_status cvsr_syndrome(cvsr_ctx *ctx, const cvsr_code *code, const uint8_t *label, int32_t frames,
+                          int32_t slice_j, uint32_t *synd_out);
+
+/* ------------------------------------------------------------- Alice: LLR */
+/* Conditional LLR of slice j (PAPER.md:114 step 4; reading A-2):
+ * L = clamp(ln N_0 - ln N_1, +-llr_max), N_beta = sum of Gaussian bin
+ * probabilities P_b(x) = Phi((e_{b+1}-x)/sigma_n) - Phi((e_b-x)/sigma_n) over
+ * bins whose Gray label agrees with known_label on known_mask and has bit j =
+ * beta.  Positive L means bit 0.  Evaluated in the log domain (fp32).
+ * x float[frames][n]; known_label uint8[frames][n] (may be NULL iff
+ * known_mask == 0; bit j of known_mask must be 0); llr_out float[frames][n]. */
+cvsr_status cvsr_llr_slice(cvsr_ctx *ctx, const cvsr_quantiser *q, const float *x, int32_t frames, int32_t n,
+                           float sigma_n, int32_t slice_j, uint32_t known_mask, const uint8_t *known_label,
+                           float llr_max, float *llr_out);
+
+/* BI-AWGN channel LLR (config C1, reading A-16): llr = clamp(2y/sigma2). */
+cvsr_status cvsr_llr_biawgn(cvsr_ctx *ctx, const float *y, int64_t count, float sigma2, float llr_max,
+                            float *llr_out);
+
+/* ------------------------------------------------------------- Alice: BP */
+/* max_iter >= 0 (reading A-9); msg_clamp = Q_MAX > 0, the V2C clamp
+ * (reading A-10, 40); flags reserved (0). */
+typedef struct {
+    int32_t max_iter;
+    float msg_clamp;
+    int32_t flags;
+} cvsr_decode_opts;
+
+/* Syndrome-based flooding sum-product BP (
+ * SURVEY.md §8(c) O5) of `frames` independent sub-blocks sharing code H:
+ *  k = 0 decision xhat = [L < 0]; iterations k = 1..max_iter of
+ *  CN r_e = (1-2 s_c) BOXPLUS_{e' != e} q_e', VN post = L + sum r,
+ *  q_e = clamp(post - r_e), xhat = [post < 0]; a frame stops at the first k
+ *  with H xhat = s (converged, iters = k) else iters = max_iter, converged = 0.
+ * llr float[frames][n_vars]; synd uint32[frames][ceil(n_checks/32)];
+ * bits_out uint32[frames][ceil(n_vars/32)]; converged_out uint8[frames];
+ * iters_out int32[frames]. */
+cvsr_status cvsr_decode(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, const uint32_t *synd,
+                        int32_t frames, const cvsr_decode_opts *opts, uint32_t *bits_out, uint8_t *converged_out,
+                        int32_t *iters_out);
+
+/* Parity/debug: exactly k_iters >= 1 iterations, no early stop; c2v_out
+ * float[frames][E] = C2V messages r_e of iteration k in CSR edge order,
+ * post_out float[frames][n_vars] = posteriors of iteration k.  Either output
+ * may be NULL. */
+cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, const uint32_t *synd,
+                              int32_t frames, int32_t k_iters, float msg_clamp, float *c2v_out, float *post_out);
+
+/* ------------------------------------------------------------- scheduler */
+/* Per-run statistics (host struct).  Slice arrays are indexed by slice j. */
+typedef struct {
+    int64_t frames;           /* frames processed                                     */
+    int64_t frames_ok;        /* frames whose every coded slice converged             */
+    int64_t bits_reconciled;  /* m * n per ok frame                     */
+    int64_t attempted[8];     /* frames that reached slice j                          */
+    int64_t converged[8];     /* frames whose slice j converged (disclosed: attempted)*/
+    int64_t iters_sum[8];     /* sum of BP iterations D_j over attempted frames       */
+    int64_t edge_iters[8];    /* sum over attempted frames of E_j * D_j               */
+    double alice_seconds;     /* device time of the call (CUDA events)                */
+} cvsr_stats;
+
+/* Multi-stage sliced reconciliation, Alice's side (PAPER.md:114 steps 4-6,
+ * Fig. 3), for `frames` sub-blocks of n symbols.
+ *  m in [1,8]; codes: HOST array of m code pointers, codes[j] == NULL means
+ *  slice j is disclosed (synd[j] then holds Bob's packed slice bits);
+ *  order: HOST int32[m], a permutation of 0..m-1 (decode order);
+ *  q: quantiser; sigma_n: noise std (reading A-5/A-18); x float[frames][n];
+ *  synd: HOST array of m DEVICE pointers, synd[j] uint32[frames][ceil(M_j/32)]
+ *  (or [frames][ceil(n/32)] for a disclosed slice);
+ *  opts: BP options (llr clamp is fixed at msg_clamp as well, reading A-11);
+ *  outputs: label_out uint8[frames][n] (Alice's labels: bits of attempted
+ *  slices), frame_ok uint8[frames], iters int32[frames][m] (D_j; 0 for a
+ *  disclosed slice; -1 if not attempted because an earlier slice failed,
+ *  reading A-13).  stats_out: optional HOST struct; if non-NULL the call
+ *  synchronises and fills it. */
+cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *codes, const int32_t *order,
+                           const cvsr_quantiser *q, float sigma_n, const float *x, const uint32_t *const *synd,
+                           int32_t frames, int32_t n, const cvsr_decode_opts *opts, uint8_t *label_out,
+                           uint8_t *frame_ok, int32_t *iters, cvsr_stats *stats_out);
+
+/* Simulation-only check against Bob's labels (both uint8[frames][n]):
+ * counts_out HOST int64[3] = {frames ok, ok frames whose labels differ from
+ * Bob's (undetected errors), differing label bytes over ok frames}.  Syncs. */
+cvsr_status cvsr_count_errors(cvsr_ctx *ctx, const uint8_t *label_alice, const uint8_t *label_bob,
+                              const uint8_t *frame_ok, int32_t frames, int32_t n, int64_t *counts_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CVSR_H */

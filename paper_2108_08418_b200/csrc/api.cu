@@ -1,0 +1,706 @@
+// C ABI of the cvsr library (include/cvsr.h): validation, contexts, code
+// layout (B1), the BP iteration scheduler (B3) and the multi-stage slice
+// driver (PAPER.md:114 steps 4-6).
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace cvsr;
+
+namespace {
+
+thread_local std::string g_err;
+
+cvsr_status fail(cvsr_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CK(call)                                                                                      \
+    do {                                                                                              \
+        cudaError_t e_ = (call);                                                                      \
+        if (e_ != cudaSuccess) return fail(CVSR_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));      \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = (cudaSetDevice(dev) == cudaSuccess);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+constexpr int RING = 8;
+constexpr int LOOKAHEAD = 3;
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// bump allocator over the scratch arena
+struct Carve {
+    char *base;
+    size_t off = 0;
+    template <typename P>
+    P *take(size_t bytes) {
+        P *p = reinterpret_cast<P *>(base + off);
+        off += align_up(bytes);
+        return p;
+    }
+};
+
+}  // namespace
+
+struct cvsr_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    void *scratch = nullptr;
+    size_t scratch_cap = 0;
+    int32_t *host_counts = nullptr;      // mapped pinned: [n_act, n_ret, lanes, epoch]
+    int32_t *host_counts_dev = nullptr;  // device alias of host_counts
+    int32_t epoch = 0;
+    cudaEvent_t ring[RING] = {};
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    unsigned long long *acc = nullptr;   // device accumulators for stats [32]
+    int64_t launches = 0;
+    // optional per-kernel-class timing (CUDA events around launches)
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<int, size_t>> prof;  // (class, index of start event; stop = index + 1)
+};
+
+struct cvsr_code {
+    int device = 0;
+    CodeDev d{};
+    void *mem = nullptr;
+};
+
+namespace {
+
+// kernel classes for cvsr_ctx_kernel_times
+enum { KC_CN = 0, KC_VN = 1, KC_INIT = 2, KC_CTRL = 3, KC_N = 4 };
+
+void prof_begin(cvsr_ctx *ctx, int cls) {
+    if (!ctx->profiling) return;
+    while (ctx->ev_pool.size() < ctx->ev_used + 2) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            ctx->profiling = false;
+            return;
+        }
+        ctx->ev_pool.push_back(e);
+    }
+    ctx->prof.push_back({cls, ctx->ev_used});
+    cudaEventRecord(ctx->ev_pool[ctx->ev_used], ctx->stream);
+    ctx->ev_used += 2;
+}
+
+void prof_end(cvsr_ctx *ctx) {
+    if (!ctx->profiling || ctx->prof.empty()) return;
+    cudaEventRecord(ctx->ev_pool[ctx->prof.back().second + 1], ctx->stream);
+}
+
+cvsr_status check_launch(cvsr_ctx *ctx, int n_launched) {
+    ctx->launches += n_launched;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(CVSR_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return CVSR_OK;
+}
+
+cvsr_status scratch_reserve(cvsr_ctx *ctx, size_t bytes, char **out) {
+    if (bytes > ctx->scratch_cap) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->scratch) CK(cudaFree(ctx->scratch));
+        ctx->scratch = nullptr;
+        ctx->scratch_cap = 0;
+        cudaError_t e = cudaMalloc(&ctx->scratch, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(CVSR_ENOMEM, "scratch arena of %zu bytes: %s", bytes, cudaGetErrorString(e));
+        }
+        ctx->scratch_cap = bytes;
+    }
+    *out = static_cast<char *>(ctx->scratch);
+    return CVSR_OK;
+}
+
+size_t decstate_bytes(int tiles, int frames, int64_t n, int64_t M, int64_t E) {
+    size_t b = 0;
+    b += align_up((size_t)tiles * E * T * sizeof(float));
+    b += align_up((size_t)tiles * n * T * sizeof(float));
+    b += align_up((size_t)tiles * n * sizeof(uint32_t));
+    b += align_up((size_t)tiles * M * sizeof(uint32_t));
+    b += 5 * align_up((size_t)tiles * sizeof(uint32_t));
+    b += align_up(16 * sizeof(int32_t));
+    b += align_up((size_t)frames * sizeof(int32_t));
+    b += align_up((size_t)frames);
+    return b;
+}
+
+DecState carve_decstate(Carve &cv, int tiles, int frames, int64_t n, int64_t M, int64_t E, int32_t *iters_user,
+                        uint8_t *conv_user) {
+    DecState ds{};
+    ds.tiles = tiles;
+    ds.frames = frames;
+    ds.msg = cv.take<float>((size_t)tiles * E * T * sizeof(float));
+    ds.L = cv.take<float>((size_t)tiles * n * T * sizeof(float));
+    ds.hb = cv.take<uint32_t>((size_t)tiles * n * sizeof(uint32_t));
+    ds.st = cv.take<uint32_t>((size_t)tiles * M * sizeof(uint32_t));
+    ds.tile_active = cv.take<uint32_t>((size_t)tiles * sizeof(uint32_t));
+    ds.tile_unsat = cv.take<uint32_t>((size_t)tiles * sizeof(uint32_t));
+    ds.tile_newly = cv.take<uint32_t>((size_t)tiles * sizeof(uint32_t));
+    ds.active_list = cv.take<int32_t>((size_t)tiles * sizeof(int32_t));
+    ds.retire_list = cv.take<int32_t>((size_t)tiles * sizeof(int32_t));
+    ds.counts = cv.take<int32_t>(16 * sizeof(int32_t));
+    int32_t *it = cv.take<int32_t>((size_t)frames * sizeof(int32_t));
+    uint8_t *cvb = cv.take<uint8_t>((size_t)frames);
+    ds.iters = iters_user ? iters_user : it;
+    ds.conv = conv_user ? conv_user : cvb;
+    return ds;
+}
+
+// Flooding BP iterations with per-frame early termination (B3).  Expects
+// ds.L, ds.st, tile state and counts initialised.  Host control: iterations
+// are launched LOOKAHEAD ahead of a mapped-memory progress counter written by
+// the status kernel; the counter also bounds the grid's tile dimension.
+cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds, int max_iter, float qmax,
+                       uint32_t *bits_out) {
+    cudaStream_t s = ctx->stream;
+    const CodeDev &cd = code->d;
+    volatile int32_t *hc = ctx->host_counts;
+    const int32_t epoch = ++ctx->epoch;
+    (void)epoch;
+    // the mapped counter is only read after an event of THIS run completed;
+    // every status kernel of this run writes it, so stale values are impossible.
+    prof_begin(ctx, KC_INIT);
+    launch_vn(cd, ds, ds.tiles, qmax, true, nullptr, s);
+    prof_end(ctx);
+    int launched = 1;
+    int bound = ds.tiles;
+    for (int k = 1; k <= max_iter + 1; ++k) {
+        const int final_pass = (k == max_iter + 1);
+        prof_begin(ctx, KC_CN);
+        launch_cn(cd, ds, bound, qmax, final_pass, s);
+        prof_end(ctx);
+        prof_begin(ctx, KC_CTRL);
+        launch_status(ds, k, max_iter, final_pass, ctx->host_counts_dev, s);
+        launch_retire(ds, cd.n, bound, bits_out, s);
+        prof_end(ctx);
+        launched += 3;
+        if (!final_pass) {
+            prof_begin(ctx, KC_VN);
+            launch_vn(cd, ds, bound, qmax, false, nullptr, s);
+            prof_end(ctx);
+            launched += 1;
+        }
+        CK(cudaEventRecord(ctx->ring[k % RING], s));
+        if (k >= LOOKAHEAD && !final_pass) {
+            CK(cudaEventSynchronize(ctx->ring[(k - LOOKAHEAD + 1) % RING]));
+            const int32_t na = hc[0];
+            const int32_t lanes = hc[2];
+            if (lanes == 0) break;
+            bound = std::min(bound, std::max(na, 1));
+        }
+    }
+    return check_launch(ctx, launched);
+}
+
+cvsr_status check_ctx(cvsr_ctx *ctx) {
+    if (!ctx) return fail(CVSR_EINVAL, "null context");
+    return CVSR_OK;
+}
+
+cvsr_status check_quantiser(const cvsr_quantiser *q) {
+    if (!q) return fail(CVSR_EINVAL, "null quantiser");
+    if (q->m < 1 || q->m > 8) return fail(CVSR_EINVAL, "quantiser m=%d outside [1,8]", q->m);
+    const int ne = (1 << q->m) - 1;
+    for (int i = 0; i < ne; ++i) {
+        if (!(q->edges[i] == q->edges[i]) || q->edges[i] == INFINITY || q->edges[i] == -INFINITY)
+            return fail(CVSR_EINVAL, "quantiser edge %d not finite", i);
+        if (i > 0 && !(q->edges[i] > q->edges[i - 1]))
+            return fail(CVSR_EINVAL, "quantiser edges not strictly ascending at %d", i);
+    }
+    return CVSR_OK;
+}
+
+}  // namespace
+
+// =================================================================== ABI
+
+extern "C" {
+
+const char *cvsr_last_error(void) { return g_err.c_str(); }
+
+int32_t cvsr_abi_version(void) { return CVSR_ABI_VERSION; }
+
+cvsr_status cvsr_ctx_create(int32_t device, void *cuda_stream, cvsr_ctx **out) {
+    if (!out) return fail(CVSR_EINVAL, "null out");
+    *out = nullptr;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(CVSR_EINVAL, "device %d not in [0,%d)", device, ndev);
+    DeviceGuard g(device);
+    if (!g.ok) return fail(CVSR_ECUDA, "cudaSetDevice(%d) failed", device);
+    cvsr_ctx *c = new cvsr_ctx();
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void **>(&c->host_counts), 16 * sizeof(int32_t),
+                                  cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->host_counts_dev), c->host_counts, 0);
+    for (int i = 0; i < RING && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&c->ring[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->t0);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->t1);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&c->acc), 32 * sizeof(unsigned long long));
+    if (e != cudaSuccess) {
+        cvsr_ctx_destroy(c);
+        return fail(CVSR_ECUDA, "context setup: %s", cudaGetErrorString(e));
+    }
+    memset(c->host_counts, 0, 16 * sizeof(int32_t));
+    *out = c;
+    return CVSR_OK;
+}
+
+cvsr_status cvsr_ctx_set_stream(cvsr_ctx *ctx, void *cuda_stream) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+    return CVSR_OK;
+}
+
+cvsr_status cvsr_ctx_sync(cvsr_ctx *ctx) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    DeviceGuard g(ctx->device);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    return CVSR_OK;
+}
+
+int64_t cvsr_ctx_launch_count(const cvsr_ctx *ctx) { return ctx ? ctx->launches : -1; }
+
+cvsr_status cvsr_ctx_set_profiling(cvsr_ctx *ctx, int32_t enable) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    ctx->profiling = enable != 0;
+    return CVSR_OK;
+}
+
+cvsr_status cvsr_ctx_kernel_times(cvsr_ctx *ctx, double *ms_out, int64_t *launches_out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (!ms_out || !launches_out) return fail(CVSR_EINVAL, "null output");
+    DeviceGuard g(ctx->device);
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int c = 0; c < KC_N; ++c) {
+        ms_out[c] = 0.0;
+        launches_out[c] = 0;
+    }
+    for (const auto &pr : ctx->prof) {
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev_pool[pr.second], ctx->ev_pool[pr.second + 1]));
+        ms_out[pr.first] += ms;
+        launches_out[pr.first] += 1;
+    }
+    ctx->prof.clear();
+    ctx->ev_used = 0;
+    return CVSR_OK;
+}
+
+void cvsr_ctx_destroy(cvsr_ctx *ctx) {
+    if (!ctx) return;
+    DeviceGuard g(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    else cudaDeviceSynchronize();
+    if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->host_counts) cudaFreeHost(ctx->host_counts);
+    for (int i = 0; i < RING; ++i)
+        if (ctx->ring[i]) cudaEventDestroy(ctx->ring[i]);
+    if (ctx->t0) cudaEventDestroy(ctx->t0);
+    if (ctx->t1) cudaEventDestroy(ctx->t1);
+    if (ctx->acc) cudaFree(ctx->acc);
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    delete ctx;
+}
+
+cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, const int32_t *row_ptr,
+                           const int32_t *col_idx, cvsr_code **out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (!out || !row_ptr || (!col_idx && n_checks > 0)) return fail(CVSR_EINVAL, "null argument");
+    *out = nullptr;
+    if (n_vars <= 0 || n_checks <= 0) return fail(CVSR_EINVAL, "n_vars=%d n_checks=%d must be > 0", n_vars, n_checks);
+    if (row_ptr[0] != 0) return fail(CVSR_ECODE, "row_ptr[0] = %d != 0", row_ptr[0]);
+    for (int32_t c = 0; c < n_checks; ++c)
+        if (row_ptr[c + 1] < row_ptr[c]) return fail(CVSR_ECODE, "row_ptr decreasing at %d", c);
+    const int64_t E = row_ptr[n_checks];
+    if (E <= 0) return fail(CVSR_ECODE, "matrix has no edges");
+    std::vector<int32_t> col_cnt(n_vars + 1, 0);
+    std::vector<int32_t> mark(n_vars, -1);
+    int32_t max_dc = 0;
+    for (int32_t c = 0; c < n_checks; ++c) {
+        max_dc = std::max(max_dc, row_ptr[c + 1] - row_ptr[c]);
+        for (int32_t e = row_ptr[c]; e < row_ptr[c + 1]; ++e) {
+            const int32_t v = col_idx[e];
+            if (v < 0 || v >= n_vars) return fail(CVSR_ECODE, "col_idx[%d] = %d out of range", e, v);
+            if (mark[v] == c) return fail(CVSR_ECODE, "duplicate column %d in row %d", v, c);
+            mark[v] = c;
+            col_cnt[v + 1]++;
+        }
+    }
+    // CSC by variable with the CSR position of each entry (edge permutation)
+    std::vector<int32_t> col_ptr(n_vars + 1, 0);
+    int32_t max_dv = 0;
+    for (int32_t v = 0; v < n_vars; ++v) {
+        col_ptr[v + 1] = col_ptr[v] + col_cnt[v + 1];
+        max_dv = std::max(max_dv, col_cnt[v + 1]);
+    }
+    std::vector<int32_t> fill(col_ptr.begin(), col_ptr.end() - 1);
+    std::vector<int32_t> csc_slot((size_t)E);
+    for (int32_t c = 0; c < n_checks; ++c)
+        for (int32_t e = row_ptr[c]; e < row_ptr[c + 1]; ++e) csc_slot[fill[col_idx[e]]++] = e;
+
+    DeviceGuard g(ctx->device);
+    cvsr_code *code = new cvsr_code();
+    code->device = ctx->device;
+    const size_t b_rp = align_up((size_t)(n_checks + 1) * 4), b_ci = align_up((size_t)E * 4);
+    const size_t b_cp = align_up((size_t)(n_vars + 1) * 4), b_cs = align_up((size_t)E * 4);
+    cudaError_t e = cudaMalloc(&code->mem, b_rp + b_ci + b_cp + b_cs);
+    if (e != cudaSuccess) {
+        delete code;
+        cudaGetLastError();
+        return fail(CVSR_ENOMEM, "code arrays: %s", cudaGetErrorString(e));
+    }
+    char *base = static_cast<char *>(code->mem);
+    int32_t *d_rp = reinterpret_cast<int32_t *>(base);
+    int32_t *d_ci = reinterpret_cast<int32_t *>(base + b_rp);
+    int32_t *d_cp = reinterpret_cast<int32_t *>(base + b_rp + b_ci);
+    int32_t *d_cs = reinterpret_cast<int32_t *>(base + b_rp + b_ci + b_cp);
+    cudaError_t e1 = cudaMemcpy(d_rp, row_ptr, (size_t)(n_checks + 1) * 4, cudaMemcpyHostToDevice);
+    cudaError_t e2 = cudaMemcpy(d_ci, col_idx, (size_t)E * 4, cudaMemcpyHostToDevice);
+    cudaError_t e3 = cudaMemcpy(d_cp, col_ptr.data(), (size_t)(n_vars + 1) * 4, cudaMemcpyHostToDevice);
+    cudaError_t e4 = cudaMemcpy(d_cs, csc_slot.data(), (size_t)E * 4, cudaMemcpyHostToDevice);
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess) {
+        cudaFree(code->mem);
+        delete code;
+        return fail(CVSR_ECUDA, "code upload failed");
+    }
+    code->d = CodeDev{n_vars, n_checks, E, d_rp, d_ci, d_cp, d_cs, max_dc, max_dv};
+    *out = code;
+    return CVSR_OK;
+}
+
+cvsr_status cvsr_code_info(const cvsr_code *code, int32_t *n_vars, int32_t *n_checks, int64_t *n_edges) {
+    if (!code) return fail(CVSR_EINVAL, "null code");
+    if (n_vars) *n_vars = code->d.n;
+    if (n_checks) *n_checks = code->d.M;
+    if (n_edges) *n_edges = code->d.E;
+    return CVSR_OK;
+}
+
+void cvsr_code_free(cvsr_code *code) {
+    if (!code) return;
+    DeviceGuard g(code->device);
+    cudaDeviceSynchronize();
+    cudaFree(code->mem);
+    delete code;
+}
+
+cvsr_status cvsr_quantise(cvsr_ctx *ctx, const cvsr_quantiser *q, const float *y, int64_t count, uint8_t *label_out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (cvsr_status st = check_quantiser(q)) return st;
+    if (count < 0) return fail(CVSR_ESHAPE, "count < 0");
+    if (count == 0) return CVSR_OK;
+    if (!y || !label_out) return fail(CVSR_EINVAL, "null buffer");
+    DeviceGuard g(ctx->device);
+    launch_quantise(q->edges, q->m, y, count, label_out, ctx->stream);
+    return check_launch(ctx, 1);
+}
+
+cvsr_status cvsr_slice_bits(cvsr_ctx *ctx, const uint8_t *label, int32_t frames, int32_t n, int32_t slice_j,
+                            uint32_t *bits_out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (frames < 0 || n <= 0) return fail(CVSR_ESHAPE, "frames=%d n=%d", frames, n);
+    if (slice_j < 0 || slice_j > 7) return fail(CVSR_EINVAL, "slice_j=%d", slice_j);
+    if (frames == 0) return CVSR_OK;
+    if (!label || !bits_out) return fail(CVSR_EINVAL, "null buffer");
+    DeviceGuard g(ctx->device);
+    launch_slice_bits(label, frames, n, slice_j, bits_out, ctx->stream);
+    return check_launch(ctx, 1);
+}
+
+cvsr_status cvsr_syndrome(cvsr_ctx *ctx, const cvsr_code *code, const uint8_t *label, int32_t frames,
+                          int32_t slice_j, uint32_t *synd_out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (!code) return fail(CVSR_EINVAL, "null code");
+    if (code->device != ctx->device) return fail(CVSR_EINVAL, "code and context on different devices");
+    if (frames < 0) return fail(CVSR_ESHAPE, "frames < 0");
+    if (slice_j < 0 || slice_j > 7) return fail(CVSR_EINVAL, "slice_j=%d", slice_j);
+    if (frames == 0) return CVSR_OK;
+    if (!label || !synd_out) return fail(CVSR_EINVAL, "null buffer");
+    DeviceGuard g(ctx->device);
+    launch_syndrome(code->d, label, frames, slice_j, synd_out, ctx->stream);
+    return check_launch(ctx, 1);
+}
+
+static void fill_llr_params(LlrParams &p, const cvsr_quantiser *q, int j, uint32_t mask, float sigma_n, float llr_max) {
+    memset(&p, 0, sizeof(p));
+    p.m = q->m;
+    p.j = j;
+    p.known_mask = mask;
+    p.sigma_n = sigma_n;
+    p.inv_sigma = 1.0f / sigma_n;
+    p.llr_max = llr_max;
+    for (int i = 0; i < (1 << q->m) - 1; ++i) p.edges[i] = q->edges[i];
+}
+
+cvsr_status cvsr_llr_slice(cvsr_ctx *ctx, const cvsr_quantiser *q, const float *x, int32_t frames, int32_t n,
+                           float sigma_n, int32_t slice_j, uint32_t known_mask, const uint8_t *known_label,
+                           float llr_max, float *llr_out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (cvsr_status st = check_quantiser(q)) return st;
+    if (frames < 0 || n <= 0) return fail(CVSR_ESHAPE, "frames=%d n=%d", frames, n);
+    if (slice_j < 0 || slice_j >= q->m) return fail(CVSR_EINVAL, "slice_j=%d not in [0,m)", slice_j);
+    if ((known_mask >> slice_j) & 1u) return fail(CVSR_EINVAL, "known_mask contains slice_j");
+    if (known_mask >> q->m) return fail(CVSR_EINVAL, "known_mask has bits >= m");
+    if (known_mask && !known_label) return fail(CVSR_EINVAL, "known_label required when known_mask != 0");
+    if (!(sigma_n > 0.0f) || !(llr_max > 0.0f)) return fail(CVSR_EINVAL, "sigma_n and llr_max must be > 0");
+    if (frames == 0) return CVSR_OK;
+    if (!x || !llr_out) return fail(CVSR_EINVAL, "null buffer");
+    DeviceGuard g(ctx->device);
+    LlrParams p;
+    fill_llr_params(p, q, slice_j, known_mask, sigma_n, llr_max);
+    launch_llr_slice(p, x, known_label, frames, n, llr_out, ctx->stream);
+    return check_launch(ctx, 1);
+}
+
+cvsr_status cvsr_llr_biawgn(cvsr_ctx *ctx, const float *y, int64_t count, float sigma2, float llr_max,
+                            float *llr_out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (count < 0) return fail(CVSR_ESHAPE, "count < 0");
+    if (!(sigma2 > 0.0f) || !(llr_max > 0.0f)) return fail(CVSR_EINVAL, "sigma2 and llr_max must be > 0");
+    if (count == 0) return CVSR_OK;
+    if (!y || !llr_out) return fail(CVSR_EINVAL, "null buffer");
+    DeviceGuard g(ctx->device);
+    launch_llr_biawgn(y, count, sigma2, llr_max, llr_out, ctx->stream);
+    return check_launch(ctx, 1);
+}
+
+static cvsr_status check_opts(const cvsr_decode_opts *o) {
+    if (!o) return fail(CVSR_EINVAL, "null decode opts");
+    if (o->max_iter < 0 || o->max_iter > 1000000) return fail(CVSR_EINVAL, "max_iter=%d", o->max_iter);
+    if (!(o->msg_clamp > 0.0f)) return fail(CVSR_EINVAL, "msg_clamp must be > 0");
+    return CVSR_OK;
+}
+
+cvsr_status cvsr_decode(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, const uint32_t *synd,
+                        int32_t frames, const cvsr_decode_opts *opts, uint32_t *bits_out, uint8_t *converged_out,
+                        int32_t *iters_out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (!code) return fail(CVSR_EINVAL, "null code");
+    if (code->device != ctx->device) return fail(CVSR_EINVAL, "code and context on different devices");
+    if (cvsr_status st = check_opts(opts)) return st;
+    if (frames < 0) return fail(CVSR_ESHAPE, "frames < 0");
+    if (frames == 0) return CVSR_OK;
+    if (!llr || !synd || !bits_out || !converged_out || !iters_out) return fail(CVSR_EINVAL, "null buffer");
+    DeviceGuard g(ctx->device);
+    const CodeDev &cd = code->d;
+    const int tiles = (frames + T - 1) / T;
+    char *base;
+    if (cvsr_status st = scratch_reserve(ctx, decstate_bytes(tiles, frames, cd.n, cd.M, cd.E), &base)) return st;
+    Carve cv{base};
+    DecState ds = carve_decstate(cv, tiles, frames, cd.n, cd.M, cd.E, iters_out, converged_out);
+    cudaStream_t s = ctx->stream;
+    launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, s);
+    launch_synd_transpose(synd, frames, cd.M, ds.st, tiles, s);
+    launch_init_tiles(ds, nullptr, s);
+    launch_set_counts(ds, tiles, s);
+    if (cvsr_status st = check_launch(ctx, 4)) return st;
+    return run_decode(ctx, code, ds, opts->max_iter, opts->msg_clamp, bits_out);
+}
+
+cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, const uint32_t *synd,
+                              int32_t frames, int32_t k_iters, float msg_clamp, float *c2v_out, float *post_out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (!code) return fail(CVSR_EINVAL, "null code");
+    if (code->device != ctx->device) return fail(CVSR_EINVAL, "code and context on different devices");
+    if (k_iters < 1) return fail(CVSR_EINVAL, "k_iters must be >= 1");
+    if (!(msg_clamp > 0.0f)) return fail(CVSR_EINVAL, "msg_clamp must be > 0");
+    if (frames < 0) return fail(CVSR_ESHAPE, "frames < 0");
+    if (frames == 0) return CVSR_OK;
+    if (!llr || !synd) return fail(CVSR_EINVAL, "null buffer");
+    DeviceGuard g(ctx->device);
+    const CodeDev &cd = code->d;
+    const int tiles = (frames + T - 1) / T;
+    const size_t post_bytes = align_up((size_t)tiles * cd.n * T * sizeof(float));
+    char *base;
+    if (cvsr_status st = scratch_reserve(ctx, decstate_bytes(tiles, frames, cd.n, cd.M, cd.E) + post_bytes, &base))
+        return st;
+    Carve cv{base};
+    DecState ds = carve_decstate(cv, tiles, frames, cd.n, cd.M, cd.E, nullptr, nullptr);
+    float *post_il = cv.take<float>(post_bytes);
+    cudaStream_t s = ctx->stream;
+    launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, s);
+    launch_synd_transpose(synd, frames, cd.M, ds.st, tiles, s);
+    launch_init_tiles(ds, nullptr, s);
+    launch_set_counts(ds, tiles, s);
+    launch_vn(cd, ds, tiles, msg_clamp, true, nullptr, s);
+    int launched = 5;
+    for (int k = 1; k <= k_iters; ++k) {
+        launch_cn(cd, ds, tiles, msg_clamp, 0, s);
+        ++launched;
+        if (k == k_iters && c2v_out) {
+            launch_from_interleaved(ds.msg, c2v_out, frames, cd.E, tiles, s);
+            ++launched;
+        }
+        launch_vn(cd, ds, tiles, msg_clamp, false, (k == k_iters) ? post_il : nullptr, s);
+        ++launched;
+    }
+    if (post_out) {
+        launch_from_interleaved(post_il, post_out, frames, cd.n, tiles, s);
+        ++launched;
+    }
+    return check_launch(ctx, launched);
+}
+
+cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *codes, const int32_t *order,
+                           const cvsr_quantiser *q, float sigma_n, const float *x, const uint32_t *const *synd,
+                           int32_t frames, int32_t n, const cvsr_decode_opts *opts, uint8_t *label_out,
+                           uint8_t *frame_ok, int32_t *iters, cvsr_stats *stats_out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (cvsr_status st = check_quantiser(q)) return st;
+    if (cvsr_status st = check_opts(opts)) return st;
+    if (m < 1 || m > 8 || m != q->m) return fail(CVSR_EINVAL, "m=%d must be in [1,8] and equal quantiser m", m);
+    if (!codes || !order || !synd) return fail(CVSR_EINVAL, "null codes/order/synd array");
+    if (frames < 0 || n <= 0) return fail(CVSR_ESHAPE, "frames=%d n=%d", frames, n);
+    if (!(sigma_n > 0.0f)) return fail(CVSR_EINVAL, "sigma_n must be > 0");
+    uint32_t seen = 0u;
+    int64_t maxE = 1, maxM = 1;
+    for (int t = 0; t < m; ++t) {
+        const int j = order[t];
+        if (j < 0 || j >= m || ((seen >> j) & 1u)) return fail(CVSR_EINVAL, "order is not a permutation of 0..m-1");
+        seen |= 1u << j;
+    }
+    for (int j = 0; j < m; ++j) {
+        if (codes[j]) {
+            if (codes[j]->device != ctx->device) return fail(CVSR_EINVAL, "code %d on another device", j);
+            if (codes[j]->d.n != n) return fail(CVSR_ESHAPE, "code %d has n=%d, expected %d", j, codes[j]->d.n, n);
+            maxE = std::max<int64_t>(maxE, codes[j]->d.E);
+            maxM = std::max<int64_t>(maxM, codes[j]->d.M);
+        }
+        if (frames > 0 && !synd[j]) return fail(CVSR_EINVAL, "synd[%d] is null", j);
+    }
+    if (frames == 0) {
+        if (stats_out) memset(stats_out, 0, sizeof(*stats_out));
+        return CVSR_OK;
+    }
+    if (!x || !label_out || !frame_ok || !iters) return fail(CVSR_EINVAL, "null buffer");
+    DeviceGuard g(ctx->device);
+    const int tiles = (frames + T - 1) / T;
+    const int Wn = words_of(n);
+    size_t bytes = decstate_bytes(tiles, frames, n, maxM, maxE);
+    bytes += (size_t)m * align_up((size_t)frames * Wn * 4) + 3 * align_up((size_t)frames);
+    char *base;
+    if (cvsr_status st = scratch_reserve(ctx, bytes, &base)) return st;
+    Carve cv{base};
+    DecState ds = carve_decstate(cv, tiles, frames, n, maxM, maxE, nullptr, nullptr);
+    uint32_t *bits_dec[8] = {};
+    for (int j = 0; j < m; ++j) bits_dec[j] = cv.take<uint32_t>((size_t)frames * Wn * 4);
+    uint8_t *alive = cv.take<uint8_t>((size_t)frames);
+    uint8_t *attempt = cv.take<uint8_t>((size_t)2 * frames);
+    cudaStream_t s = ctx->stream;
+    CK(cudaEventRecord(ctx->t0, s));
+    launch_fill_i32(iters, (int64_t)frames * m, -1, s);
+    launch_fill_u8(alive, frames, 1, s);
+    launch_fill_u8(attempt, 2 * (int64_t)frames, 0, s);
+    int launched = 3;
+    const uint32_t *known_bits[8] = {};
+    uint32_t known_mask = 0u;
+    for (int t = 0; t < m; ++t) {
+        const int j = order[t];
+        if (!codes[j]) {
+            launch_slice_done(ds, m, j, 1, alive, attempt, iters, s);
+            ++launched;
+            known_bits[j] = synd[j];
+        } else {
+            const CodeDev &cd = codes[j]->d;
+            CK(cudaMemsetAsync(bits_dec[j], 0, (size_t)frames * Wn * 4, s));
+            launch_init_tiles(ds, alive, s);
+            launch_set_counts(ds, tiles, s);
+            launch_synd_transpose(synd[j], frames, cd.M, ds.st, tiles, s);
+            LlrParams p;
+            fill_llr_params(p, q, j, known_mask, sigma_n, opts->msg_clamp);
+            for (int jj = 0; jj < m; ++jj) p.known_bits[jj] = known_bits[jj];
+            prof_begin(ctx, KC_INIT);
+            launch_llr_interleaved(p, x, frames, n, tiles, ds.L, s);
+            prof_end(ctx);
+            launched += 4;
+            if (cvsr_status st = check_launch(ctx, 0)) return st;
+            if (cvsr_status st = run_decode(ctx, codes[j], ds, opts->max_iter, opts->msg_clamp, bits_dec[j]))
+                return st;
+            launch_slice_done(ds, m, j, 0, alive, attempt, iters, s);
+            ++launched;
+            known_bits[j] = bits_dec[j];
+        }
+        known_mask |= 1u << j;
+    }
+    launch_assemble(known_bits, m, attempt, frames, n, label_out, s);
+    CK(cudaMemcpyAsync(frame_ok, alive, (size_t)frames, cudaMemcpyDeviceToDevice, s));
+    ++launched;
+    CK(cudaEventRecord(ctx->t1, s));
+    if (cvsr_status st = check_launch(ctx, launched)) return st;
+    if (stats_out) {
+        CK(cudaMemsetAsync(ctx->acc, 0, 32 * sizeof(unsigned long long), s));
+        launch_frame_stats(alive, attempt, iters, frames, m, ctx->acc, s);
+        if (cvsr_status st = check_launch(ctx, 1)) return st;
+        unsigned long long acc[32];
+        CK(cudaMemcpyAsync(acc, ctx->acc, sizeof(acc), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        memset(stats_out, 0, sizeof(*stats_out));
+        stats_out->frames = frames;
+        stats_out->frames_ok = (int64_t)acc[0];
+        stats_out->bits_reconciled = (int64_t)acc[0] * m * (int64_t)n;
+        for (int j = 0; j < m; ++j) {
+            stats_out->attempted[j] = (int64_t)acc[1 + j];
+            stats_out->converged[j] = (int64_t)acc[9 + j];
+            stats_out->iters_sum[j] = (int64_t)acc[17 + j];
+            stats_out->edge_iters[j] = codes[j] ? (int64_t)acc[17 + j] * codes[j]->d.E : 0;
+        }
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, ctx->t0, ctx->t1));
+        stats_out->alice_seconds = ms * 1e-3;
+    }
+    return CVSR_OK;
+}
+
+cvsr_status cvsr_count_errors(cvsr_ctx *ctx, const uint8_t *label_alice, const uint8_t *label_bob,
+                              const uint8_t *frame_ok, int32_t frames, int32_t n, int64_t *counts_out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (!counts_out) return fail(CVSR_EINVAL, "null counts_out");
+    if (frames < 0 || n <= 0) return fail(CVSR_ESHAPE, "frames=%d n=%d", frames, n);
+    counts_out[0] = counts_out[1] = counts_out[2] = 0;
+    if (frames == 0) return CVSR_OK;
+    if (!label_alice || !label_bob || !frame_ok) return fail(CVSR_EINVAL, "null buffer");
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemsetAsync(ctx->acc, 0, 4 * sizeof(unsigned long long), s));
+    launch_count_errors(label_alice, label_bob, frame_ok, frames, n, ctx->acc, s);
+    if (cvsr_status st = check_launch(ctx, 1)) return st;
+    unsigned long long acc[4];
+    CK(cudaMemcpyAsync(acc, ctx->acc, sizeof(acc), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int i = 0; i < 3; ++i) counts_out[i] = (int64_t)acc[i];
+    return CVSR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// Internal definitions of the cvsr CUDA library (sm_100a).  Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cvsr.h"
+
+namespace cvsr {
+
+// Frames per tile: one warp lane per frame.  Edge messages of the T frames of
+// a tile are stored contiguously per edge ("frame-interleaved arena",
+// SURVEY.md §2.6 row 45), so a warp reads/writes one 128-byte line per edge.
+constexpr int T = 32;
+constexpr int WARPS_PER_BLOCK = 8;
+constexpr int BLOCK = 32 * WARPS_PER_BLOCK;
+
+// Device view of a loaded parity-check matrix (SURVEY.md §1 layer B1).
+struct CodeDev {
+    int32_t n;          // variables (N_R)
+    int32_t M;          // checks
+    int64_t E;          // edges (G)
+    const int32_t *row_ptr;   // [M+1]  CSR by check
+    const int32_t *col_idx;   // [E]    variable of each CSR edge
+    const int32_t *col_ptr;   // [n+1]  CSC by variable
+    const int32_t *csc_slot;  // [E]    CSR position of each CSC entry
+    int32_t max_dc, max_dv;
+};
+
+// Per-decode device state (lives in the context's scratch arena).
+struct DecState {
+    int32_t tiles;
+    int32_t frames;
+    float *msg;             // [tiles][E][T]  in-place V2C/C2V message per edge slot
+    float *L;               // [tiles][n][T]  channel LLR
+    uint32_t *hb;           // [tiles][n]     hard decisions, bit = lane
+    uint32_t *st;           // [tiles][M]     syndrome bits, bit = lane
+    uint32_t *tile_active;  // [tiles] lanes still iterating
+    uint32_t *tile_unsat;   // [tiles] lanes with >= 1 unsatisfied check in this CN pass
+    uint32_t *tile_newly;   // [tiles] lanes retired by the last status pass
+    int32_t *active_list;   // [tiles]
+    int32_t *retire_list;   // [tiles]
+    int32_t *counts;        // [4]: n_active, n_retire, total active lanes, pad
+    int32_t *iters;         // [frames] D of the current decode
+    uint8_t *conv;          // [frames]
+};
+
+// Conditional-LLR parameters for the reconcile LLR kernel.
+struct LlrParams {
+    int32_t m;
+    int32_t j;
+    uint32_t known_mask;
+    float sigma_n;
+    float inv_sigma;
+    float llr_max;
+    const uint32_t *known_bits[8];  // packed [F][Wn] per known slice (nullptr if unknown)
+    float edges[255];
+};
+
+__host__ __device__ inline int32_t words_of(int64_t bits) { return (int32_t)((bits + 31) / 32); }
+
+}  // namespace cvsr

@@ -1,0 +1,152 @@
+// Alice-side LLR kernels.
+//
+// Conditional LLR of slice j (PAPER.md:114 step 4; reading A-2), log domain:
+//   log P_b(x) from log Q(z) = ln(erfcx(z/sqrt2)/2) - z^2/2 (z >= 0),
+//                              log1p(-erfc(-z/sqrt2)/2)      (z < 0),
+//   bins entirely above (below) the mean use the upper (lower) tail,
+//   straddling bins use (erf(hi/sqrt2) + erf(-lo/sqrt2))/2 (no cancellation);
+//   ln N_beta = log-sum-exp over the admissible bins, which are enumerated
+//   directly (labels agreeing with the known bits), so every lane runs the
+//   same trip count 2^(m - |K|).
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cvsr {
+
+constexpr float RSQRT2 = 0.70710678118654752f;
+
+__device__ __forceinline__ float log_q(float z) {
+    if (z >= 0.0f) return logf(0.5f * erfcxf(z * RSQRT2)) - 0.5f * z * z;
+    return log1pf(-0.5f * erfcf(-z * RSQRT2));
+}
+
+// log(1 - e^d) for d < 0
+__device__ __forceinline__ float log1m_exp(float d) { return logf(-expm1f(d)); }
+
+__device__ __forceinline__ float log_bin(const float *se, int b, int nb, float x, float inv_sigma) {
+    const bool lo_inf = (b == 0), hi_inf = (b == nb - 1);
+    if (lo_inf && hi_inf) return 0.0f;
+    const float lo = lo_inf ? 0.0f : (se[b - 1] - x) * inv_sigma;
+    const float hi = hi_inf ? 0.0f : (se[b] - x) * inv_sigma;
+    if (lo_inf) return log_q(-hi);
+    if (hi_inf) return log_q(lo);
+    if (lo >= 0.0f) {
+        const float a = log_q(lo), c = log_q(hi);
+        return a + log1m_exp(c - a);
+    }
+    if (hi <= 0.0f) {
+        const float a = log_q(-hi), c = log_q(-lo);
+        return a + log1m_exp(c - a);
+    }
+    return logf(0.5f * (erff(hi * RSQRT2) + erff(-lo * RSQRT2)));
+}
+
+__device__ __forceinline__ float log_add(float a, float b) {
+    const float mx = fmaxf(a, b), mn = fminf(a, b);
+    if (mx == -INFINITY) return -INFINITY;
+    return mx + log1pf(expf(mn - mx));
+}
+
+__device__ __forceinline__ uint32_t gray_inv(uint32_t g) {
+    g ^= g >> 1;
+    g ^= g >> 2;
+    g ^= g >> 4;
+    return g;
+}
+
+__device__ float llr_cond(const float *se, int m, int j, uint32_t kmask, uint32_t kappa, float x, float inv_sigma,
+                          float llr_max) {
+    const int nb = 1 << m;
+    const uint32_t free_mask = (uint32_t)(nb - 1) & ~kmask;
+    const uint32_t base = kappa & kmask;
+    float ln0 = -INFINITY, ln1 = -INFINITY;
+    uint32_t sub = 0u;
+    do {
+        const uint32_t g = base | sub;
+        const float lp = log_bin(se, (int)gray_inv(g), nb, x, inv_sigma);
+        if ((g >> j) & 1u) ln1 = log_add(ln1, lp);
+        else ln0 = log_add(ln0, lp);
+        sub = (sub - free_mask) & free_mask;
+    } while (sub);
+    if (ln0 == -INFINITY) return -llr_max;
+    if (ln1 == -INFINITY) return llr_max;
+    return fminf(fmaxf(ln0 - ln1, -llr_max), llr_max);
+}
+
+// public API: natural layout out[f][v]
+__global__ void k_llr_slice(LlrParams p, const float *__restrict__ x, const uint8_t *__restrict__ known_label,
+                            int64_t count, float *__restrict__ out) {
+    __shared__ float se[256];
+    for (int i = threadIdx.x; i < 255; i += blockDim.x) se[i] = p.edges[i];
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t kappa = p.known_mask ? known_label[i] : 0u;
+        out[i] = llr_cond(se, p.m, p.j, p.known_mask, kappa, x[i], p.inv_sigma, p.llr_max);
+    }
+}
+
+// decoder feed: conditional LLR written straight into the interleaved arena
+// L[t][v][lane] (fused transpose); known bits read from packed slices.
+__global__ void __launch_bounds__(256) k_llr_interleaved(LlrParams p, const float *__restrict__ x, int32_t F,
+                                                         int32_t n, float *__restrict__ L) {
+    __shared__ float se[256];
+    __shared__ float sm[32][33];
+    for (int i = threadIdx.x; i < 255; i += blockDim.x) se[i] = p.edges[i];
+    __syncthreads();
+    const int t = blockIdx.y;
+    const int v0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int Wn = words_of(n);
+    for (int fl = ty; fl < 32; fl += 8) {
+        const int f = t * T + fl;
+        const int v = v0 + tx;
+        float val = 0.0f;
+        if (f < F && v < n) {
+            uint32_t kappa = 0u;
+            if (p.known_mask) {
+                for (int jj = 0; jj < p.m; ++jj)
+                    if ((p.known_mask >> jj) & 1u)
+                        kappa |= ((p.known_bits[jj][(size_t)f * Wn + (v >> 5)] >> (v & 31)) & 1u) << jj;
+            }
+            val = llr_cond(se, p.m, p.j, p.known_mask, kappa, x[(size_t)f * n + v], p.inv_sigma, p.llr_max);
+        }
+        sm[fl][tx] = val;
+    }
+    __syncthreads();
+    for (int vl = ty; vl < 32; vl += 8) {
+        const int v = v0 + vl;
+        if (v < n) L[((size_t)t * n + v) * T + tx] = sm[tx][vl];
+    }
+}
+
+__global__ void k_llr_biawgn(const float *__restrict__ y, int64_t count, float sigma2, float llr_max,
+                             float *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = fminf(fmaxf(2.0f * y[i] / sigma2, -llr_max), llr_max);
+}
+
+static int grid_for(int64_t work, int block) {
+    int64_t g = (work + block - 1) / block;
+    if (g > 148 * 32) g = 148 * 32;
+    return (int)(g < 1 ? 1 : g);
+}
+
+void launch_llr_slice(const LlrParams &p, const float *x, const uint8_t *known_label, int32_t F, int32_t n,
+                      float *out, cudaStream_t s) {
+    const int64_t count = (int64_t)F * n;
+    k_llr_slice<<<grid_for(count, 256), 256, 0, s>>>(p, x, known_label, count, out);
+}
+
+void launch_llr_biawgn(const float *y, int64_t count, float sigma2, float llr_max, float *out, cudaStream_t s) {
+    k_llr_biawgn<<<grid_for(count, 256), 256, 0, s>>>(y, count, sigma2, llr_max, out);
+}
+
+void launch_llr_interleaved(const LlrParams &p, const float *x, int32_t F, int32_t n, int tiles, float *L,
+                            cudaStream_t s) {
+    dim3 grid((n + 31) / 32, tiles);
+    k_llr_interleaved<<<grid, 256, 0, s>>>(p, x, F, n, L);
+}
+
+}  // namespace cvsr

@@ -1,0 +1,83 @@
+"""One sliced-reconciliation step (Bob + Alice) composed from the C ABI.
+
+Argument marshalling and buffer ownership only: every step of the hot path
+runs in libcvsr.so kernels.  torch provides device memory and the stream.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import cvsr
+
+
+class SRPipeline:
+    """Device buffers + loaded codes for `frames` sub-blocks of n symbols.
+
+    codes[j] is a host code object with (n, m_checks, row_ptr, col_idx) or
+    None for a disclosed slice.  Bob: quantise y, syndromes of coded slices,
+    packed bits of disclosed slices.  Alice: cvsr_reconcile.
+    """
+
+    def __init__(self, m: int, edges, codes: Sequence, order: Sequence[int], sigma_n: float, n: int, frames: int,
+                 device: torch.device, max_iter: int = 100, msg_clamp: float = 40.0, stream=None):
+        self.m, self.n, self.frames, self.device = m, n, frames, device
+        self.order = list(order)
+        self.sigma_n = float(sigma_n)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        self.ctx = cvsr.cvsr_ctx_create(device.index or 0, self.stream)
+        self.q = cvsr.make_quantiser(edges)
+        self.opts = cvsr.decode_opts(max_iter, msg_clamp)
+        self.code_h: List[Optional[int]] = []
+        self.code_E: List[int] = []
+        for c in codes:
+            if c is None:
+                self.code_h.append(None)
+                self.code_E.append(0)
+            else:
+                if c.n != n:
+                    raise ValueError("code length != n")
+                self.code_h.append(cvsr.cvsr_code_load(self.ctx, c.n, c.m_checks, c.row_ptr, c.col_idx))
+                self.code_E.append(c.n_edges)
+        W = lambda bits: (bits + 31) // 32  # noqa: E731
+        kw = dict(device=device)
+        self.label_bob = torch.empty((frames, n), dtype=torch.uint8, **kw)
+        self.synd = [torch.empty((frames, W(c.m_checks) if c is not None else W(n)), dtype=torch.int32, **kw)
+                     for c in codes]
+        self.label_alice = torch.empty((frames, n), dtype=torch.uint8, **kw)
+        self.frame_ok = torch.empty((frames,), dtype=torch.uint8, **kw)
+        self.iters = torch.empty((frames, m), dtype=torch.int32, **kw)
+        self.codes = list(codes)
+
+    def bob(self, y: torch.Tensor) -> None:
+        cvsr.cvsr_quantise(self.ctx, self.q, y, self.frames * self.n, self.label_bob)
+        for j in range(self.m):
+            if self.code_h[j] is None:
+                cvsr.cvsr_slice_bits(self.ctx, self.label_bob, self.frames, self.n, j, self.synd[j])
+            else:
+                cvsr.cvsr_syndrome(self.ctx, self.code_h[j], self.label_bob, self.frames, j, self.synd[j])
+
+    def alice(self, x: torch.Tensor, want_stats: bool = False) -> Optional[dict]:
+        return cvsr.cvsr_reconcile(self.ctx, self.m, self.code_h, self.order, self.q, self.sigma_n, x, self.synd,
+                                   self.frames, self.n, self.opts, self.label_alice, self.frame_ok, self.iters,
+                                   want_stats=want_stats)
+
+    def step(self, x: torch.Tensor, y: torch.Tensor, want_stats: bool = False) -> Optional[dict]:
+        self.bob(y)
+        return self.alice(x, want_stats)
+
+    def count_errors(self):
+        return cvsr.cvsr_count_errors(self.ctx, self.label_alice, self.label_bob, self.frame_ok, self.frames, self.n)
+
+    def launches(self) -> int:
+        return cvsr.cvsr_ctx_launch_count(self.ctx)
+
+    def close(self) -> None:
+        if self.ctx:
+            cvsr.cvsr_ctx_sync(self.ctx)
+            for h in self.code_h:
+                if h:
+                    cvsr.cvsr_code_free(h)
+            cvsr.cvsr_ctx_destroy(self.ctx)
+            self.ctx = 0

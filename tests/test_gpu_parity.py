@@ -1,0 +1,350 @@
+"""CUDA path (libcvsr.so via the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Parity criteria (north star): quantiser labels, slice bits
+and syndromes bit-exact; LLRs and BP messages/posteriors within
+|gpu - ref| <= 1e-4 (|ref| + 1) (reading A-22); decoded bits identical on
+every frame where the oracle converges; FER inside the oracle's 95%
+Clopper-Pearson interval.
+"""
+import numpy as np
+import pytest
+import torch
+from scipy import stats
+
+import _brute
+import oracle
+from cvsr_inputs import awgn, codes, configs
+from cvsr_inputs.quantiser import edge_table
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def rel_err(a, ref):
+    return float(np.max(np.abs(np.asarray(a, np.float64) - ref) / (np.abs(ref) + 1.0))) if np.size(ref) else 0.0
+
+
+def dev(a):
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint32:
+        a = a.view(np.int32)
+    return torch.from_numpy(a).cuda()
+
+
+def host_u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+@pytest.fixture(scope="module")
+def cv(gpu):
+    from paper_2108_08418_b200 import cvsr
+    return cvsr
+
+
+@pytest.fixture(scope="module")
+def ctx(cv):
+    c = cv.cvsr_ctx_create(0, torch.cuda.current_stream())
+    yield c
+    cv.cvsr_ctx_destroy(c)
+
+
+def load(cv, ctx, code):
+    return cv.cvsr_code_load(ctx, code.n, code.m_checks, code.row_ptr, code.col_idx)
+
+
+def gpu_decode(cv, ctx, code, llr32, synd, max_iter=100):
+    F = llr32.shape[0]
+    h = load(cv, ctx, code)
+    bits = torch.empty((F, (code.n + 31) // 32), dtype=torch.int32, device="cuda")
+    conv = torch.empty(F, dtype=torch.uint8, device="cuda")
+    iters = torch.empty(F, dtype=torch.int32, device="cuda")
+    cv.cvsr_decode(ctx, h, dev(llr32), dev(synd), F, cv.decode_opts(max_iter, 40.0), bits, conv, iters)
+    cv.cvsr_ctx_sync(ctx)
+    cv.cvsr_code_free(h)
+    return host_u32(bits), conv.cpu().numpy(), iters.cpu().numpy()
+
+
+def gpu_trace(cv, ctx, code, llr32, synd, k):
+    F = llr32.shape[0]
+    h = load(cv, ctx, code)
+    c2v = torch.empty((F, code.n_edges), dtype=torch.float32, device="cuda")
+    post = torch.empty((F, code.n), dtype=torch.float32, device="cuda")
+    cv.cvsr_decode_trace(ctx, h, dev(llr32), dev(synd), F, k, 40.0, c2v, post)
+    cv.cvsr_ctx_sync(ctx)
+    cv.cvsr_code_free(h)
+    return c2v.cpu().numpy(), post.cpu().numpy()
+
+
+# ------------------------------------------------------------------ Bob side
+
+@pytest.mark.parametrize("m,delta", [(1, 0.0), (4, 0.44905), (5, 0.21359), (8, 0.013)])
+def test_quantise_bitexact(cv, ctx, m, delta):
+    e = edge_table(m, delta)
+    rng = np.random.default_rng(m)
+    y = np.concatenate([rng.normal(0, 3, 1_000_003), e, np.nextafter(e, np.float32(np.inf)),
+                        np.nextafter(e, np.float32(-np.inf)), [0.0, -0.0, 3e38, -3e38, 1e-45, -1e-45]]
+                       ).astype(np.float32)
+    ref = oracle.quantise(e, y)
+    yd = dev(y)
+    out = torch.empty(len(y), dtype=torch.uint8, device="cuda")
+    q = cv.make_quantiser(e)
+    cv.cvsr_quantise(ctx, q, yd, len(y), out)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    # unaligned views (scalar path) give the same labels
+    out2 = torch.empty(len(y) - 1, dtype=torch.uint8, device="cuda")
+    cv.cvsr_quantise(ctx, q, yd[1:], len(y) - 1, out2)
+    assert np.array_equal(out2.cpu().numpy(), ref[1:])
+
+
+CODES = {
+    "c1_36": lambda: codes.regular(1024, 3, 6, seed=1),
+    "irreg_ragged": lambda: codes.irregular_rate(4100, 0.406, seed=3),
+    "met": lambda: codes.met_low_rate(2000, 0.04, 0.02, 3, 6, seed=5),
+    "high_dc": lambda: codes.regular(1500, 3, 15, seed=2),
+}
+
+
+@pytest.mark.parametrize("name", list(CODES))
+def test_slice_bits_and_syndrome_bitexact(cv, ctx, name):
+    code = CODES[name]()
+    rng = np.random.default_rng(17)
+    F = 37
+    lab = rng.integers(0, 256, (F, code.n), dtype=np.uint8)
+    h = load(cv, ctx, code)
+    ld = dev(lab)
+    for j in (0, 2, 7):
+        s = torch.empty((F, (code.m_checks + 31) // 32), dtype=torch.int32, device="cuda")
+        cv.cvsr_syndrome(ctx, h, ld, F, j, s)
+        assert np.array_equal(host_u32(s), oracle.syndrome(code, lab, j))
+        b = torch.empty((F, (code.n + 31) // 32), dtype=torch.int32, device="cuda")
+        cv.cvsr_slice_bits(ctx, ld, F, code.n, j, b)
+        assert np.array_equal(host_u32(b), oracle.slice_bits(lab, j))
+    cv.cvsr_code_free(h)
+
+
+# ------------------------------------------------------------------ LLR
+
+@pytest.mark.parametrize("gamma,m,delta", [(2.214676, 5, 0.21359), (1.0, 4, 0.44905), (0.08, 1, 0.0)])
+def test_llr_slice_parity(cv, ctx, gamma, m, delta):
+    e = edge_table(m, delta)
+    sigma = float(1 / np.sqrt(gamma))
+    F, n = 5, 4001
+    x, y = awgn.quadratures(F, n, gamma, seed=31)
+    x[0, :50] *= 4.0  # tails
+    lab_bob = oracle.quantise(e, y)
+    rng = np.random.default_rng(5)
+    wrong = lab_bob ^ (rng.random(lab_bob.shape) < 0.1).astype(np.uint8) * rng.integers(0, 2 ** m, lab_bob.shape, dtype=np.uint8)
+    q = cv.make_quantiser(e)
+    xd = dev(x)
+    full = (1 << m) - 1
+    worst = 0.0
+    for j in range(m):
+        for mask, kl in ((0, None), (((1 << j) - 1), lab_bob), (full & ~(1 << j), lab_bob),
+                         (full & ~(1 << j), wrong)):
+            ref = oracle.llr_slice(e, sigma, x, j, mask, kl)
+            out = torch.empty((F, n), dtype=torch.float32, device="cuda")
+            cv.cvsr_llr_slice(ctx, q, xd, F, n, sigma, j, mask, dev(kl) if mask else None, 40.0, out)
+            worst = max(worst, rel_err(out.cpu().numpy(), ref))
+    assert worst <= TOL, worst
+
+
+def test_llr_biawgn_parity(cv, ctx):
+    sigma = awgn.biawgn_sigma(0.5, 1.5)
+    u, y = awgn.biawgn(3, 1000, sigma, seed=1)
+    out = torch.empty(y.shape, dtype=torch.float32, device="cuda")
+    cv.cvsr_llr_biawgn(ctx, dev(y), y.size, sigma ** 2, 40.0, out)
+    assert rel_err(out.cpu().numpy(), oracle.llr_biawgn(y, sigma ** 2)) <= 1e-6
+
+
+# ------------------------------------------------------------------ BP messages
+
+def _channel(code, F, ebn0, seed):
+    sigma = awgn.biawgn_sigma(max(code.rate, 0.02), ebn0)
+    u, y = awgn.biawgn(F, code.n, sigma, seed=seed)
+    llr = np.clip(2.0 * y.astype(np.float64) / sigma ** 2, -40, 40).astype(np.float32)
+    return u, llr, oracle.syndrome(code, u, 0)
+
+
+@pytest.mark.parametrize("name", list(CODES))
+def test_trace_messages_parity(cv, ctx, name):
+    code = CODES[name]()
+    ebn0 = {"met": -1.0}.get(name, 1.5)
+    F = 45  # two tiles, ragged
+    u, llr, synd = _channel(code, F, ebn0, seed=7)
+    for k in (1, 2, 5, 10):
+        c2v_ref, post_ref = oracle.bp_trace(code, llr.astype(np.float64), synd, k)
+        c2v, post = gpu_trace(cv, ctx, code, llr, synd, k)
+        assert rel_err(c2v, c2v_ref) <= TOL, (k, rel_err(c2v, c2v_ref))
+        assert rel_err(post, post_ref) <= TOL, (k, rel_err(post, post_ref))
+
+
+def test_tree_exact_marginals_gpu(cv, ctx):
+    rng = np.random.default_rng(12)
+    for trial in range(25):
+        H = _brute.random_tree_code(rng, int(rng.integers(2, 6)), 4)
+        if H.shape[1] > 16:
+            continue
+        code = codes.from_dense(H)
+        L = rng.normal(0, 3, (3, H.shape[1]))
+        u = rng.integers(0, 2, (3, H.shape[1]), dtype=np.uint8)
+        s = (u.astype(np.int64) @ H.T) % 2
+        _, post = gpu_trace(cv, ctx, code, L.astype(np.float32), _brute.pack_bits(s), 2 * H.shape[0] + 2)
+        for f in range(3):
+            ref = _brute.exact_marginal_llr(H, s[f], L[f].astype(np.float32).astype(np.float64))
+            assert rel_err(post[f], ref) <= TOL
+
+
+# ------------------------------------------------------------------ decode (C1)
+
+def _clopper_pearson(k, n, a=0.05):
+    lo = stats.beta.ppf(a / 2, k, n - k + 1) if k > 0 else 0.0
+    hi = stats.beta.ppf(1 - a / 2, k + 1, n - k) if k < n else 1.0
+    return lo, hi
+
+
+def test_decode_c1_parity(cv, ctx):
+    """C1: (3,6) n=1024, 100 frames, E_b/N_0 = 1.5 dB BI-AWGN (reading A-16)."""
+    c = configs.C1
+    code = codes.regular(c["n"], c["dv"], c["dc"], seed=configs.CODE_SEED)
+    sigma = awgn.biawgn_sigma(0.5, c["ebn0_db"])
+    u, y = awgn.biawgn(c["frames"], c["n"], sigma)
+    llr_d = torch.empty(y.shape, dtype=torch.float32, device="cuda")
+    cv.cvsr_llr_biawgn(ctx, dev(y), y.size, sigma ** 2, 40.0, llr_d)
+    llr = llr_d.cpu().numpy()
+    synd = oracle.syndrome(code, u, 0)
+    b_ref, c_ref, i_ref = oracle.bp_decode(code, llr.astype(np.float64), synd, c["max_iter"])
+    b, cg, it = gpu_decode(cv, ctx, code, llr, synd, c["max_iter"])
+    conv_ok = c_ref.astype(bool)
+    assert np.array_equal(b[conv_ok], b_ref[conv_ok])
+    assert np.sum(cg != c_ref) <= 2
+    assert np.sum(it[conv_ok] != i_ref[conv_ok]) <= 2
+    k_fail = int(np.sum(c_ref == 0))
+    lo, hi = _clopper_pearson(k_fail, len(c_ref))
+    assert lo <= float(np.mean(cg == 0)) <= hi
+    # converged => H xhat = s exactly; noiseless decoded bits match u
+    dec = _brute.unpack_bits(b, code.n)
+    s_dec = oracle.syndrome(code, dec, 0)
+    for f in range(len(cg)):
+        if cg[f]:
+            assert np.array_equal(s_dec[f], synd[f])
+
+
+def test_decode_determinism_and_batch_invariance(cv, ctx):
+    code = codes.regular(1024, 3, 6, seed=1)
+    u, llr, synd = _channel(code, 100, 1.5, seed=3)
+    a = gpu_decode(cv, ctx, code, llr, synd)
+    b = gpu_decode(cv, ctx, code, llr, synd)
+    sub = gpu_decode(cv, ctx, code, llr[37:90], synd[37:90])
+    perm = np.random.default_rng(1).permutation(100)
+    p = gpu_decode(cv, ctx, code, llr[perm], synd[perm])
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    for x, y in zip(a, sub):
+        assert np.array_equal(x[37:90], y)
+    for x, y in zip(a, p):
+        assert np.array_equal(x[perm], y)
+
+
+def test_decode_edge_cases(cv, ctx):
+    code = codes.regular(96, 3, 6, seed=4)
+    u, llr, synd = _channel(code, 33, 2.0, seed=9)
+    # max_iter = 0: decision of L only, D = 0 for satisfied frames
+    b, cg, it = gpu_decode(cv, ctx, code, llr, synd, max_iter=0)
+    b_ref, c_ref, i_ref = oracle.bp_decode(code, llr.astype(np.float64), synd, 0)
+    assert np.array_equal(b, b_ref) and np.array_equal(cg, c_ref) and np.array_equal(it, i_ref)
+    # noiseless: D = 0 everywhere
+    L0 = (40.0 * (1 - 2.0 * u)).astype(np.float32)
+    b, cg, it = gpu_decode(cv, ctx, code, L0, synd)
+    assert cg.all() and not it.any() and np.array_equal(_brute.unpack_bits(b, code.n), u)
+    # frames = 0 is a no-op
+    h = load(cv, ctx, code)
+    cv.cvsr_decode(ctx, h, None, None, 0, cv.decode_opts(), None, None, None)
+    # validation errors
+    with pytest.raises(cv.CvsrError) as ei:
+        cv.cvsr_decode(ctx, h, None, None, 1, cv.decode_opts(), None, None, None)
+    assert ei.value.status == cv.CVSR_EINVAL
+    cv.cvsr_code_free(h)
+    with pytest.raises(cv.CvsrError) as ei:
+        cv.cvsr_code_load(ctx, 4, 1, np.array([0, 2], np.int32), np.array([1, 1], np.int32))
+    assert ei.value.status == cv.CVSR_ECODE
+    bad = cv.make_quantiser(np.array([0.0, -1.0, 1.0], np.float32))
+    with pytest.raises(cv.CvsrError) as ei:
+        cv.cvsr_quantise(ctx, bad, 0, 1, 0)
+    assert ei.value.status == cv.CVSR_EINVAL
+
+
+# ------------------------------------------------------------------ reconcile
+
+def _run_reconcile(cv, cfg, codes_l, x, y, F, n, max_iter=100):
+    from paper_2108_08418_b200.pipeline import SRPipeline
+    pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, torch.device("cuda:0"),
+                      max_iter=max_iter)
+    stats_ = pipe.step(dev(x), dev(y), want_stats=True)
+    torch.cuda.synchronize()
+    out = dict(label=pipe.label_alice.cpu().numpy(), ok=pipe.frame_ok.cpu().numpy(), iters=pipe.iters.cpu().numpy(),
+               bob=pipe.label_bob.cpu().numpy(), synd=[host_u32(s) for s in pipe.synd], stats=stats_,
+               errors=pipe.count_errors())
+    pipe.close()
+    return out
+
+
+def test_reconcile_parity_c2_scaled(cv, ctx):
+    cfg = configs.scaled(configs.C2, 8192, 40)
+    codes_l = cfg.build_codes()
+    x, y = awgn.quadratures(cfg.frames, cfg.n, cfg.gamma, seed=11)
+    g = _run_reconcile(cv, cfg, codes_l, x, y, cfg.frames, cfg.n, cfg.max_iter)
+    lab_bob = oracle.quantise(cfg.edges(), y)
+    assert np.array_equal(g["bob"], lab_bob)
+    synd_ref = [oracle.slice_bits(lab_bob, j) if c is None else oracle.syndrome(c, lab_bob, j)
+                for j, c in enumerate(codes_l)]
+    for s_g, s_r in zip(g["synd"], synd_ref):
+        assert np.array_equal(s_g, s_r)
+    lab_ref, ok_ref, it_ref = oracle.reconcile(codes_l, cfg.order, cfg.edges(), cfg.sigma_n, x, synd_ref, cfg.max_iter)
+    both = ok_ref.astype(bool) & g["ok"].astype(bool)
+    assert np.array_equal(g["label"][both], lab_ref[both])
+    assert np.sum(g["ok"] != ok_ref) <= max(2, cfg.frames // 20)
+    assert np.sum(np.any(g["iters"][both] != it_ref[both], axis=1)) <= max(2, cfg.frames // 20)
+    st = g["stats"]
+    assert st["frames_ok"] == int(g["ok"].sum())
+    assert g["errors"][0] == st["frames_ok"]
+
+
+def test_reconcile_full_size_sampled(cv, ctx):
+    """C2 at full size (n = 2^16) in the bench launch configuration (2048 frames);
+    oracle on a sample of frames; properties on all frames."""
+    cfg = configs.C2
+    codes_l = cfg.build_codes()
+    F, n = cfg.frames, cfg.n
+    from cvsr_inputs.awgn import torch_quadratures
+    xd, yd = torch_quadratures(F, n, cfg.gamma, torch.device("cuda:0"))
+    from paper_2108_08418_b200.pipeline import SRPipeline
+    pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, torch.device("cuda:0"),
+                      max_iter=cfg.max_iter)
+    st = pipe.step(xd, yd, want_stats=True)
+    torch.cuda.synchronize()
+    ok = pipe.frame_ok.cpu().numpy()
+    assert st["frames_ok"] == int(ok.sum()) and st["frames"] == F
+    # every ok frame: Alice's labels reproduce Bob's syndromes exactly (converged => H xhat = s)
+    lab_a = pipe.label_alice
+    for j, c in enumerate(codes_l):
+        if c is None:
+            continue
+        s_a = torch.empty_like(pipe.synd[j])
+        cv.cvsr_syndrome(pipe.ctx, pipe.code_h[j], lab_a, F, j, s_a)
+        torch.cuda.synchronize()
+        eq = (s_a == pipe.synd[j]).all(dim=1).cpu().numpy()
+        assert eq[ok.astype(bool)].all()
+    # oracle on sampled frames
+    sample = np.array([0, 1, 777, F - 1])
+    x = xd[sample].cpu().numpy()
+    lab_bob = pipe.label_bob[sample].cpu().numpy()
+    synd = [host_u32(s[sample]) for s in pipe.synd]
+    lab_ref, ok_ref, it_ref = oracle.reconcile(codes_l, cfg.order, cfg.edges(), cfg.sigma_n, x, synd, cfg.max_iter)
+    lab_g = pipe.label_alice[sample].cpu().numpy()
+    ok_g = ok[sample]
+    both = ok_ref.astype(bool) & ok_g.astype(bool)
+    assert np.array_equal(lab_g[both], lab_ref[both])
+    assert np.sum(ok_g != ok_ref) <= 1
+    assert np.array_equal(lab_ref[ok_ref.astype(bool)], lab_bob[ok_ref.astype(bool)])
+    pipe.close()
