@@ -14,8 +14,9 @@
  * indices sorted ascending.  G (the paper's number of non-zeros)
  * equals E = row_ptr[M].
  *
+ * Degrees may be 0 (used when a structured part is merged in by the caller).
  * Error behaviour: returns 0 on success, -1 on bad arguments (degree sums
- * differ, degree < 1, degree > number of opposite nodes), -2 if duplicate
+ * differ, degree < 0, degree > number of opposite nodes), -2 if duplicate
  * repair did not converge within its attempt budget, -3 on allocation failure.
  */
 #include <stdint.h>
@@ -83,11 +84,11 @@ int ldpc_configuration_model(int32_t n_vars, int32_t n_checks,
         return -1;
     int64_t ev = 0, ec = 0;
     for (int32_t v = 0; v < n_vars; ++v) {
-        if (var_deg[v] < 1 || var_deg[v] > n_checks) return -1;
+        if (var_deg[v] < 0 || var_deg[v] > n_checks) return -1;
         ev += var_deg[v];
     }
     for (int32_t c = 0; c < n_checks; ++c) {
-        if (chk_deg[c] < 1 || chk_deg[c] > n_vars) return -1;
+        if (chk_deg[c] < 0 || chk_deg[c] > n_vars) return -1;
         ec += chk_deg[c];
     }
     if (ev != ec || ev > INT32_MAX) return -1;
