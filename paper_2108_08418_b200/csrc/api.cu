@@ -350,6 +350,8 @@ cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, cons
     int32_t max_dc = 0;
     for (int32_t c = 0; c < n_checks; ++c) {
         max_dc = std::max(max_dc, row_ptr[c + 1] - row_ptr[c]);
+        if (row_ptr[c + 1] - row_ptr[c] > MAX_DC)
+            return fail(CVSR_ECODE, "row %d has degree %d > %d (unsupported)", c, row_ptr[c + 1] - row_ptr[c], MAX_DC);
         for (int32_t e = row_ptr[c]; e < row_ptr[c + 1]; ++e) {
             const int32_t v = col_idx[e];
             if (v < 0 || v >= n_vars) return fail(CVSR_ECODE, "col_idx[%d] = %d out of range", e, v);
@@ -521,7 +523,7 @@ cvsr_status cvsr_decode(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, 
     Carve cv{base};
     DecState ds = carve_decstate(cv, tiles, frames, cd.n, cd.M, cd.E, iters_out, converged_out);
     cudaStream_t s = ctx->stream;
-    launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, s);
+    launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, LOG2E, s);
     launch_synd_transpose(synd, frames, cd.M, ds.st, tiles, s);
     launch_init_tiles(ds, nullptr, s);
     launch_set_counts(ds, tiles, s);
@@ -550,7 +552,7 @@ cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float 
     DecState ds = carve_decstate(cv, tiles, frames, cd.n, cd.M, cd.E, nullptr, nullptr);
     float *post_il = cv.take<float>(post_bytes);
     cudaStream_t s = ctx->stream;
-    launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, s);
+    launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, LOG2E, s);
     launch_synd_transpose(synd, frames, cd.M, ds.st, tiles, s);
     launch_init_tiles(ds, nullptr, s);
     launch_set_counts(ds, tiles, s);
@@ -560,14 +562,14 @@ cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float 
         launch_cn(cd, ds, tiles, msg_clamp, 0, s);
         ++launched;
         if (k == k_iters && c2v_out) {
-            launch_from_interleaved(ds.msg, c2v_out, frames, cd.E, tiles, s);
+            launch_from_interleaved(ds.msg, c2v_out, frames, cd.E, tiles, LN2, s);
             ++launched;
         }
         launch_vn(cd, ds, tiles, msg_clamp, false, (k == k_iters) ? post_il : nullptr, s);
         ++launched;
     }
     if (post_out) {
-        launch_from_interleaved(post_il, post_out, frames, cd.n, tiles, s);
+        launch_from_interleaved(post_il, post_out, frames, cd.n, tiles, LN2, s);
         ++launched;
     }
     return check_launch(ctx, launched);

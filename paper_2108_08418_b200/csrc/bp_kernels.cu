@@ -5,17 +5,23 @@
 // contiguous bytes, so each warp-level access is one fully-used 128-byte line.
 // Messages are stored IN PLACE: the CN pass reads V2C q_e and overwrites it
 // with C2V r_e; the VN pass reads r_e and overwrites it with the next q_e.
+// Arena values are in log2 units (LLR * log2 e): every exp/log below is then a
+// single MUFU ex2/lg2, and the conversion happens once at the arena boundary
+// (LLR load, trace dumps).  A warp processes one check (or variable) for TPW
+// tiles at once, so each warp has TPW x degree independent 128-byte requests
+// in flight.
 //
 // Algorithm (PAPER.md:189 BP decoder, PAPER.md:231 message passes; SURVEY.md
 // §8(c) O5 readings A-8 flooding, A-10 V2C clamp, A-12 stopping rule):
-//   CN: r_e = (1 - 2 s_c) * BOXPLUS_{e' != e} q_e'
-//       evaluated in the phi domain, phi(x) = -ln tanh(x/2) (self-inverse):
-//       |r_e| = phi( sum_{e' != e} phi(|q_e'|) ),  sign = prod of the other signs.
-//       The extrinsic sum is formed without "total minus own" cancellation:
-//       ext_e = S_ex                       for the edge of largest phi (argmax),
-//             = (S_ex - phi_e) + phi_max   otherwise,
-//       where S_ex = sum of all phi except the max (then ext_e >= S/2, so its
-//       relative error stays O(d_c eps)).
+//   CN: r_e = (1 - 2 s_c) * BOXPLUS_{e' != e} q_e'.  With t = tanh(|q|/2) the
+//       magnitude is 2 atanh(P_e), P_e = prod_{e' != e} t_e'.  It is evaluated
+//       through complements, which never cancel:
+//         w = 1 - t = 2u / (1 + u),  u = e^-|q|
+//         c_e = 1 - P_e = (+)_{e' != e} w_e',   a (+) b = a + b - ab  (prefix/suffix)
+//         |r_e| = ln((1 + P_e) / (1 - P_e)) = ln((2 - c_e) / c_e)
+//       (4 MUFU per edge; a zero message gives w = 1, c = 1, r = 0 exactly; a
+//       degree-1 check gives c = 0, |r| = +inf -> Q_MAX, the empty-fold rule).
+//       Sign = syndrome bit XOR the other edges' signs.
 //   VN: post_v = L_v + sum_e r_e ; q_e = clamp(post_v - r_e, +-Q_MAX);
 //       xhat_v = [post_v < 0].
 //   The syndrome test H xhat = s of iteration k-1 is fused into CN pass k.
@@ -25,210 +31,261 @@
 namespace cvsr {
 
 constexpr unsigned FULL = 0xffffffffu;
-// phi is evaluated at max(x, PHI_XMIN) so that phi <= 60 stays finite
-// (phi(2e^-60) = 60); an exact 0 message then yields |r| ~ 1e-26 on the
-// other edges instead of exactly 0 (far inside the 1e-4 parity tolerance).
-constexpr float PHI_XMIN = 1.7516230e-26f;
+constexpr int TPW = 4;  // tiles per warp
 
-// phi(x) = ln((1 + e^-x) / (1 - e^-x)) for x > 0, cancellation-safe:
-//  x >= 4      : 2 atanh(u) = 2u (1 + u^2/3 + u^4/5), u = e^-x   (no 1+tiny rounding)
-//  x <  0.375  : 1 - e^-x from its Taylor series (no 1 - u cancellation)
-__device__ __forceinline__ float phi_f(float x) {
-    x = fmaxf(x, PHI_XMIN);
-    const float u = __expf(-x);
-    const float u2 = u * u;
-    const float big = 2.0f * u * fmaf(u2, fmaf(u2, 0.2f, 0.33333334f), 1.0f);
-    const float dp = x * fmaf(-x, fmaf(-x, fmaf(-x, fmaf(-x, fmaf(-x, 1.0f / 720.0f, 1.0f / 120.0f),
-                                                        1.0f / 24.0f), 1.0f / 6.0f), 0.5f), 1.0f);
-    const float d = (x < 0.375f) ? dp : (1.0f - u);
-    const float small = __logf(__fdividef(1.0f + u, d));
-    return (x >= 4.0f) ? big : small;
+__device__ __forceinline__ float ex2f(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float lg2f(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcpf(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// a (+) b = 1 - (1 - a)(1 - b)
+__device__ __forceinline__ float cplus(float a, float b) { return fmaf(b, 1.0f - a, a); }
+__device__ __forceinline__ uint32_t sgnbit(float x) { return __float_as_uint(x) >> 31; }
+
+// q (log2 units) -> r (log2 units), in registers
+template <int DC>
+__device__ __forceinline__ void cn_update(float (&q)[DC], uint32_t sbit, float qmax2) {
+    float w[DC];
+    uint32_t par = sbit;
+#pragma unroll
+    for (int i = 0; i < DC; ++i) {
+        const float u = ex2f(-fabsf(q[i]));
+        w[i] = 2.0f * u * rcpf(1.0f + u);
+        par ^= sgnbit(q[i]);
+    }
+    float pre[DC];
+    pre[0] = 0.0f;
+#pragma unroll
+    for (int i = 1; i < DC; ++i) pre[i] = cplus(pre[i - 1], w[i - 1]);
+    float suf = 0.0f;
+#pragma unroll
+    for (int i = DC - 1; i >= 0; --i) {
+        const float c = cplus(pre[i], suf);
+        const float mag = fmaxf(fminf(lg2f((2.0f - c) * rcpf(c)), qmax2), 0.0f);
+        suf = cplus(suf, w[i]);
+        q[i] = (par ^ sgnbit(q[i])) ? -mag : mag;
+    }
+}
+
+struct TileSet {
+    int t[TPW];
+    uint32_t act[TPW];
+};
+
+__device__ __forceinline__ TileSet load_tiles(const DecState &ds, int g) {
+    TileSet ts;
+    const int cnt = ds.counts[0];
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+        const int idx = g * TPW + i;
+        const bool valid = idx < cnt;
+        ts.t[i] = valid ? ds.active_list[idx] : 0;
+        ts.act[i] = valid ? ds.tile_active[ts.t[i]] : 0u;
+    }
+    return ts;
 }
 
 template <int DC>
-__device__ __forceinline__ void cn_core(float *__restrict__ m, uint32_t sbit, float qmax) {
-    float q[DC], ph[DC];
+__device__ __forceinline__ void cn_tiles(const CodeDev &cd, const DecState &ds, const TileSet &ts, int beg,
+                                         const uint32_t (&s)[TPW], int lane, float qmax2) {
+    float q[TPW][DC];
+    float *base[TPW];
 #pragma unroll
-    for (int i = 0; i < DC; ++i) q[i] = m[(size_t)i * T];
-    uint32_t par = sbit;
+    for (int i = 0; i < TPW; ++i) {
+        base[i] = ds.msg + ((size_t)ts.t[i] * cd.E + beg) * T + lane;
+        const bool a = (ts.act[i] >> lane) & 1u;
 #pragma unroll
-    for (int i = 0; i < DC; ++i) {
-        ph[i] = phi_f(fabsf(q[i]));
-        par ^= __float_as_uint(q[i]) >> 31;
-    }
-    float pmax = ph[0], sex = 0.0f;
-    int amax = 0;
-#pragma unroll
-    for (int i = 1; i < DC; ++i) {
-        sex += fminf(ph[i], pmax);
-        amax = (ph[i] > pmax) ? i : amax;
-        pmax = fmaxf(ph[i], pmax);
+        for (int k = 0; k < DC; ++k) q[i][k] = a ? base[i][(size_t)k * T] : 0.0f;
     }
 #pragma unroll
-    for (int i = 0; i < DC; ++i) {
-        const float ext = (i == amax) ? sex : (sex - ph[i]) + pmax;
-        const float mag = fminf(phi_f(ext), qmax);
-        const uint32_t sg = par ^ (__float_as_uint(q[i]) >> 31);
-        m[(size_t)i * T] = sg ? -mag : mag;
+    for (int i = 0; i < TPW; ++i) {
+        if (!((ts.act[i] >> lane) & 1u)) continue;
+        cn_update<DC>(q[i], (s[i] >> lane) & 1u, qmax2);
+#pragma unroll
+        for (int k = 0; k < DC; ++k) base[i][(size_t)k * T] = q[i][k];
     }
 }
 
-// any degree: two passes, the second re-reads q (L1-resident) and recomputes phi
-__device__ __noinline__ void cn_generic(float *__restrict__ m, int deg, uint32_t sbit, float qmax) {
-    uint32_t par = sbit;
-    float pmax = -1.0f, sex = 0.0f;
-    int amax = 0;
-    for (int i = 0; i < deg; ++i) {
-        const float qi = m[(size_t)i * T];
-        const float p = phi_f(fabsf(qi));
-        par ^= __float_as_uint(qi) >> 31;
-        if (i == 0) {
-            pmax = p;
-        } else {
-            sex += fminf(p, pmax);
-            amax = (p > pmax) ? i : amax;
-            pmax = fmaxf(p, pmax);
+// any degree up to MAX_DC (checks above 12 are rare: none in the shipped ensembles);
+// w and suffix complements live in thread-local arrays.
+__device__ __noinline__ void cn_tiles_generic(const CodeDev cd, const DecState ds, const TileSet ts, int beg,
+                                              int deg, const uint32_t *s, int lane, float qmax2) {
+    float wl[MAX_DC], sf[MAX_DC + 1];
+    uint32_t sg[MAX_DC / 32];
+    for (int i = 0; i < TPW; ++i) {
+        if (!((ts.act[i] >> lane) & 1u)) continue;
+        float *m = ds.msg + ((size_t)ts.t[i] * cd.E + beg) * T + lane;
+        uint32_t par = (s[i] >> lane) & 1u;
+        for (int k = 0; k < MAX_DC / 32; ++k) sg[k] = 0u;
+        for (int k = 0; k < deg; ++k) {
+            const float qk = m[(size_t)k * T];
+            const uint32_t b = sgnbit(qk);
+            par ^= b;
+            sg[k >> 5] |= b << (k & 31);
+            const float u = ex2f(-fabsf(qk));
+            wl[k] = 2.0f * u * rcpf(1.0f + u);
+        }
+        sf[deg] = 0.0f;
+        for (int k = deg - 1; k >= 0; --k) sf[k] = cplus(sf[k + 1], wl[k]);
+        float pre = 0.0f;
+        for (int k = 0; k < deg; ++k) {
+            const float c = cplus(pre, sf[k + 1]);
+            const float mag = fmaxf(fminf(lg2f((2.0f - c) * rcpf(c)), qmax2), 0.0f);
+            m[(size_t)k * T] = (((sg[k >> 5] >> (k & 31)) & 1u) ^ par) ? -mag : mag;
+            pre = cplus(pre, wl[k]);
         }
     }
-    for (int i = 0; i < deg; ++i) {
-        const float qi = m[(size_t)i * T];
-        const float p = phi_f(fabsf(qi));
-        const float ext = (i == amax) ? sex : (sex - p) + pmax;
-        const float mag = fminf(phi_f(ext), qmax);
-        const uint32_t sg = par ^ (__float_as_uint(qi) >> 31);
-        m[(size_t)i * T] = sg ? -mag : mag;
-    }
 }
 
-__global__ void __launch_bounds__(BLOCK) k_cn(CodeDev cd, DecState ds, float qmax, int check_only) {
-    const int ti = blockIdx.y;
-    if (ti >= ds.counts[0]) return;
-    const int t = ds.active_list[ti];
-    const uint32_t active = ds.tile_active[t];
+__global__ void __launch_bounds__(BLOCK, 3) k_cn(CodeDev cd, DecState ds, float qmax2, int check_only) {
+    const int g = blockIdx.y;
+    if (g * TPW >= ds.counts[0]) return;
+    const TileSet ts = load_tiles(ds, g);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x * WARPS_PER_BLOCK + warp;
-    __shared__ uint32_t s_unsat;
-    if (threadIdx.x == 0) s_unsat = 0u;
+    __shared__ uint32_t s_unsat[TPW];
+    if (threadIdx.x < TPW) s_unsat[threadIdx.x] = 0u;
     __syncthreads();
     int beg = 0, deg = 0;
-    uint32_t s = 0u;
+    uint32_t s[TPW];
     if (c < cd.M) {
         beg = cd.row_ptr[c];
         deg = cd.row_ptr[c + 1] - beg;
-        s = ds.st[(size_t)t * cd.M + c];
         // fused syndrome test of decision k-1: lanes split the row's edges
-        const uint32_t *hbt = ds.hb + (size_t)t * cd.n;
-        uint32_t w = 0u;
+        uint32_t w[TPW];
+#pragma unroll
+        for (int i = 0; i < TPW; ++i) w[i] = 0u;
         for (int i0 = 0; i0 < deg; i0 += 32) {
-            const int i = i0 + lane;
-            w ^= (i < deg) ? hbt[cd.col_idx[beg + i]] : 0u;
+            const int e = i0 + lane;
+            const int v = (e < deg) ? cd.col_idx[beg + e] : 0;
+#pragma unroll
+            for (int i = 0; i < TPW; ++i)
+                if (e < deg && ts.act[i]) w[i] ^= ds.hb[(size_t)ts.t[i] * cd.n + v];
         }
-        const uint32_t p = s ^ __reduce_xor_sync(FULL, w);
-        const uint32_t u = p & active;
-        if (lane == 0 && u) atomicOr(&s_unsat, u);
+#pragma unroll
+        for (int i = 0; i < TPW; ++i) {
+            s[i] = ts.act[i] ? ds.st[(size_t)ts.t[i] * cd.M + c] : 0u;
+            const uint32_t u = (s[i] ^ __reduce_xor_sync(FULL, w[i])) & ts.act[i];
+            if (lane == 0 && u) atomicOr(&s_unsat[i], u);
+        }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && s_unsat) atomicOr(&ds.tile_unsat[t], s_unsat);
-    if (check_only || c >= cd.M || !((active >> lane) & 1u)) return;
-    float *m = ds.msg + ((size_t)t * cd.E + beg) * T + lane;
-    const uint32_t sbit = (s >> lane) & 1u;
+    if (threadIdx.x < TPW && s_unsat[threadIdx.x]) atomicOr(&ds.tile_unsat[ts.t[threadIdx.x]], s_unsat[threadIdx.x]);
+    if (check_only || c >= cd.M) return;
     switch (deg) {
-        case 1: cn_core<1>(m, sbit, qmax); break;
-        case 2: cn_core<2>(m, sbit, qmax); break;
-        case 3: cn_core<3>(m, sbit, qmax); break;
-        case 4: cn_core<4>(m, sbit, qmax); break;
-        case 5: cn_core<5>(m, sbit, qmax); break;
-        case 6: cn_core<6>(m, sbit, qmax); break;
-        case 7: cn_core<7>(m, sbit, qmax); break;
-        case 8: cn_core<8>(m, sbit, qmax); break;
-        case 9: cn_core<9>(m, sbit, qmax); break;
-        case 10: cn_core<10>(m, sbit, qmax); break;
-        case 11: cn_core<11>(m, sbit, qmax); break;
-        case 12: cn_core<12>(m, sbit, qmax); break;
-        default: cn_generic(m, deg, sbit, qmax); break;
+        case 1: cn_tiles<1>(cd, ds, ts, beg, s, lane, qmax2); break;
+        case 2: cn_tiles<2>(cd, ds, ts, beg, s, lane, qmax2); break;
+        case 3: cn_tiles<3>(cd, ds, ts, beg, s, lane, qmax2); break;
+        case 4: cn_tiles<4>(cd, ds, ts, beg, s, lane, qmax2); break;
+        case 5: cn_tiles<5>(cd, ds, ts, beg, s, lane, qmax2); break;
+        case 6: cn_tiles<6>(cd, ds, ts, beg, s, lane, qmax2); break;
+        case 7: cn_tiles<7>(cd, ds, ts, beg, s, lane, qmax2); break;
+        case 8: cn_tiles<8>(cd, ds, ts, beg, s, lane, qmax2); break;
+        case 9: cn_tiles<9>(cd, ds, ts, beg, s, lane, qmax2); break;
+        case 10: cn_tiles<10>(cd, ds, ts, beg, s, lane, qmax2); break;
+        default: cn_tiles_generic(cd, ds, ts, beg, deg, s, lane, qmax2); break;
     }
 }
 
 template <int DV, bool FIRST>
-__device__ __forceinline__ float vn_core(float *__restrict__ mt, int sl, float Lv, float qmax, bool act) {
-    if (FIRST) {
-        const float q = fminf(fmaxf(Lv, -qmax), qmax);
+__device__ __forceinline__ void vn_tiles(const CodeDev &cd, const DecState &ds, const TileSet &ts, int v, int sl,
+                                         int lane, float qmax2, float *post_dbg) {
+    int slot[DV > 0 ? DV : 1];
 #pragma unroll
-        for (int i = 0; i < DV; ++i) {
-            const int slot = __shfl_sync(FULL, sl, i);
-            if (act) mt[(size_t)slot * T] = q;
+    for (int k = 0; k < DV; ++k) slot[k] = __shfl_sync(FULL, sl, k);
+    float Lv[TPW];
+    float r[TPW][DV > 0 ? DV : 1];
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+        const bool a = (ts.act[i] >> lane) & 1u;
+        Lv[i] = a ? ds.L[((size_t)ts.t[i] * cd.n + v) * T + lane] : 0.0f;
+        if (!FIRST) {
+            const float *mt = ds.msg + (size_t)ts.t[i] * cd.E * T + lane;
+#pragma unroll
+            for (int k = 0; k < DV; ++k) r[i][k] = a ? mt[(size_t)slot[k] * T] : 0.0f;
         }
-        return Lv;
     }
-    int slot[DV];
-    float r[DV];
 #pragma unroll
-    for (int i = 0; i < DV; ++i) slot[i] = __shfl_sync(FULL, sl, i);
-    float post = Lv;
-    if (act) {
+    for (int i = 0; i < TPW; ++i) {
+        const bool a = (ts.act[i] >> lane) & 1u;
+        float post = Lv[i];
+        if (!FIRST) {
 #pragma unroll
-        for (int i = 0; i < DV; ++i) r[i] = mt[(size_t)slot[i] * T];
+            for (int k = 0; k < DV; ++k) post += r[i][k];
+        }
+        if (a) {
+            float *mt = ds.msg + (size_t)ts.t[i] * cd.E * T + lane;
 #pragma unroll
-        for (int i = 0; i < DV; ++i) post += r[i];
-#pragma unroll
-        for (int i = 0; i < DV; ++i) mt[(size_t)slot[i] * T] = fminf(fmaxf(post - r[i], -qmax), qmax);
+            for (int k = 0; k < DV; ++k)
+                mt[(size_t)slot[k] * T] = fminf(fmaxf(FIRST ? post : post - r[i][k], -qmax2), qmax2);
+            if (post_dbg) post_dbg[((size_t)ts.t[i] * cd.n + v) * T + lane] = post;
+        }
+        const uint32_t word = __ballot_sync(FULL, a && post < 0.0f);
+        if (lane == 0 && ts.act[i]) {
+            uint32_t *h = ds.hb + (size_t)ts.t[i] * cd.n + v;
+            *h = FIRST ? (word & ts.act[i]) : ((word & ts.act[i]) | (*h & ~ts.act[i]));
+        }
     }
-    return post;
 }
 
 template <bool FIRST>
-__device__ __noinline__ float vn_generic(float *__restrict__ mt, const int32_t *__restrict__ slots, int deg,
-                                         float Lv, float qmax, bool act) {
-    float post = Lv;
-    if (!act) return post;
-    if (FIRST) {
-        const float q = fminf(fmaxf(Lv, -qmax), qmax);
-        for (int i = 0; i < deg; ++i) mt[(size_t)slots[i] * T] = q;
-        return post;
+__device__ __noinline__ void vn_tiles_generic(const CodeDev cd, const DecState ds, const TileSet ts, int v,
+                                              int beg, int deg, int lane, float qmax2, float *post_dbg) {
+    const int32_t *slots = cd.csc_slot + beg;
+    for (int i = 0; i < TPW; ++i) {
+        const bool a = (ts.act[i] >> lane) & 1u;
+        float *mt = ds.msg + (size_t)ts.t[i] * cd.E * T + lane;
+        float post = a ? ds.L[((size_t)ts.t[i] * cd.n + v) * T + lane] : 0.0f;
+        if (a) {
+            if (!FIRST)
+                for (int k = 0; k < deg; ++k) post += mt[(size_t)slots[k] * T];
+            for (int k = 0; k < deg; ++k) {
+                float *p = mt + (size_t)slots[k] * T;
+                *p = fminf(fmaxf(FIRST ? post : post - *p, -qmax2), qmax2);
+            }
+            if (post_dbg) post_dbg[((size_t)ts.t[i] * cd.n + v) * T + lane] = post;
+        }
+        const uint32_t word = __ballot_sync(FULL, a && post < 0.0f);
+        if (lane == 0 && ts.act[i]) {
+            uint32_t *h = ds.hb + (size_t)ts.t[i] * cd.n + v;
+            *h = FIRST ? (word & ts.act[i]) : ((word & ts.act[i]) | (*h & ~ts.act[i]));
+        }
     }
-    for (int i = 0; i < deg; ++i) post += mt[(size_t)slots[i] * T];
-    for (int i = 0; i < deg; ++i) {
-        float *p = mt + (size_t)slots[i] * T;
-        *p = fminf(fmaxf(post - *p, -qmax), qmax);
-    }
-    return post;
 }
 
 template <bool FIRST>
-__global__ void __launch_bounds__(BLOCK) k_vn(CodeDev cd, DecState ds, float qmax, float *post_dbg) {
-    const int ti = blockIdx.y;
-    if (ti >= ds.counts[0]) return;
-    const int t = ds.active_list[ti];
-    const uint32_t active = ds.tile_active[t];
+__global__ void __launch_bounds__(BLOCK, 3) k_vn(CodeDev cd, DecState ds, float qmax2, float *post_dbg) {
+    const int g = blockIdx.y;
+    if (g * TPW >= ds.counts[0]) return;
+    const TileSet ts = load_tiles(ds, g);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int v = blockIdx.x * WARPS_PER_BLOCK + warp;
     if (v >= cd.n) return;
     const int beg = cd.col_ptr[v];
     const int deg = cd.col_ptr[v + 1] - beg;
-    const bool act = (active >> lane) & 1u;
-    const size_t lv = ((size_t)t * cd.n + v) * T + lane;
-    const float Lv = ds.L[lv];
-    float *mt = ds.msg + (size_t)t * cd.E * T + lane;
     const int sl = (lane < deg) ? cd.csc_slot[beg + lane] : 0;
-    float post;
     switch (deg) {
-        case 0: post = Lv; break;
-        case 1: post = vn_core<1, FIRST>(mt, sl, Lv, qmax, act); break;
-        case 2: post = vn_core<2, FIRST>(mt, sl, Lv, qmax, act); break;
-        case 3: post = vn_core<3, FIRST>(mt, sl, Lv, qmax, act); break;
-        case 4: post = vn_core<4, FIRST>(mt, sl, Lv, qmax, act); break;
-        case 5: post = vn_core<5, FIRST>(mt, sl, Lv, qmax, act); break;
-        case 6: post = vn_core<6, FIRST>(mt, sl, Lv, qmax, act); break;
-        case 7: post = vn_core<7, FIRST>(mt, sl, Lv, qmax, act); break;
-        case 8: post = vn_core<8, FIRST>(mt, sl, Lv, qmax, act); break;
-        default: post = vn_generic<FIRST>(mt, cd.csc_slot + beg, deg, Lv, qmax, act); break;
+        case 0: vn_tiles<0, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
+        case 1: vn_tiles<1, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
+        case 2: vn_tiles<2, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
+        case 3: vn_tiles<3, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
+        case 4: vn_tiles<4, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
+        case 5: vn_tiles<5, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
+        case 6: vn_tiles<6, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
+        case 7: vn_tiles<7, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
+        case 8: vn_tiles<8, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
+        default: vn_tiles_generic<FIRST>(cd, ds, ts, v, beg, deg, lane, qmax2, post_dbg); break;
     }
-    const uint32_t word = __ballot_sync(FULL, act && post < 0.0f);
-    if (lane == 0) {
-        uint32_t *h = ds.hb + (size_t)t * cd.n + v;
-        *h = FIRST ? (word & active) : ((word & active) | (*h & ~active));
-    }
-    if (post_dbg && act) post_dbg[lv] = post;
 }
 
 // Block-wide exclusive scan of 0/1 flags (blockDim.x multiple of 32, <= 1024).
@@ -349,7 +406,8 @@ __global__ void __launch_bounds__(BLOCK) k_retire(DecState ds, int32_t n, uint32
 }
 
 // natural [F][rows] -> interleaved [tiles][rows][T] (zero-fill missing frames)
-__global__ void k_to_interleaved(const float *__restrict__ src, float *__restrict__ dst, int32_t F, int64_t rows) {
+__global__ void k_to_interleaved(const float *__restrict__ src, float *__restrict__ dst, int32_t F, int64_t rows,
+                                 float scale) {
     __shared__ float sm[32][33];
     const int t = blockIdx.y;
     const int64_t r0 = (int64_t)blockIdx.x * 32;
@@ -357,7 +415,7 @@ __global__ void k_to_interleaved(const float *__restrict__ src, float *__restric
     for (int fl = ty; fl < 32; fl += 8) {
         const int f = t * T + fl;
         const int64_t r = r0 + tx;
-        sm[fl][tx] = (f < F && r < rows) ? src[(size_t)f * rows + r] : 0.0f;
+        sm[fl][tx] = (f < F && r < rows) ? src[(size_t)f * rows + r] * scale : 0.0f;
     }
     __syncthreads();
     for (int rl = ty; rl < 32; rl += 8) {
@@ -367,7 +425,8 @@ __global__ void k_to_interleaved(const float *__restrict__ src, float *__restric
 }
 
 // interleaved [tiles][rows][T] -> natural [F][rows]
-__global__ void k_from_interleaved(const float *__restrict__ src, float *__restrict__ dst, int32_t F, int64_t rows) {
+__global__ void k_from_interleaved(const float *__restrict__ src, float *__restrict__ dst, int32_t F, int64_t rows,
+                                   float scale) {
     __shared__ float sm[32][33];
     const int t = blockIdx.y;
     const int64_t r0 = (int64_t)blockIdx.x * 32;
@@ -380,7 +439,7 @@ __global__ void k_from_interleaved(const float *__restrict__ src, float *__restr
     for (int fl = ty; fl < 32; fl += 8) {
         const int f = t * T + fl;
         const int64_t r = r0 + tx;
-        if (f < F && r < rows) dst[(size_t)f * rows + r] = sm[tx][fl];
+        if (f < F && r < rows) dst[(size_t)f * rows + r] = sm[tx][fl] * scale;
     }
 }
 
@@ -429,18 +488,19 @@ __global__ void k_set_counts(DecState ds, int32_t n_active) {
 
 // ---------------------------------------------------------------- launchers
 
+// qmax is in natural LLR units; the arena works in log2 units
 void launch_cn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, int check_only, cudaStream_t s) {
     if (grid_tiles <= 0) return;
-    dim3 grid((cd.M + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, grid_tiles);
-    k_cn<<<grid, BLOCK, 0, s>>>(cd, ds, qmax, check_only);
+    dim3 grid((cd.M + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, (grid_tiles + TPW - 1) / TPW);
+    k_cn<<<grid, BLOCK, 0, s>>>(cd, ds, qmax * LOG2E, check_only);
 }
 
 void launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float *post_dbg,
                cudaStream_t s) {
     if (grid_tiles <= 0) return;
-    dim3 grid((cd.n + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, grid_tiles);
-    if (first) k_vn<true><<<grid, BLOCK, 0, s>>>(cd, ds, qmax, post_dbg);
-    else k_vn<false><<<grid, BLOCK, 0, s>>>(cd, ds, qmax, post_dbg);
+    dim3 grid((cd.n + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, (grid_tiles + TPW - 1) / TPW);
+    if (first) k_vn<true><<<grid, BLOCK, 0, s>>>(cd, ds, qmax * LOG2E, post_dbg);
+    else k_vn<false><<<grid, BLOCK, 0, s>>>(cd, ds, qmax * LOG2E, post_dbg);
 }
 
 void launch_status(const DecState &ds, int k, int max_iter, int final_pass, int32_t *host_counts, cudaStream_t s) {
@@ -453,14 +513,16 @@ void launch_retire(const DecState &ds, int32_t n, int grid_tiles, uint32_t *bits
     k_retire<<<grid, BLOCK, 0, s>>>(ds, n, bits_out);
 }
 
-void launch_to_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, cudaStream_t s) {
+void launch_to_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, float scale,
+                           cudaStream_t s) {
     dim3 grid((unsigned)((rows + 31) / 32), tiles);
-    k_to_interleaved<<<grid, 256, 0, s>>>(src, dst, F, rows);
+    k_to_interleaved<<<grid, 256, 0, s>>>(src, dst, F, rows, scale);
 }
 
-void launch_from_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, cudaStream_t s) {
+void launch_from_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, float scale,
+                             cudaStream_t s) {
     dim3 grid((unsigned)((rows + 31) / 32), tiles);
-    k_from_interleaved<<<grid, 256, 0, s>>>(src, dst, F, rows);
+    k_from_interleaved<<<grid, 256, 0, s>>>(src, dst, F, rows, scale);
 }
 
 void launch_synd_transpose(const uint32_t *synd, int32_t F, int32_t M, uint32_t *st, int tiles, cudaStream_t s) {

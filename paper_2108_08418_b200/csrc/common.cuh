@@ -14,6 +14,11 @@ namespace cvsr {
 constexpr int T = 32;
 constexpr int WARPS_PER_BLOCK = 8;
 constexpr int BLOCK = 32 * WARPS_PER_BLOCK;
+// largest check degree supported (cvsr_code_load rejects larger rows with CVSR_ECODE)
+constexpr int MAX_DC = 128;
+// arena values are LLR * log2(e)
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
 
 // Device view of a loaded parity-check matrix (SURVEY.md §1 layer B1).
 struct CodeDev {

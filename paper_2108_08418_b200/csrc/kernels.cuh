@@ -10,8 +10,10 @@ void launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax
                cudaStream_t s);
 void launch_status(const DecState &ds, int k, int max_iter, int final_pass, int32_t *host_counts, cudaStream_t s);
 void launch_retire(const DecState &ds, int32_t n, int grid_tiles, uint32_t *bits_out, cudaStream_t s);
-void launch_to_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, cudaStream_t s);
-void launch_from_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, cudaStream_t s);
+void launch_to_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, float scale,
+                           cudaStream_t s);
+void launch_from_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, float scale,
+                             cudaStream_t s);
 void launch_synd_transpose(const uint32_t *synd, int32_t F, int32_t M, uint32_t *st, int tiles, cudaStream_t s);
 void launch_init_tiles(const DecState &ds, const uint8_t *alive, cudaStream_t s);
 void launch_set_counts(const DecState &ds, int32_t n_active, cudaStream_t s);

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) k_llr_interleaved(LlrParams p, const floa
     __syncthreads();
     for (int vl = ty; vl < 32; vl += 8) {
         const int v = v0 + vl;
-        if (v < n) L[((size_t)t * n + v) * T + tx] = sm[tx][vl];
+        if (v < n) L[((size_t)t * n + v) * T + tx] = sm[tx][vl] * LOG2E;  // arena: log2 units
     }
 }
 
