@@ -144,9 +144,9 @@ size_t decstate_bytes(int tiles, int frames, int64_t n, int64_t M, int64_t E) {
     size_t b = 0;
     b += align_up((size_t)tiles * E * T * sizeof(float));
     b += align_up((size_t)tiles * n * T * sizeof(float));
-    b += align_up((size_t)tiles * n * sizeof(uint32_t));
-    b += align_up((size_t)tiles * M * sizeof(uint32_t));
-    b += 5 * align_up((size_t)tiles * sizeof(uint32_t));
+    b += align_up((size_t)tiles * n * sizeof(uint4));
+    b += align_up((size_t)tiles * M * sizeof(uint4));
+    b += 5 * align_up((size_t)tiles * sizeof(uint4));
     b += align_up(16 * sizeof(int32_t));
     b += align_up((size_t)frames * sizeof(int32_t));
     b += align_up((size_t)frames);
@@ -158,13 +158,13 @@ DecState carve_decstate(Carve &cv, int tiles, int frames, int64_t n, int64_t M, 
     DecState ds{};
     ds.tiles = tiles;
     ds.frames = frames;
-    ds.msg = cv.take<float>((size_t)tiles * E * T * sizeof(float));
-    ds.L = cv.take<float>((size_t)tiles * n * T * sizeof(float));
-    ds.hb = cv.take<uint32_t>((size_t)tiles * n * sizeof(uint32_t));
-    ds.st = cv.take<uint32_t>((size_t)tiles * M * sizeof(uint32_t));
-    ds.tile_active = cv.take<uint32_t>((size_t)tiles * sizeof(uint32_t));
-    ds.tile_unsat = cv.take<uint32_t>((size_t)tiles * sizeof(uint32_t));
-    ds.tile_newly = cv.take<uint32_t>((size_t)tiles * sizeof(uint32_t));
+    ds.msg = cv.take<float4>((size_t)tiles * E * T * sizeof(float));
+    ds.L = cv.take<float4>((size_t)tiles * n * T * sizeof(float));
+    ds.hb = cv.take<uint4>((size_t)tiles * n * sizeof(uint4));
+    ds.st = cv.take<uint4>((size_t)tiles * M * sizeof(uint4));
+    ds.tile_active = cv.take<uint4>((size_t)tiles * sizeof(uint4));
+    ds.tile_unsat = cv.take<uint4>((size_t)tiles * sizeof(uint4));
+    ds.tile_newly = cv.take<uint4>((size_t)tiles * sizeof(uint4));
     ds.active_list = cv.take<int32_t>((size_t)tiles * sizeof(int32_t));
     ds.retire_list = cv.take<int32_t>((size_t)tiles * sizeof(int32_t));
     ds.counts = cv.take<int32_t>(16 * sizeof(int32_t));
@@ -550,7 +550,7 @@ cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float 
         return st;
     Carve cv{base};
     DecState ds = carve_decstate(cv, tiles, frames, cd.n, cd.M, cd.E, nullptr, nullptr);
-    float *post_il = cv.take<float>(post_bytes);
+    float4 *post_il = cv.take<float4>(post_bytes);
     cudaStream_t s = ctx->stream;
     launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, LOG2E, s);
     launch_synd_transpose(synd, frames, cd.M, ds.st, tiles, s);

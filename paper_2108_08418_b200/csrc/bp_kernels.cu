@@ -1,15 +1,17 @@
 // Sum-product BP kernels for sm_100a.
 //
-// Layout ("frame-interleaved arena"): a tile holds T = 32 frames, one per warp
-// lane.  For every edge slot (CSR position) the 32 frames' messages are 128
-// contiguous bytes, so each warp-level access is one fully-used 128-byte line.
+// Layout ("frame-interleaved arena"): a tile holds T = 128 frames; lane l of a
+// warp owns frames {128 t + 32 s + l : s = 0..3} as one float4.  For every edge
+// slot (CSR position) the 128 frames' messages are 512 contiguous bytes, so a
+// warp moves one 512-byte line per edge with one 16-byte access per lane.
 // Messages are stored IN PLACE: the CN pass reads V2C q_e and overwrites it
 // with C2V r_e; the VN pass reads r_e and overwrites it with the next q_e.
 // Arena values are in log2 units (LLR * log2 e): every exp/log below is then a
-// single MUFU ex2/lg2, and the conversion happens once at the arena boundary
-// (LLR load, trace dumps).  A warp processes one check (or variable) for TPW
-// tiles at once, so each warp has TPW x degree independent 128-byte requests
-// in flight.
+// single MUFU ex2/lg2; conversion happens once at the arena boundary (LLR
+// load, trace dumps).  Each warp handles CPW consecutive checks (VPW
+// consecutive variables) so that one row_ptr/col_ptr load serves several
+// rows, and the syndrome test is reduced after the message pass so that its
+// gathers overlap the message traffic.
 //
 // Algorithm (PAPER.md:189 BP decoder, PAPER.md:231 message passes; SURVEY.md
 // §8(c) O5 readings A-8 flooding, A-10 V2C clamp, A-12 stopping rule):
@@ -31,7 +33,8 @@
 namespace cvsr {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int TPW = 4;  // tiles per warp
+constexpr int CPW = 4;  // checks per warp
+constexpr int VPW = 4;  // variables per warp
 
 __device__ __forceinline__ float ex2f(float x) {
     float y;
@@ -51,6 +54,21 @@ __device__ __forceinline__ float rcpf(float x) {
 // a (+) b = 1 - (1 - a)(1 - b)
 __device__ __forceinline__ float cplus(float a, float b) { return fmaf(b, 1.0f - a, a); }
 __device__ __forceinline__ uint32_t sgnbit(float x) { return __float_as_uint(x) >> 31; }
+
+__device__ __forceinline__ float cmp4(const float4 &v, int s) { return s == 0 ? v.x : s == 1 ? v.y : s == 2 ? v.z : v.w; }
+__device__ __forceinline__ void set4(float4 &v, int s, float x) {
+    if (s == 0) v.x = x;
+    else if (s == 1) v.y = x;
+    else if (s == 2) v.z = x;
+    else v.w = x;
+}
+__device__ __forceinline__ uint32_t cmpu(const uint4 &v, int s) { return s == 0 ? v.x : s == 1 ? v.y : s == 2 ? v.z : v.w; }
+__device__ __forceinline__ uint4 lanebits4(const uint4 &m, int lane) {
+    return make_uint4((m.x >> lane) & 1u, (m.y >> lane) & 1u, (m.z >> lane) & 1u, (m.w >> lane) & 1u);
+}
+__device__ __forceinline__ float clampf(float x, float lim) { return fminf(fmaxf(x, -lim), lim); }
+
+// ------------------------------------------------------------------ check nodes
 
 // q (log2 units) -> r (log2 units), in registers
 template <int DC>
@@ -77,61 +95,37 @@ __device__ __forceinline__ void cn_update(float (&q)[DC], uint32_t sbit, float q
     }
 }
 
-struct TileSet {
-    int t[TPW];
-    uint32_t act[TPW];
-};
-
-__device__ __forceinline__ TileSet load_tiles(const DecState &ds, int g) {
-    TileSet ts;
-    const int cnt = ds.counts[0];
-#pragma unroll
-    for (int i = 0; i < TPW; ++i) {
-        const int idx = g * TPW + i;
-        const bool valid = idx < cnt;
-        ts.t[i] = valid ? ds.active_list[idx] : 0;
-        ts.act[i] = valid ? ds.tile_active[ts.t[i]] : 0u;
-    }
-    return ts;
-}
-
+// one check, 4 frames per lane (al = this lane's active bit per sub-tile)
 template <int DC>
-__device__ __forceinline__ void cn_tiles(const CodeDev &cd, const DecState &ds, const TileSet &ts, int beg,
-                                         const uint32_t (&s)[TPW], int lane, float qmax2) {
-    float q[TPW][DC];
-    float *base[TPW];
+__device__ __forceinline__ void cn_check(float4 *__restrict__ m, const uint4 &sb, const uint4 &al, float qmax2) {
+    if (!(al.x | al.y | al.z | al.w)) return;
+    float4 q[DC];
 #pragma unroll
-    for (int i = 0; i < TPW; ++i) {
-        base[i] = ds.msg + ((size_t)ts.t[i] * cd.E + beg) * T + lane;
-        const bool a = (ts.act[i] >> lane) & 1u;
+    for (int k = 0; k < DC; ++k) q[k] = m[(size_t)k * LANES];
 #pragma unroll
-        for (int k = 0; k < DC; ++k) q[i][k] = a ? base[i][(size_t)k * T] : 0.0f;
+    for (int s = 0; s < SUBS; ++s) {
+        if (!cmpu(al, s)) continue;
+        float a[DC];
+#pragma unroll
+        for (int k = 0; k < DC; ++k) a[k] = cmp4(q[k], s);
+        cn_update<DC>(a, cmpu(sb, s), qmax2);
+#pragma unroll
+        for (int k = 0; k < DC; ++k) set4(q[k], s, a[k]);
     }
 #pragma unroll
-    for (int i = 0; i < TPW; ++i) {
-        if (!((ts.act[i] >> lane) & 1u)) continue;
-        cn_update<DC>(q[i], (s[i] >> lane) & 1u, qmax2);
-#pragma unroll
-        for (int k = 0; k < DC; ++k) base[i][(size_t)k * T] = q[i][k];
-    }
+    for (int k = 0; k < DC; ++k) m[(size_t)k * LANES] = q[k];
 }
 
-// any degree up to MAX_DC (checks above 12 are rare: none in the shipped ensembles);
-// w and suffix complements live in thread-local arrays.
-__device__ __noinline__ void cn_tiles_generic(const CodeDev cd, const DecState ds, const TileSet ts, int beg,
-                                              int deg, const uint32_t *s, int lane, float qmax2) {
+// any degree up to MAX_DC (rare): w and suffix complements in thread-local arrays
+__device__ __noinline__ void cn_check_generic(float4 *__restrict__ m, int deg, uint4 sb, uint4 al, float qmax2) {
     float wl[MAX_DC], sf[MAX_DC + 1];
-    uint32_t sg[MAX_DC / 32];
-    for (int i = 0; i < TPW; ++i) {
-        if (!((ts.act[i] >> lane) & 1u)) continue;
-        float *m = ds.msg + ((size_t)ts.t[i] * cd.E + beg) * T + lane;
-        uint32_t par = (s[i] >> lane) & 1u;
-        for (int k = 0; k < MAX_DC / 32; ++k) sg[k] = 0u;
+    float *mf = reinterpret_cast<float *>(m);
+    for (int s = 0; s < SUBS; ++s) {
+        if (!cmpu(al, s)) continue;
+        uint32_t par = cmpu(sb, s);
         for (int k = 0; k < deg; ++k) {
-            const float qk = m[(size_t)k * T];
-            const uint32_t b = sgnbit(qk);
-            par ^= b;
-            sg[k >> 5] |= b << (k & 31);
+            const float qk = mf[(size_t)k * LANES * 4 + s];
+            par ^= sgnbit(qk);
             const float u = ex2f(-fabsf(qk));
             wl[k] = 2.0f * u * rcpf(1.0f + u);
         }
@@ -139,154 +133,225 @@ __device__ __noinline__ void cn_tiles_generic(const CodeDev cd, const DecState d
         for (int k = deg - 1; k >= 0; --k) sf[k] = cplus(sf[k + 1], wl[k]);
         float pre = 0.0f;
         for (int k = 0; k < deg; ++k) {
+            float *p = mf + (size_t)k * LANES * 4 + s;
             const float c = cplus(pre, sf[k + 1]);
             const float mag = fmaxf(fminf(lg2f((2.0f - c) * rcpf(c)), qmax2), 0.0f);
-            m[(size_t)k * T] = (((sg[k >> 5] >> (k & 31)) & 1u) ^ par) ? -mag : mag;
             pre = cplus(pre, wl[k]);
+            *p = (par ^ sgnbit(*p)) ? -mag : mag;
         }
     }
 }
 
 __global__ void __launch_bounds__(BLOCK, 3) k_cn(CodeDev cd, DecState ds, float qmax2, int check_only) {
-    const int g = blockIdx.y;
-    if (g * TPW >= ds.counts[0]) return;
-    const TileSet ts = load_tiles(ds, g);
+    const int ti = blockIdx.y;
+    if (ti >= ds.counts[0]) return;
+    const int t = ds.active_list[ti];
+    const uint4 act = ds.tile_active[t];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = blockIdx.x * WARPS_PER_BLOCK + warp;
-    __shared__ uint32_t s_unsat[TPW];
-    if (threadIdx.x < TPW) s_unsat[threadIdx.x] = 0u;
+    __shared__ uint32_t s_unsat[SUBS];
+    __shared__ int s_done;
+    if (threadIdx.x < SUBS) s_unsat[threadIdx.x] = 0u;
+    if (threadIdx.x == 0) s_done = 0;
     __syncthreads();
-    int beg = 0, deg = 0;
-    uint32_t s[TPW];
-    if (c < cd.M) {
-        beg = cd.row_ptr[c];
-        deg = cd.row_ptr[c + 1] - beg;
-        // fused syndrome test of decision k-1: lanes split the row's edges
-        uint32_t w[TPW];
+    const int c0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * CPW;
+    const int nc = min(CPW, cd.M - c0);
+    if (nc > 0) {
+        const int rp = (lane <= nc) ? cd.row_ptr[c0 + lane] : 0;
+        int lo[CPW + 1];
 #pragma unroll
-        for (int i = 0; i < TPW; ++i) w[i] = 0u;
-        for (int i0 = 0; i0 < deg; i0 += 32) {
-            const int e = i0 + lane;
-            const int v = (e < deg) ? cd.col_idx[beg + e] : 0;
+        for (int i = 0; i <= CPW; ++i) lo[i] = __shfl_sync(FULL, rp, i <= nc ? i : nc);
+        const int ebeg = lo[0], eend = lo[nc];
+        // per-check parity accumulators, seeded with the syndrome bits s_c
+        uint4 par[CPW];
 #pragma unroll
-            for (int i = 0; i < TPW; ++i)
-                if (e < deg && ts.act[i]) w[i] ^= ds.hb[(size_t)ts.t[i] * cd.n + v];
+        for (int i = 0; i < CPW; ++i)
+            par[i] = (i < nc) ? ds.st[(size_t)t * cd.M + c0 + i] : make_uint4(0u, 0u, 0u, 0u);
+        // hard-decision word of this lane's edge (first 32 edges), issued before the message pass
+        const uint4 *hbt = ds.hb + (size_t)t * cd.n;
+        int e = ebeg + lane;
+        uint4 h = make_uint4(0u, 0u, 0u, 0u);
+        if (e < eend) h = hbt[cd.col_idx[e]];
+        if (!check_only) {
+            const uint4 al = lanebits4(act, lane);
+            float4 *mt = ds.msg + (size_t)t * cd.E * LANES + lane;
+#pragma unroll
+            for (int i = 0; i < CPW; ++i) {
+                if (i < nc) {
+                    const int deg = lo[i + 1] - lo[i];
+                    float4 *m = mt + (size_t)lo[i] * LANES;
+                    const uint4 sb = lanebits4(par[i], lane);
+                    switch (deg) {
+                        case 1: cn_check<1>(m, sb, al, qmax2); break;
+                        case 2: cn_check<2>(m, sb, al, qmax2); break;
+                        case 3: cn_check<3>(m, sb, al, qmax2); break;
+                        case 4: cn_check<4>(m, sb, al, qmax2); break;
+                        case 5: cn_check<5>(m, sb, al, qmax2); break;
+                        case 6: cn_check<6>(m, sb, al, qmax2); break;
+                        case 7: cn_check<7>(m, sb, al, qmax2); break;
+                        case 8: cn_check<8>(m, sb, al, qmax2); break;
+                        default: cn_check_generic(m, deg, sb, al, qmax2); break;
+                    }
+                }
+            }
         }
+        // syndrome test of decision k-1 (H xhat = s), chunks of 32 edges
+        for (int e0 = ebeg;;) {
 #pragma unroll
-        for (int i = 0; i < TPW; ++i) {
-            s[i] = ts.act[i] ? ds.st[(size_t)ts.t[i] * cd.M + c] : 0u;
-            const uint32_t u = (s[i] ^ __reduce_xor_sync(FULL, w[i])) & ts.act[i];
-            if (lane == 0 && u) atomicOr(&s_unsat[i], u);
+            for (int i = 0; i < CPW; ++i) {
+                const bool in = (i < nc) && e >= lo[i] && e < lo[i + 1];
+                par[i].x ^= __reduce_xor_sync(FULL, in ? h.x : 0u);
+                par[i].y ^= __reduce_xor_sync(FULL, in ? h.y : 0u);
+                par[i].z ^= __reduce_xor_sync(FULL, in ? h.z : 0u);
+                par[i].w ^= __reduce_xor_sync(FULL, in ? h.w : 0u);
+            }
+            e0 += 32;
+            if (e0 >= eend) break;
+            e = e0 + lane;
+            h = make_uint4(0u, 0u, 0u, 0u);
+            if (e < eend) h = hbt[cd.col_idx[e]];
+        }
+        uint4 u = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int i = 0; i < CPW; ++i) {
+            u.x |= par[i].x; u.y |= par[i].y; u.z |= par[i].z; u.w |= par[i].w;
+        }
+        u.x &= act.x; u.y &= act.y; u.z &= act.z; u.w &= act.w;
+        if (lane < SUBS) {
+            const uint32_t v = cmpu(u, lane);
+            if (v) atomicOr(&s_unsat[lane], v);
         }
     }
-    __syncthreads();
-    if (threadIdx.x < TPW && s_unsat[threadIdx.x]) atomicOr(&ds.tile_unsat[ts.t[threadIdx.x]], s_unsat[threadIdx.x]);
-    if (check_only || c >= cd.M) return;
-    switch (deg) {
-        case 1: cn_tiles<1>(cd, ds, ts, beg, s, lane, qmax2); break;
-        case 2: cn_tiles<2>(cd, ds, ts, beg, s, lane, qmax2); break;
-        case 3: cn_tiles<3>(cd, ds, ts, beg, s, lane, qmax2); break;
-        case 4: cn_tiles<4>(cd, ds, ts, beg, s, lane, qmax2); break;
-        case 5: cn_tiles<5>(cd, ds, ts, beg, s, lane, qmax2); break;
-        case 6: cn_tiles<6>(cd, ds, ts, beg, s, lane, qmax2); break;
-        case 7: cn_tiles<7>(cd, ds, ts, beg, s, lane, qmax2); break;
-        case 8: cn_tiles<8>(cd, ds, ts, beg, s, lane, qmax2); break;
-        case 9: cn_tiles<9>(cd, ds, ts, beg, s, lane, qmax2); break;
-        case 10: cn_tiles<10>(cd, ds, ts, beg, s, lane, qmax2); break;
-        default: cn_tiles_generic(cd, ds, ts, beg, deg, s, lane, qmax2); break;
+    // last warp of the block publishes the block's unsatisfied lanes (no barrier in the hot part)
+    __threadfence_block();
+    int last = 0;
+    if (lane == 0) last = (atomicAdd(&s_done, 1) == WARPS_PER_BLOCK - 1);
+    last = __shfl_sync(FULL, last, 0);
+    if (last && lane < SUBS) {
+        const uint32_t v = atomicOr(&s_unsat[lane], 0u);
+        if (v) atomicOr(reinterpret_cast<uint32_t *>(&ds.tile_unsat[t]) + lane, v);
     }
+}
+
+// ------------------------------------------------------------------ variable nodes
+
+template <int DV, bool FIRST>
+__device__ __forceinline__ void vn_var(float4 *__restrict__ mt, const int (&slot)[DV > 0 ? DV : 1], float4 Lv,
+                                       bool any, float qmax2, float4 &post) {
+    post = Lv;
+    if (!any) return;
+    if (FIRST) {
+        const float4 q = make_float4(clampf(Lv.x, qmax2), clampf(Lv.y, qmax2), clampf(Lv.z, qmax2), clampf(Lv.w, qmax2));
+#pragma unroll
+        for (int k = 0; k < DV; ++k) mt[(size_t)slot[k] * LANES] = q;
+        return;
+    }
+    float4 r[DV > 0 ? DV : 1];
+#pragma unroll
+    for (int k = 0; k < DV; ++k) r[k] = mt[(size_t)slot[k] * LANES];
+#pragma unroll
+    for (int k = 0; k < DV; ++k) {
+        post.x += r[k].x;
+        post.y += r[k].y;
+        post.z += r[k].z;
+        post.w += r[k].w;
+    }
+#pragma unroll
+    for (int k = 0; k < DV; ++k)
+        mt[(size_t)slot[k] * LANES] = make_float4(clampf(post.x - r[k].x, qmax2), clampf(post.y - r[k].y, qmax2),
+                                                  clampf(post.z - r[k].z, qmax2), clampf(post.w - r[k].w, qmax2));
+}
+
+template <bool FIRST>
+__device__ __noinline__ float4 vn_var_generic(float4 *__restrict__ mt, const int32_t *__restrict__ slots, int deg,
+                                              float4 Lv, bool any, float qmax2) {
+    float4 post = Lv;
+    if (!any) return post;
+    if (!FIRST) {
+        for (int k = 0; k < deg; ++k) {
+            const float4 r = mt[(size_t)slots[k] * LANES];
+            post.x += r.x;
+            post.y += r.y;
+            post.z += r.z;
+            post.w += r.w;
+        }
+    }
+    for (int k = 0; k < deg; ++k) {
+        float4 *p = mt + (size_t)slots[k] * LANES;
+        const float4 r = FIRST ? make_float4(0.f, 0.f, 0.f, 0.f) : *p;
+        *p = make_float4(clampf(post.x - r.x, qmax2), clampf(post.y - r.y, qmax2), clampf(post.z - r.z, qmax2),
+                         clampf(post.w - r.w, qmax2));
+    }
+    return post;
 }
 
 template <int DV, bool FIRST>
-__device__ __forceinline__ void vn_tiles(const CodeDev &cd, const DecState &ds, const TileSet &ts, int v, int sl,
-                                         int lane, float qmax2, float *post_dbg) {
+__device__ __forceinline__ float4 vn_dispatch_one(float4 *mt, int sl, int off, float4 Lv, bool any, float qmax2) {
     int slot[DV > 0 ? DV : 1];
 #pragma unroll
-    for (int k = 0; k < DV; ++k) slot[k] = __shfl_sync(FULL, sl, k);
-    float Lv[TPW];
-    float r[TPW][DV > 0 ? DV : 1];
-#pragma unroll
-    for (int i = 0; i < TPW; ++i) {
-        const bool a = (ts.act[i] >> lane) & 1u;
-        Lv[i] = a ? ds.L[((size_t)ts.t[i] * cd.n + v) * T + lane] : 0.0f;
-        if (!FIRST) {
-            const float *mt = ds.msg + (size_t)ts.t[i] * cd.E * T + lane;
-#pragma unroll
-            for (int k = 0; k < DV; ++k) r[i][k] = a ? mt[(size_t)slot[k] * T] : 0.0f;
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < TPW; ++i) {
-        const bool a = (ts.act[i] >> lane) & 1u;
-        float post = Lv[i];
-        if (!FIRST) {
-#pragma unroll
-            for (int k = 0; k < DV; ++k) post += r[i][k];
-        }
-        if (a) {
-            float *mt = ds.msg + (size_t)ts.t[i] * cd.E * T + lane;
-#pragma unroll
-            for (int k = 0; k < DV; ++k)
-                mt[(size_t)slot[k] * T] = fminf(fmaxf(FIRST ? post : post - r[i][k], -qmax2), qmax2);
-            if (post_dbg) post_dbg[((size_t)ts.t[i] * cd.n + v) * T + lane] = post;
-        }
-        const uint32_t word = __ballot_sync(FULL, a && post < 0.0f);
-        if (lane == 0 && ts.act[i]) {
-            uint32_t *h = ds.hb + (size_t)ts.t[i] * cd.n + v;
-            *h = FIRST ? (word & ts.act[i]) : ((word & ts.act[i]) | (*h & ~ts.act[i]));
-        }
-    }
+    for (int k = 0; k < DV; ++k) slot[k] = __shfl_sync(FULL, sl, off + k);
+    float4 post;
+    vn_var<DV, FIRST>(mt, slot, Lv, any, qmax2, post);
+    return post;
 }
 
 template <bool FIRST>
-__device__ __noinline__ void vn_tiles_generic(const CodeDev cd, const DecState ds, const TileSet ts, int v,
-                                              int beg, int deg, int lane, float qmax2, float *post_dbg) {
-    const int32_t *slots = cd.csc_slot + beg;
-    for (int i = 0; i < TPW; ++i) {
-        const bool a = (ts.act[i] >> lane) & 1u;
-        float *mt = ds.msg + (size_t)ts.t[i] * cd.E * T + lane;
-        float post = a ? ds.L[((size_t)ts.t[i] * cd.n + v) * T + lane] : 0.0f;
-        if (a) {
-            if (!FIRST)
-                for (int k = 0; k < deg; ++k) post += mt[(size_t)slots[k] * T];
-            for (int k = 0; k < deg; ++k) {
-                float *p = mt + (size_t)slots[k] * T;
-                *p = fminf(fmaxf(FIRST ? post : post - *p, -qmax2), qmax2);
-            }
-            if (post_dbg) post_dbg[((size_t)ts.t[i] * cd.n + v) * T + lane] = post;
-        }
-        const uint32_t word = __ballot_sync(FULL, a && post < 0.0f);
-        if (lane == 0 && ts.act[i]) {
-            uint32_t *h = ds.hb + (size_t)ts.t[i] * cd.n + v;
-            *h = FIRST ? (word & ts.act[i]) : ((word & ts.act[i]) | (*h & ~ts.act[i]));
-        }
-    }
-}
-
-template <bool FIRST>
-__global__ void __launch_bounds__(BLOCK, 3) k_vn(CodeDev cd, DecState ds, float qmax2, float *post_dbg) {
-    const int g = blockIdx.y;
-    if (g * TPW >= ds.counts[0]) return;
-    const TileSet ts = load_tiles(ds, g);
+__global__ void __launch_bounds__(BLOCK, 3) k_vn(CodeDev cd, DecState ds, float qmax2, float4 *post_dbg) {
+    const int ti = blockIdx.y;
+    if (ti >= ds.counts[0]) return;
+    const int t = ds.active_list[ti];
+    const uint4 act = ds.tile_active[t];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int v = blockIdx.x * WARPS_PER_BLOCK + warp;
-    if (v >= cd.n) return;
-    const int beg = cd.col_ptr[v];
-    const int deg = cd.col_ptr[v + 1] - beg;
-    const int sl = (lane < deg) ? cd.csc_slot[beg + lane] : 0;
-    switch (deg) {
-        case 0: vn_tiles<0, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
-        case 1: vn_tiles<1, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
-        case 2: vn_tiles<2, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
-        case 3: vn_tiles<3, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
-        case 4: vn_tiles<4, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
-        case 5: vn_tiles<5, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
-        case 6: vn_tiles<6, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
-        case 7: vn_tiles<7, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
-        case 8: vn_tiles<8, FIRST>(cd, ds, ts, v, sl, lane, qmax2, post_dbg); break;
-        default: vn_tiles_generic<FIRST>(cd, ds, ts, v, beg, deg, lane, qmax2, post_dbg); break;
+    const int v0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * VPW;
+    const int nv = min(VPW, cd.n - v0);
+    if (nv <= 0) return;
+    const int cp = (lane <= nv) ? cd.col_ptr[v0 + lane] : 0;
+    int lo[VPW + 1];
+#pragma unroll
+    for (int i = 0; i <= VPW; ++i) lo[i] = __shfl_sync(FULL, cp, i <= nv ? i : nv);
+    const int ebeg = lo[0], eend = lo[nv];
+    const bool staged = (eend - ebeg) <= 32;
+    const int sl = (staged && ebeg + lane < eend) ? cd.csc_slot[ebeg + lane] : 0;
+    const bool any = ((act.x | act.y | act.z | act.w) >> lane) & 1u;
+    float4 Lv[VPW];
+#pragma unroll
+    for (int i = 0; i < VPW; ++i)
+        Lv[i] = (i < nv && any) ? ds.L[((size_t)t * cd.n + v0 + i) * LANES + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 *mt = ds.msg + (size_t)t * cd.E * LANES + lane;
+    uint4 *hbt = ds.hb + (size_t)t * cd.n;
+#pragma unroll
+    for (int i = 0; i < VPW; ++i) {
+        if (i >= nv) break;
+        const int deg = lo[i + 1] - lo[i];
+        const int off = lo[i] - ebeg;
+        float4 post;
+        if (!staged) {
+            post = vn_var_generic<FIRST>(mt, cd.csc_slot + lo[i], deg, Lv[i], any, qmax2);
+        } else {
+            switch (deg) {
+                case 0: post = Lv[i]; break;
+                case 1: post = vn_dispatch_one<1, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
+                case 2: post = vn_dispatch_one<2, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
+                case 3: post = vn_dispatch_one<3, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
+                case 4: post = vn_dispatch_one<4, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
+                case 5: post = vn_dispatch_one<5, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
+                case 6: post = vn_dispatch_one<6, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
+                case 7: post = vn_dispatch_one<7, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
+                case 8: post = vn_dispatch_one<8, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
+                default: post = vn_var_generic<FIRST>(mt, cd.csc_slot + lo[i], deg, Lv[i], any, qmax2); break;
+            }
+        }
+        // hard decisions (retired frames were copied out before this pass; their bits may change)
+        uint4 word;
+        word.x = __ballot_sync(FULL, post.x < 0.0f) & act.x;
+        word.y = __ballot_sync(FULL, post.y < 0.0f) & act.y;
+        word.z = __ballot_sync(FULL, post.z < 0.0f) & act.z;
+        word.w = __ballot_sync(FULL, post.w < 0.0f) & act.w;
+        if (lane == 0) hbt[v0 + i] = word;
+        if (post_dbg && any) post_dbg[((size_t)t * cd.n + v0 + i) * LANES + lane] = post;
     }
 }
+
+// ------------------------------------------------------------------ scheduling
 
 // Block-wide exclusive scan of 0/1 flags (blockDim.x multiple of 32, <= 1024).
 __device__ __forceinline__ int block_scan_flag(bool flag, int *s_warp, int *total) {
@@ -313,6 +378,16 @@ __device__ __forceinline__ int block_scan_flag(bool flag, int *s_warp, int *tota
     return r;
 }
 
+__device__ __forceinline__ void mark_frames(const DecState &ds, int t, int s, uint32_t bits, int32_t it, uint8_t cv) {
+    while (bits) {
+        const int l = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int f = t * T + s * LANES + l;
+        ds.iters[f] = it;
+        ds.conv[f] = cv;
+    }
+}
+
 // Convergence bookkeeping after CN pass k (which tested decision k-1).
 // Single block; loops over tiles.  final_pass: k = max_iter + 1.
 __global__ void __launch_bounds__(1024) k_status(DecState ds, int k, int max_iter, int final_pass,
@@ -321,98 +396,95 @@ __global__ void __launch_bounds__(1024) k_status(DecState ds, int k, int max_ite
     __shared__ int s_lanes;
     if (threadIdx.x == 0) s_lanes = 0;
     __syncthreads();
-    int n_act = 0, n_ret = 0, lanes = 0;
+    int n_act = 0, n_ret = 0;
     for (int t0 = 0; t0 < ds.tiles; t0 += blockDim.x) {
         const int t = t0 + threadIdx.x;
-        uint32_t rem = 0u, newly = 0u;
+        uint4 rem = make_uint4(0u, 0u, 0u, 0u), newly = make_uint4(0u, 0u, 0u, 0u);
         if (t < ds.tiles) {
-            const uint32_t a = ds.tile_active[t];
-            const uint32_t u = ds.tile_unsat[t];
-            if (a) {
-                ds.tile_unsat[t] = 0u;
-                const uint32_t done = a & ~u;
-                rem = a & u;
-                uint32_t d = done;
-                while (d) {
-                    const int l = __ffs(d) - 1;
-                    d &= d - 1;
-                    ds.iters[t * T + l] = k - 1;
-                    ds.conv[t * T + l] = 1;
+            const uint4 a = ds.tile_active[t];
+            if (a.x | a.y | a.z | a.w) {
+                const uint4 u = ds.tile_unsat[t];
+                ds.tile_unsat[t] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                for (int s = 0; s < SUBS; ++s) {
+                    const uint32_t as = cmpu(a, s), us = cmpu(u, s);
+                    mark_frames(ds, t, s, as & ~us, k - 1, 1);
+                    if (final_pass) mark_frames(ds, t, s, as & us, max_iter, 0);
                 }
                 if (final_pass) {
-                    uint32_t f = rem;
-                    while (f) {
-                        const int l = __ffs(f) - 1;
-                        f &= f - 1;
-                        ds.iters[t * T + l] = max_iter;
-                        ds.conv[t * T + l] = 0;
-                    }
                     newly = a;
-                    rem = 0u;
                 } else {
-                    newly = done;
+                    newly = make_uint4(a.x & ~u.x, a.y & ~u.y, a.z & ~u.z, a.w & ~u.w);
+                    rem = make_uint4(a.x & u.x, a.y & u.y, a.z & u.z, a.w & u.w);
                 }
                 ds.tile_active[t] = rem;
             }
             ds.tile_newly[t] = newly;
         }
+        const bool ra = (rem.x | rem.y | rem.z | rem.w) != 0u;
+        const bool rn = (newly.x | newly.y | newly.z | newly.w) != 0u;
         int tot;
-        const int pa = block_scan_flag(rem != 0u, s_warp, &tot);
-        if (rem) ds.active_list[n_act + pa] = t;
+        const int pa = block_scan_flag(ra, s_warp, &tot);
+        if (ra) ds.active_list[n_act + pa] = t;
         n_act += tot;
-        const int pr = block_scan_flag(newly != 0u, s_warp, &tot);
-        if (newly) ds.retire_list[n_ret + pr] = t;
+        const int pr = block_scan_flag(rn, s_warp, &tot);
+        if (rn) ds.retire_list[n_ret + pr] = t;
         n_ret += tot;
-        int v = __popc(rem);
+        int v = __popc(rem.x) + __popc(rem.y) + __popc(rem.z) + __popc(rem.w);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-        if ((threadIdx.x & 31) == 0) atomicAdd(&s_lanes, v);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_lanes, v);
     }
     __syncthreads();
-    lanes = s_lanes;
     if (threadIdx.x == 0) {
         ds.counts[0] = n_act;
         ds.counts[1] = n_ret;
-        ds.counts[2] = lanes;
+        ds.counts[2] = s_lanes;
         if (host_counts) {
             volatile int32_t *h = host_counts;
             h[0] = n_act;
             h[1] = n_ret;
-            h[2] = lanes;
+            h[2] = s_lanes;
         }
     }
 }
 
-// Write the hard decisions of retired lanes as packed bits (32x32 bit transpose by ballots).
+// Write the hard decisions of retired frames as packed bits (32x32 bit transposes by ballots).
 __global__ void __launch_bounds__(BLOCK) k_retire(DecState ds, int32_t n, uint32_t *bits_out) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[1]) return;
     const int t = ds.retire_list[ti];
-    const uint32_t newly = ds.tile_newly[t];
+    const uint4 newly = ds.tile_newly[t];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Wn = words_of(n);
     const int w = blockIdx.x * WARPS_PER_BLOCK + warp;
     if (w >= Wn) return;
     const int v = w * 32 + lane;
-    const uint32_t word = (v < n) ? ds.hb[(size_t)t * n + v] : 0u;
-    uint32_t mine = 0u;
+    const uint4 word = (v < n) ? ds.hb[(size_t)t * n + v] : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-    for (int f = 0; f < 32; ++f) {
-        const uint32_t b = __ballot_sync(FULL, (word >> f) & 1u);
-        if (lane == f) mine = b;
+    for (int s = 0; s < SUBS; ++s) {
+        const uint32_t ns = cmpu(newly, s);
+        if (!ns) continue;
+        const uint32_t ws = cmpu(word, s);
+        uint32_t mine = 0u;
+#pragma unroll
+        for (int f = 0; f < 32; ++f) {
+            const uint32_t b = __ballot_sync(FULL, (ws >> f) & 1u);
+            if (lane == f) mine = b;
+        }
+        const int frame = t * T + s * LANES + lane;
+        if (((ns >> lane) & 1u) && frame < ds.frames) bits_out[(size_t)frame * Wn + w] = mine;
     }
-    const int frame = t * T + lane;
-    if (((newly >> lane) & 1u) && frame < ds.frames) bits_out[(size_t)frame * Wn + w] = mine;
 }
 
-// natural [F][rows] -> interleaved [tiles][rows][T] (zero-fill missing frames)
-__global__ void k_to_interleaved(const float *__restrict__ src, float *__restrict__ dst, int32_t F, int64_t rows,
-                                 float scale) {
-    __shared__ float sm[32][33];
+// natural [F][rows] -> interleaved [tiles][rows][32] float4 (zero-fill missing frames), times scale
+__global__ void __launch_bounds__(256) k_to_interleaved(const float *__restrict__ src, float4 *__restrict__ dst,
+                                                        int32_t F, int64_t rows, float scale) {
+    __shared__ float sm[T][33];
     const int t = blockIdx.y;
     const int64_t r0 = (int64_t)blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    for (int fl = ty; fl < 32; fl += 8) {
+    for (int fl = ty; fl < T; fl += 8) {
         const int f = t * T + fl;
         const int64_t r = r0 + tx;
         sm[fl][tx] = (f < F && r < rows) ? src[(size_t)f * rows + r] * scale : 0.0f;
@@ -420,61 +492,73 @@ __global__ void k_to_interleaved(const float *__restrict__ src, float *__restric
     __syncthreads();
     for (int rl = ty; rl < 32; rl += 8) {
         const int64_t r = r0 + rl;
-        if (r < rows) dst[((size_t)t * rows + r) * T + tx] = sm[tx][rl];
+        if (r < rows)
+            dst[((size_t)t * rows + r) * LANES + tx] = make_float4(sm[tx][rl], sm[32 + tx][rl], sm[64 + tx][rl], sm[96 + tx][rl]);
     }
 }
 
-// interleaved [tiles][rows][T] -> natural [F][rows]
-__global__ void k_from_interleaved(const float *__restrict__ src, float *__restrict__ dst, int32_t F, int64_t rows,
-                                   float scale) {
-    __shared__ float sm[32][33];
+// interleaved [tiles][rows][32] float4 -> natural [F][rows], times scale
+__global__ void __launch_bounds__(256) k_from_interleaved(const float4 *__restrict__ src, float *__restrict__ dst,
+                                                          int32_t F, int64_t rows, float scale) {
+    __shared__ float sm[T][33];
     const int t = blockIdx.y;
     const int64_t r0 = (int64_t)blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int rl = ty; rl < 32; rl += 8) {
         const int64_t r = r0 + rl;
-        sm[rl][tx] = (r < rows) ? src[((size_t)t * rows + r) * T + tx] : 0.0f;
+        const float4 v = (r < rows) ? src[((size_t)t * rows + r) * LANES + tx] : make_float4(0.f, 0.f, 0.f, 0.f);
+        sm[tx][rl] = v.x;
+        sm[32 + tx][rl] = v.y;
+        sm[64 + tx][rl] = v.z;
+        sm[96 + tx][rl] = v.w;
     }
     __syncthreads();
-    for (int fl = ty; fl < 32; fl += 8) {
+    for (int fl = ty; fl < T; fl += 8) {
         const int f = t * T + fl;
         const int64_t r = r0 + tx;
-        if (f < F && r < rows) dst[(size_t)f * rows + r] = sm[tx][fl] * scale;
+        if (f < F && r < rows) dst[(size_t)f * rows + r] = sm[fl][tx] * scale;
     }
 }
 
-// public syndrome [F][Wm] -> per-tile lane-bit words st[t][c]
+// public syndrome [F][Wm] -> per-tile lane-bit words st[t][c] (uint4 over sub-tiles)
 __global__ void __launch_bounds__(BLOCK) k_synd_transpose(const uint32_t *__restrict__ synd, int32_t F, int32_t M,
-                                                           uint32_t *__restrict__ st) {
+                                                           uint4 *__restrict__ st) {
     const int t = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Wm = words_of(M);
     const int w = blockIdx.x * WARPS_PER_BLOCK + warp;
     if (w >= Wm) return;
-    const int f = t * T + lane;
-    const uint32_t word = (f < F) ? synd[(size_t)f * Wm + w] : 0u;
-    uint32_t mine = 0u;
+    uint32_t mine[SUBS];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-        const uint32_t b = __ballot_sync(FULL, (word >> k) & 1u);
-        if (lane == k) mine = b;
+    for (int s = 0; s < SUBS; ++s) {
+        const int f = t * T + s * LANES + lane;
+        const uint32_t word = (f < F) ? synd[(size_t)f * Wm + w] : 0u;
+        mine[s] = 0u;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t b = __ballot_sync(FULL, (word >> k) & 1u);
+            if (lane == k) mine[s] = b;
+        }
     }
     const int c = w * 32 + lane;
-    if (c < M) st[(size_t)t * M + c] = mine;
+    if (c < M) st[(size_t)t * M + c] = make_uint4(mine[0], mine[1], mine[2], mine[3]);
 }
 
-// initial tile state: active lanes = valid frames (& alive mask if given)
+// initial tile state: active frames = valid frames (& alive mask if given)
 __global__ void k_init_tiles(DecState ds, const uint8_t *__restrict__ alive) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ds.tiles) return;
-    uint32_t a = 0u;
-    for (int l = 0; l < T; ++l) {
-        const int f = t * T + l;
-        if (f < ds.frames && (!alive || alive[f])) a |= 1u << l;
+    uint32_t a[SUBS];
+    for (int s = 0; s < SUBS; ++s) {
+        a[s] = 0u;
+        for (int l = 0; l < LANES; ++l) {
+            const int f = t * T + s * LANES + l;
+            if (f < ds.frames && (!alive || alive[f])) a[s] |= 1u << l;
+        }
     }
-    ds.tile_active[t] = a;
-    ds.tile_unsat[t] = 0u;
-    ds.tile_newly[t] = 0u;
+    ds.tile_active[t] = make_uint4(a[0], a[1], a[2], a[3]);
+    ds.tile_unsat[t] = make_uint4(0u, 0u, 0u, 0u);
+    ds.tile_newly[t] = make_uint4(0u, 0u, 0u, 0u);
     ds.active_list[t] = t;
 }
 
@@ -491,14 +575,16 @@ __global__ void k_set_counts(DecState ds, int32_t n_active) {
 // qmax is in natural LLR units; the arena works in log2 units
 void launch_cn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, int check_only, cudaStream_t s) {
     if (grid_tiles <= 0) return;
-    dim3 grid((cd.M + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, (grid_tiles + TPW - 1) / TPW);
+    const int per_block = WARPS_PER_BLOCK * CPW;
+    dim3 grid((cd.M + per_block - 1) / per_block, grid_tiles);
     k_cn<<<grid, BLOCK, 0, s>>>(cd, ds, qmax * LOG2E, check_only);
 }
 
-void launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float *post_dbg,
+void launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float4 *post_dbg,
                cudaStream_t s) {
     if (grid_tiles <= 0) return;
-    dim3 grid((cd.n + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, (grid_tiles + TPW - 1) / TPW);
+    const int per_block = WARPS_PER_BLOCK * VPW;
+    dim3 grid((cd.n + per_block - 1) / per_block, grid_tiles);
     if (first) k_vn<true><<<grid, BLOCK, 0, s>>>(cd, ds, qmax * LOG2E, post_dbg);
     else k_vn<false><<<grid, BLOCK, 0, s>>>(cd, ds, qmax * LOG2E, post_dbg);
 }
@@ -513,25 +599,25 @@ void launch_retire(const DecState &ds, int32_t n, int grid_tiles, uint32_t *bits
     k_retire<<<grid, BLOCK, 0, s>>>(ds, n, bits_out);
 }
 
-void launch_to_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, float scale,
+void launch_to_interleaved(const float *src, float4 *dst, int32_t F, int64_t rows, int tiles, float scale,
                            cudaStream_t s) {
     dim3 grid((unsigned)((rows + 31) / 32), tiles);
     k_to_interleaved<<<grid, 256, 0, s>>>(src, dst, F, rows, scale);
 }
 
-void launch_from_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, float scale,
+void launch_from_interleaved(const float4 *src, float *dst, int32_t F, int64_t rows, int tiles, float scale,
                              cudaStream_t s) {
     dim3 grid((unsigned)((rows + 31) / 32), tiles);
     k_from_interleaved<<<grid, 256, 0, s>>>(src, dst, F, rows, scale);
 }
 
-void launch_synd_transpose(const uint32_t *synd, int32_t F, int32_t M, uint32_t *st, int tiles, cudaStream_t s) {
+void launch_synd_transpose(const uint32_t *synd, int32_t F, int32_t M, uint4 *st, int tiles, cudaStream_t s) {
     dim3 grid((words_of(M) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, tiles);
     k_synd_transpose<<<grid, BLOCK, 0, s>>>(synd, F, M, st);
 }
 
 void launch_init_tiles(const DecState &ds, const uint8_t *alive, cudaStream_t s) {
-    k_init_tiles<<<(ds.tiles + 255) / 256, 256, 0, s>>>(ds, alive);
+    k_init_tiles<<<(ds.tiles + 127) / 128, 128, 0, s>>>(ds, alive);
 }
 
 void launch_set_counts(const DecState &ds, int32_t n_active, cudaStream_t s) {

@@ -8,10 +8,14 @@
 
 namespace cvsr {
 
-// Frames per tile: one warp lane per frame.  Edge messages of the T frames of
-// a tile are stored contiguously per edge ("frame-interleaved arena",
-// SURVEY.md §2.6 row 45), so a warp reads/writes one 128-byte line per edge.
-constexpr int T = 32;
+// Frames per tile: 128 = 32 warp lanes x 4 frames per lane (one float4).
+// Frame f of tile t sits at lane (f mod 32), component ((f / 32) mod 4)
+// ("sub-tile"), i.e. f = 128 t + 32 s + lane.  Edge messages of the 128
+// frames of a tile are stored contiguously per edge slot ("frame-interleaved
+// arena"): a warp moves one 512-byte line per edge.
+constexpr int T = 128;
+constexpr int LANES = 32;
+constexpr int SUBS = 4;
 constexpr int WARPS_PER_BLOCK = 8;
 constexpr int BLOCK = 32 * WARPS_PER_BLOCK;
 // largest check degree supported (cvsr_code_load rejects larger rows with CVSR_ECODE)
@@ -33,16 +37,17 @@ struct CodeDev {
 };
 
 // Per-decode device state (lives in the context's scratch arena).
+// Masks and bit words are uint4: component s holds the 32 lanes of sub-tile s.
 struct DecState {
     int32_t tiles;
     int32_t frames;
-    float *msg;             // [tiles][E][T]  in-place V2C/C2V message per edge slot
-    float *L;               // [tiles][n][T]  channel LLR
-    uint32_t *hb;           // [tiles][n]     hard decisions, bit = lane
-    uint32_t *st;           // [tiles][M]     syndrome bits, bit = lane
-    uint32_t *tile_active;  // [tiles] lanes still iterating
-    uint32_t *tile_unsat;   // [tiles] lanes with >= 1 unsatisfied check in this CN pass
-    uint32_t *tile_newly;   // [tiles] lanes retired by the last status pass
+    float4 *msg;            // [tiles][E][32]  in-place V2C/C2V message per edge slot (log2 units)
+    float4 *L;              // [tiles][n][32]  channel LLR (log2 units)
+    uint4 *hb;              // [tiles][n]      hard decisions, bit = lane
+    uint4 *st;              // [tiles][M]      syndrome bits, bit = lane
+    uint4 *tile_active;     // [tiles] frames still iterating
+    uint4 *tile_unsat;      // [tiles] frames with >= 1 unsatisfied check in this CN pass
+    uint4 *tile_newly;      // [tiles] frames retired by the last status pass
     int32_t *active_list;   // [tiles]
     int32_t *retire_list;   // [tiles]
     int32_t *counts;        // [4]: n_active, n_retire, total active lanes, pad

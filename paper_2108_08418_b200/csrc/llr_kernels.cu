@@ -88,18 +88,19 @@ __global__ void k_llr_slice(LlrParams p, const float *__restrict__ x, const uint
 }
 
 // decoder feed: conditional LLR written straight into the interleaved arena
-// L[t][v][lane] (fused transpose); known bits read from packed slices.
+// L[t][v][lane] (float4 over the 4 sub-tiles; fused transpose, log2 units);
+// known bits read from the packed slices.
 __global__ void __launch_bounds__(256) k_llr_interleaved(LlrParams p, const float *__restrict__ x, int32_t F,
-                                                         int32_t n, float *__restrict__ L) {
+                                                         int32_t n, float4 *__restrict__ L) {
     __shared__ float se[256];
-    __shared__ float sm[32][33];
+    __shared__ float sm[T][33];
     for (int i = threadIdx.x; i < 255; i += blockDim.x) se[i] = p.edges[i];
     __syncthreads();
     const int t = blockIdx.y;
     const int v0 = blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int Wn = words_of(n);
-    for (int fl = ty; fl < 32; fl += 8) {
+    for (int fl = ty; fl < T; fl += 8) {
         const int f = t * T + fl;
         const int v = v0 + tx;
         float val = 0.0f;
@@ -112,12 +113,13 @@ __global__ void __launch_bounds__(256) k_llr_interleaved(LlrParams p, const floa
             }
             val = llr_cond(se, p.m, p.j, p.known_mask, kappa, x[(size_t)f * n + v], p.inv_sigma, p.llr_max);
         }
-        sm[fl][tx] = val;
+        sm[fl][tx] = val * LOG2E;  // arena: log2 units
     }
     __syncthreads();
     for (int vl = ty; vl < 32; vl += 8) {
         const int v = v0 + vl;
-        if (v < n) L[((size_t)t * n + v) * T + tx] = sm[tx][vl] * LOG2E;  // arena: log2 units
+        if (v < n)
+            L[((size_t)t * n + v) * LANES + tx] = make_float4(sm[tx][vl], sm[32 + tx][vl], sm[64 + tx][vl], sm[96 + tx][vl]);
     }
 }
 
@@ -143,7 +145,7 @@ void launch_llr_biawgn(const float *y, int64_t count, float sigma2, float llr_ma
     k_llr_biawgn<<<grid_for(count, 256), 256, 0, s>>>(y, count, sigma2, llr_max, out);
 }
 
-void launch_llr_interleaved(const LlrParams &p, const float *x, int32_t F, int32_t n, int tiles, float *L,
+void launch_llr_interleaved(const LlrParams &p, const float *x, int32_t F, int32_t n, int tiles, float4 *L,
                             cudaStream_t s) {
     dim3 grid((n + 31) / 32, tiles);
     k_llr_interleaved<<<grid, 256, 0, s>>>(p, x, F, n, L);
