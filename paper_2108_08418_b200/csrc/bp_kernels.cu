@@ -95,13 +95,20 @@ __device__ __forceinline__ void cn_update(float (&q)[DC], uint32_t sbit, float q
     }
 }
 
-// one check, 4 frames per lane (al = this lane's active bit per sub-tile)
+// One check, 4 frames per lane (al = this lane's active bit per sub-tile).
+// DC is the code's maximum check degree; a check of degree deg < DC is padded
+// with "certain" dummy edges (|q| = 200 in log2 units: w = 0, the neutral
+// element of (+), sign +), which are neither loaded nor stored.  One code body
+// per code keeps the instruction cache hot.
+constexpr float DUMMY_Q = 200.0f;
+
 template <int DC>
-__device__ __forceinline__ void cn_check(float4 *__restrict__ m, const uint4 &sb, const uint4 &al, float qmax2) {
+__device__ __forceinline__ void cn_check(float4 *__restrict__ m, int deg, const uint4 &sb, const uint4 &al,
+                                         float qmax2) {
     if (!(al.x | al.y | al.z | al.w)) return;
     float4 q[DC];
 #pragma unroll
-    for (int k = 0; k < DC; ++k) q[k] = m[(size_t)k * LANES];
+    for (int k = 0; k < DC; ++k) q[k] = (k < deg) ? m[(size_t)k * LANES] : make_float4(DUMMY_Q, DUMMY_Q, DUMMY_Q, DUMMY_Q);
 #pragma unroll
     for (int s = 0; s < SUBS; ++s) {
         if (!cmpu(al, s)) continue;
@@ -113,7 +120,8 @@ __device__ __forceinline__ void cn_check(float4 *__restrict__ m, const uint4 &sb
         for (int k = 0; k < DC; ++k) set4(q[k], s, a[k]);
     }
 #pragma unroll
-    for (int k = 0; k < DC; ++k) m[(size_t)k * LANES] = q[k];
+    for (int k = 0; k < DC; ++k)
+        if (k < deg) m[(size_t)k * LANES] = q[k];
 }
 
 // any degree up to MAX_DC (rare): w and suffix complements in thread-local arrays
@@ -142,7 +150,8 @@ __device__ __noinline__ void cn_check_generic(float4 *__restrict__ m, int deg, u
     }
 }
 
-__global__ void __launch_bounds__(BLOCK, 3) k_cn(CodeDev cd, DecState ds, float qmax2, int check_only) {
+template <int DCT>  // DCT = max check degree (templated body) or 0 = generic only
+__global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT <= 5) ? 4 : 3) k_cn(CodeDev cd, DecState ds, float qmax2, int check_only) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
     const int t = ds.active_list[ti];
@@ -180,17 +189,8 @@ __global__ void __launch_bounds__(BLOCK, 3) k_cn(CodeDev cd, DecState ds, float 
                     const int deg = lo[i + 1] - lo[i];
                     float4 *m = mt + (size_t)lo[i] * LANES;
                     const uint4 sb = lanebits4(par[i], lane);
-                    switch (deg) {
-                        case 1: cn_check<1>(m, sb, al, qmax2); break;
-                        case 2: cn_check<2>(m, sb, al, qmax2); break;
-                        case 3: cn_check<3>(m, sb, al, qmax2); break;
-                        case 4: cn_check<4>(m, sb, al, qmax2); break;
-                        case 5: cn_check<5>(m, sb, al, qmax2); break;
-                        case 6: cn_check<6>(m, sb, al, qmax2); break;
-                        case 7: cn_check<7>(m, sb, al, qmax2); break;
-                        case 8: cn_check<8>(m, sb, al, qmax2); break;
-                        default: cn_check_generic(m, deg, sb, al, qmax2); break;
-                    }
+                    if constexpr (DCT > 0) cn_check<DCT>(m, deg, sb, al, qmax2);  // DCT = max_dc >= deg
+                    else cn_check_generic(m, deg, sb, al, qmax2);
                 }
             }
         }
@@ -234,20 +234,23 @@ __global__ void __launch_bounds__(BLOCK, 3) k_cn(CodeDev cd, DecState ds, float 
 
 // ------------------------------------------------------------------ variable nodes
 
+// DV = the code's maximum variable degree handled in registers; a variable of
+// degree deg < DV uses the first deg slots (missing r are 0, the neutral sum).
 template <int DV, bool FIRST>
-__device__ __forceinline__ void vn_var(float4 *__restrict__ mt, const int (&slot)[DV > 0 ? DV : 1], float4 Lv,
-                                       bool any, float qmax2, float4 &post) {
+__device__ __forceinline__ void vn_var(float4 *__restrict__ mt, const int (&slot)[DV], int deg, float4 Lv, bool any,
+                                       float qmax2, float4 &post) {
     post = Lv;
     if (!any) return;
     if (FIRST) {
         const float4 q = make_float4(clampf(Lv.x, qmax2), clampf(Lv.y, qmax2), clampf(Lv.z, qmax2), clampf(Lv.w, qmax2));
 #pragma unroll
-        for (int k = 0; k < DV; ++k) mt[(size_t)slot[k] * LANES] = q;
+        for (int k = 0; k < DV; ++k)
+            if (k < deg) mt[(size_t)slot[k] * LANES] = q;
         return;
     }
-    float4 r[DV > 0 ? DV : 1];
+    float4 r[DV];
 #pragma unroll
-    for (int k = 0; k < DV; ++k) r[k] = mt[(size_t)slot[k] * LANES];
+    for (int k = 0; k < DV; ++k) r[k] = (k < deg) ? mt[(size_t)slot[k] * LANES] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < DV; ++k) {
         post.x += r[k].x;
@@ -257,8 +260,9 @@ __device__ __forceinline__ void vn_var(float4 *__restrict__ mt, const int (&slot
     }
 #pragma unroll
     for (int k = 0; k < DV; ++k)
-        mt[(size_t)slot[k] * LANES] = make_float4(clampf(post.x - r[k].x, qmax2), clampf(post.y - r[k].y, qmax2),
-                                                  clampf(post.z - r[k].z, qmax2), clampf(post.w - r[k].w, qmax2));
+        if (k < deg)
+            mt[(size_t)slot[k] * LANES] = make_float4(clampf(post.x - r[k].x, qmax2), clampf(post.y - r[k].y, qmax2),
+                                                      clampf(post.z - r[k].z, qmax2), clampf(post.w - r[k].w, qmax2));
 }
 
 template <bool FIRST>
@@ -285,17 +289,18 @@ __device__ __noinline__ float4 vn_var_generic(float4 *__restrict__ mt, const int
 }
 
 template <int DV, bool FIRST>
-__device__ __forceinline__ float4 vn_dispatch_one(float4 *mt, int sl, int off, float4 Lv, bool any, float qmax2) {
-    int slot[DV > 0 ? DV : 1];
+__device__ __forceinline__ float4 vn_dispatch_one(float4 *mt, int sl, int off, int deg, float4 Lv, bool any,
+                                                  float qmax2) {
+    int slot[DV];
 #pragma unroll
-    for (int k = 0; k < DV; ++k) slot[k] = __shfl_sync(FULL, sl, off + k);
+    for (int k = 0; k < DV; ++k) slot[k] = __shfl_sync(FULL, sl, (off + k) & 31);
     float4 post;
-    vn_var<DV, FIRST>(mt, slot, Lv, any, qmax2, post);
+    vn_var<DV, FIRST>(mt, slot, deg, Lv, any, qmax2, post);
     return post;
 }
 
-template <bool FIRST>
-__global__ void __launch_bounds__(BLOCK, 3) k_vn(CodeDev cd, DecState ds, float qmax2, float4 *post_dbg) {
+template <int DVT, bool FIRST>  // DVT = register-path max variable degree (1..8)
+__global__ void __launch_bounds__(BLOCK, DVT <= 6 ? 4 : 3) k_vn(CodeDev cd, DecState ds, float qmax2, float4 *post_dbg) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
     const int t = ds.active_list[ti];
@@ -324,22 +329,8 @@ __global__ void __launch_bounds__(BLOCK, 3) k_vn(CodeDev cd, DecState ds, float 
         const int deg = lo[i + 1] - lo[i];
         const int off = lo[i] - ebeg;
         float4 post;
-        if (!staged) {
-            post = vn_var_generic<FIRST>(mt, cd.csc_slot + lo[i], deg, Lv[i], any, qmax2);
-        } else {
-            switch (deg) {
-                case 0: post = Lv[i]; break;
-                case 1: post = vn_dispatch_one<1, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
-                case 2: post = vn_dispatch_one<2, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
-                case 3: post = vn_dispatch_one<3, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
-                case 4: post = vn_dispatch_one<4, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
-                case 5: post = vn_dispatch_one<5, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
-                case 6: post = vn_dispatch_one<6, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
-                case 7: post = vn_dispatch_one<7, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
-                case 8: post = vn_dispatch_one<8, FIRST>(mt, sl, off, Lv[i], any, qmax2); break;
-                default: post = vn_var_generic<FIRST>(mt, cd.csc_slot + lo[i], deg, Lv[i], any, qmax2); break;
-            }
-        }
+        if (!staged || deg > DVT) post = vn_var_generic<FIRST>(mt, cd.csc_slot + lo[i], deg, Lv[i], any, qmax2);
+        else post = vn_dispatch_one<DVT, FIRST>(mt, sl, off, deg, Lv[i], any, qmax2);
         // hard decisions (retired frames were copied out before this pass; their bits may change)
         uint4 word;
         word.x = __ballot_sync(FULL, post.x < 0.0f) & act.x;
@@ -572,12 +563,34 @@ __global__ void k_set_counts(DecState ds, int32_t n_active) {
 
 // ---------------------------------------------------------------- launchers
 
-// qmax is in natural LLR units; the arena works in log2 units
+// qmax is in natural LLR units; the arena works in log2 units.  The kernel body
+// is chosen by the code's maximum degrees (one instantiation per degree bound).
 void launch_cn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, int check_only, cudaStream_t s) {
     if (grid_tiles <= 0) return;
     const int per_block = WARPS_PER_BLOCK * CPW;
     dim3 grid((cd.M + per_block - 1) / per_block, grid_tiles);
-    k_cn<<<grid, BLOCK, 0, s>>>(cd, ds, qmax * LOG2E, check_only);
+    const float q2 = qmax * LOG2E;
+    switch (cd.max_dc) {
+        case 1: case 2: k_cn<2><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 3: k_cn<3><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 4: k_cn<4><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 5: k_cn<5><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 6: k_cn<6><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 7: k_cn<7><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 8: k_cn<8><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        default: k_cn<0><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+    }
+}
+
+template <bool FIRST>
+static void launch_vn_t(const CodeDev &cd, const DecState &ds, dim3 grid, float q2, float4 *post_dbg, cudaStream_t s) {
+    const int dv = cd.max_dv;
+    if (dv <= 2) k_vn<2, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, q2, post_dbg);
+    else if (dv <= 3) k_vn<3, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, q2, post_dbg);
+    else if (dv <= 4) k_vn<4, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, q2, post_dbg);
+    else if (dv <= 6) k_vn<6, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, q2, post_dbg);
+    else if (dv <= 8) k_vn<8, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, q2, post_dbg);
+    else k_vn<2, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, q2, post_dbg);  // e.g. MET: degree-1 fast path, rest generic
 }
 
 void launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float4 *post_dbg,
@@ -585,8 +598,8 @@ void launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax
     if (grid_tiles <= 0) return;
     const int per_block = WARPS_PER_BLOCK * VPW;
     dim3 grid((cd.n + per_block - 1) / per_block, grid_tiles);
-    if (first) k_vn<true><<<grid, BLOCK, 0, s>>>(cd, ds, qmax * LOG2E, post_dbg);
-    else k_vn<false><<<grid, BLOCK, 0, s>>>(cd, ds, qmax * LOG2E, post_dbg);
+    if (first) launch_vn_t<true>(cd, ds, grid, qmax * LOG2E, post_dbg, s);
+    else launch_vn_t<false>(cd, ds, grid, qmax * LOG2E, post_dbg, s);
 }
 
 void launch_status(const DecState &ds, int k, int max_iter, int final_pass, int32_t *host_counts, cudaStream_t s) {
