@@ -189,9 +189,8 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds,
     // the mapped counter is only read after an event of THIS run completed;
     // every status kernel of this run writes it, so stale values are impossible.
     prof_begin(ctx, KC_INIT);
-    launch_vn(cd, ds, ds.tiles, qmax, true, nullptr, s);
+    int launched = launch_vn(cd, ds, ds.tiles, qmax, true, nullptr, s);
     prof_end(ctx);
-    int launched = 1;
     int bound = ds.tiles;
     for (int k = 1; k <= max_iter + 1; ++k) {
         const int final_pass = (k == max_iter + 1);
@@ -205,9 +204,8 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds,
         launched += 3;
         if (!final_pass) {
             prof_begin(ctx, KC_VN);
-            launch_vn(cd, ds, bound, qmax, false, nullptr, s);
+            launched += launch_vn(cd, ds, bound, qmax, false, nullptr, s);
             prof_end(ctx);
-            launched += 1;
         }
         CK(cudaEventRecord(ctx->ring[k % RING], s));
         if (k >= LOOKAHEAD && !final_pass) {
@@ -372,12 +370,45 @@ cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, cons
     for (int32_t c = 0; c < n_checks; ++c)
         for (int32_t e = row_ptr[c]; e < row_ptr[c + 1]; ++e) csc_slot[fill[col_idx[e]]++] = e;
 
+    // degree classes: distinct degrees ascending; beyond MAX_VCLASS-1 distinct
+    // degrees the remaining variables form one mixed class (generic VN path)
+    std::vector<int32_t> degs;
+    for (int32_t v = 0; v < n_vars; ++v) degs.push_back(col_cnt[v + 1]);
+    std::vector<int32_t> distinct(degs);
+    std::sort(distinct.begin(), distinct.end());
+    distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+    const int n_exact = (int)std::min<size_t>(distinct.size(), MAX_VCLASS - 1);
+    const int n_cls = (int)distinct.size() <= MAX_VCLASS - 1 ? (int)distinct.size() : MAX_VCLASS;
+    auto cls_of = [&](int32_t d) {
+        const int i = (int)(std::lower_bound(distinct.begin(), distinct.end(), d) - distinct.begin());
+        return i < n_exact ? i : MAX_VCLASS - 1;
+    };
+    std::vector<int32_t> vc_vars;
+    vc_vars.reserve(n_vars);
+    std::vector<int32_t> vc_slots;
+    vc_slots.reserve((size_t)E);
+    int32_t vc_deg[MAX_VCLASS], vc_off[MAX_VCLASS], vc_cnt[MAX_VCLASS];
+    int64_t vc_soff[MAX_VCLASS];
+    for (int k = 0; k < n_cls; ++k) {
+        const int cls = (k < n_exact) ? k : MAX_VCLASS - 1;
+        vc_deg[k] = (k < n_exact) ? distinct[k] : -1;
+        vc_off[k] = (int32_t)vc_vars.size();
+        vc_soff[k] = (int64_t)vc_slots.size();
+        for (int32_t v = 0; v < n_vars; ++v) {
+            if (cls_of(degs[v]) != cls) continue;
+            vc_vars.push_back(v);
+            for (int32_t p = col_ptr[v]; p < col_ptr[v + 1]; ++p) vc_slots.push_back(csc_slot[p]);
+        }
+        vc_cnt[k] = (int32_t)vc_vars.size() - vc_off[k];
+    }
+
     DeviceGuard g(ctx->device);
     cvsr_code *code = new cvsr_code();
     code->device = ctx->device;
     const size_t b_rp = align_up((size_t)(n_checks + 1) * 4), b_ci = align_up((size_t)E * 4);
     const size_t b_cp = align_up((size_t)(n_vars + 1) * 4), b_cs = align_up((size_t)E * 4);
-    cudaError_t e = cudaMalloc(&code->mem, b_rp + b_ci + b_cp + b_cs);
+    const size_t b_vv = align_up((size_t)n_vars * 4), b_vs = align_up((size_t)E * 4);
+    cudaError_t e = cudaMalloc(&code->mem, b_rp + b_ci + b_cp + b_cs + b_vv + b_vs);
     if (e != cudaSuccess) {
         delete code;
         cudaGetLastError();
@@ -388,16 +419,40 @@ cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, cons
     int32_t *d_ci = reinterpret_cast<int32_t *>(base + b_rp);
     int32_t *d_cp = reinterpret_cast<int32_t *>(base + b_rp + b_ci);
     int32_t *d_cs = reinterpret_cast<int32_t *>(base + b_rp + b_ci + b_cp);
+    int32_t *d_vv = reinterpret_cast<int32_t *>(base + b_rp + b_ci + b_cp + b_cs);
+    int32_t *d_vs = reinterpret_cast<int32_t *>(base + b_rp + b_ci + b_cp + b_cs + b_vv);
     cudaError_t e1 = cudaMemcpy(d_rp, row_ptr, (size_t)(n_checks + 1) * 4, cudaMemcpyHostToDevice);
     cudaError_t e2 = cudaMemcpy(d_ci, col_idx, (size_t)E * 4, cudaMemcpyHostToDevice);
     cudaError_t e3 = cudaMemcpy(d_cp, col_ptr.data(), (size_t)(n_vars + 1) * 4, cudaMemcpyHostToDevice);
     cudaError_t e4 = cudaMemcpy(d_cs, csc_slot.data(), (size_t)E * 4, cudaMemcpyHostToDevice);
-    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess) {
+    cudaError_t e5 = cudaMemcpy(d_vv, vc_vars.data(), (size_t)n_vars * 4, cudaMemcpyHostToDevice);
+    cudaError_t e6 = cudaMemcpy(d_vs, vc_slots.data(), (size_t)E * 4, cudaMemcpyHostToDevice);
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess || e5 != cudaSuccess ||
+        e6 != cudaSuccess) {
         cudaFree(code->mem);
         delete code;
         return fail(CVSR_ECUDA, "code upload failed");
     }
-    code->d = CodeDev{n_vars, n_checks, E, d_rp, d_ci, d_cp, d_cs, max_dc, max_dv};
+    CodeDev d{};
+    d.n = n_vars;
+    d.M = n_checks;
+    d.E = E;
+    d.row_ptr = d_rp;
+    d.col_idx = d_ci;
+    d.col_ptr = d_cp;
+    d.csc_slot = d_cs;
+    d.max_dc = max_dc;
+    d.max_dv = max_dv;
+    d.vc_vars = d_vv;
+    d.vc_slots = d_vs;
+    d.n_vclass = n_cls;
+    for (int k = 0; k < MAX_VCLASS; ++k) {
+        d.vc_deg[k] = k < n_cls ? vc_deg[k] : 0;
+        d.vc_off[k] = k < n_cls ? vc_off[k] : 0;
+        d.vc_cnt[k] = k < n_cls ? vc_cnt[k] : 0;
+        d.vc_soff[k] = k < n_cls ? vc_soff[k] : 0;
+    }
+    code->d = d;
     *out = code;
     return CVSR_OK;
 }
@@ -556,8 +611,7 @@ cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float 
     launch_synd_transpose(synd, frames, cd.M, ds.st, tiles, s);
     launch_init_tiles(ds, nullptr, s);
     launch_set_counts(ds, tiles, s);
-    launch_vn(cd, ds, tiles, msg_clamp, true, nullptr, s);
-    int launched = 5;
+    int launched = 4 + launch_vn(cd, ds, tiles, msg_clamp, true, nullptr, s);
     for (int k = 1; k <= k_iters; ++k) {
         launch_cn(cd, ds, tiles, msg_clamp, 0, s);
         ++launched;
@@ -565,8 +619,7 @@ cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float 
             launch_from_interleaved(ds.msg, c2v_out, frames, cd.E, tiles, LN2, s);
             ++launched;
         }
-        launch_vn(cd, ds, tiles, msg_clamp, false, (k == k_iters) ? post_il : nullptr, s);
-        ++launched;
+        launched += launch_vn(cd, ds, tiles, msg_clamp, false, (k == k_iters) ? post_il : nullptr, s);
     }
     if (post_out) {
         launch_from_interleaved(post_il, post_out, frames, cd.n, tiles, LN2, s);

@@ -233,113 +233,124 @@ __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT <= 5) ? 4 : 3) k_cn(Cod
 }
 
 // ------------------------------------------------------------------ variable nodes
+//
+// Variables are processed per degree class (one launch per class): every warp
+// takes VPW variables of degree DV, loads all their slot indices with one
+// coalesced load (class-major slot table), then issues all VPW x (DV + 1)
+// 512-byte message/LLR loads before using any of them.
 
-// DV = the code's maximum variable degree handled in registers; a variable of
-// degree deg < DV uses the first deg slots (missing r are 0, the neutral sum).
-template <int DV, bool FIRST>
-__device__ __forceinline__ void vn_var(float4 *__restrict__ mt, const int (&slot)[DV], int deg, float4 Lv, bool any,
-                                       float qmax2, float4 &post) {
-    post = Lv;
-    if (!any) return;
-    if (FIRST) {
-        const float4 q = make_float4(clampf(Lv.x, qmax2), clampf(Lv.y, qmax2), clampf(Lv.z, qmax2), clampf(Lv.w, qmax2));
-#pragma unroll
-        for (int k = 0; k < DV; ++k)
-            if (k < deg) mt[(size_t)slot[k] * LANES] = q;
-        return;
-    }
-    float4 r[DV];
-#pragma unroll
-    for (int k = 0; k < DV; ++k) r[k] = (k < deg) ? mt[(size_t)slot[k] * LANES] : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int k = 0; k < DV; ++k) {
-        post.x += r[k].x;
-        post.y += r[k].y;
-        post.z += r[k].z;
-        post.w += r[k].w;
-    }
-#pragma unroll
-    for (int k = 0; k < DV; ++k)
-        if (k < deg)
-            mt[(size_t)slot[k] * LANES] = make_float4(clampf(post.x - r[k].x, qmax2), clampf(post.y - r[k].y, qmax2),
-                                                      clampf(post.z - r[k].z, qmax2), clampf(post.w - r[k].w, qmax2));
+__device__ __forceinline__ float4 add4(float4 a, const float4 &b) {
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+    return a;
+}
+__device__ __forceinline__ float4 vclamp_diff(const float4 &p, const float4 &r, float q) {
+    return make_float4(clampf(p.x - r.x, q), clampf(p.y - r.y, q), clampf(p.z - r.z, q), clampf(p.w - r.w, q));
 }
 
-template <bool FIRST>
-__device__ __noinline__ float4 vn_var_generic(float4 *__restrict__ mt, const int32_t *__restrict__ slots, int deg,
-                                              float4 Lv, bool any, float qmax2) {
-    float4 post = Lv;
-    if (!any) return post;
-    if (!FIRST) {
-        for (int k = 0; k < deg; ++k) {
-            const float4 r = mt[(size_t)slots[k] * LANES];
-            post.x += r.x;
-            post.y += r.y;
-            post.z += r.z;
-            post.w += r.w;
-        }
-    }
-    for (int k = 0; k < deg; ++k) {
-        float4 *p = mt + (size_t)slots[k] * LANES;
-        const float4 r = FIRST ? make_float4(0.f, 0.f, 0.f, 0.f) : *p;
-        *p = make_float4(clampf(post.x - r.x, qmax2), clampf(post.y - r.y, qmax2), clampf(post.z - r.z, qmax2),
-                         clampf(post.w - r.w, qmax2));
-    }
-    return post;
+__device__ __forceinline__ void vn_finish(const DecState &ds, const CodeDev &cd, int t, int v, const float4 &post,
+                                          const uint4 &act, bool any, int lane, float4 *post_dbg) {
+    // hard decisions (frames retired by the preceding status pass were copied out already)
+    uint4 word;
+    word.x = __ballot_sync(FULL, post.x < 0.0f) & act.x;
+    word.y = __ballot_sync(FULL, post.y < 0.0f) & act.y;
+    word.z = __ballot_sync(FULL, post.z < 0.0f) & act.z;
+    word.w = __ballot_sync(FULL, post.w < 0.0f) & act.w;
+    if (lane == 0) ds.hb[(size_t)t * cd.n + v] = word;
+    if (post_dbg && any) post_dbg[((size_t)t * cd.n + v) * LANES + lane] = post;
 }
 
-template <int DV, bool FIRST>
-__device__ __forceinline__ float4 vn_dispatch_one(float4 *mt, int sl, int off, int deg, float4 Lv, bool any,
-                                                  float qmax2) {
-    int slot[DV];
-#pragma unroll
-    for (int k = 0; k < DV; ++k) slot[k] = __shfl_sync(FULL, sl, (off + k) & 31);
-    float4 post;
-    vn_var<DV, FIRST>(mt, slot, deg, Lv, any, qmax2, post);
-    return post;
-}
-
-template <int DVT, bool FIRST>  // DVT = register-path max variable degree (1..8)
-__global__ void __launch_bounds__(BLOCK, DVT <= 6 ? 4 : 3) k_vn(CodeDev cd, DecState ds, float qmax2, float4 *post_dbg) {
+template <int DV, int VPW_, bool FIRST>
+__global__ void __launch_bounds__(BLOCK, 3) k_vn_cls(CodeDev cd, DecState ds, int cls, float qmax2,
+                                                     float4 *post_dbg) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
     const int t = ds.active_list[ti];
     const uint4 act = ds.tile_active[t];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int v0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * VPW;
-    const int nv = min(VPW, cd.n - v0);
+    const int w0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * VPW_;
+    const int cnt = cd.vc_cnt[cls];
+    const int nv = min(VPW_, cnt - w0);
     if (nv <= 0) return;
-    const int cp = (lane <= nv) ? cd.col_ptr[v0 + lane] : 0;
-    int lo[VPW + 1];
-#pragma unroll
-    for (int i = 0; i <= VPW; ++i) lo[i] = __shfl_sync(FULL, cp, i <= nv ? i : nv);
-    const int ebeg = lo[0], eend = lo[nv];
-    const bool staged = (eend - ebeg) <= 32;
-    const int sl = (staged && ebeg + lane < eend) ? cd.csc_slot[ebeg + lane] : 0;
+    const int vv = (lane < nv) ? cd.vc_vars[cd.vc_off[cls] + w0 + lane] : 0;
+    const int sl = (lane < nv * DV) ? cd.vc_slots[cd.vc_soff[cls] + (int64_t)w0 * DV + lane] : 0;
     const bool any = ((act.x | act.y | act.z | act.w) >> lane) & 1u;
-    float4 Lv[VPW];
+    int v[VPW_];
+    float4 Lv[VPW_];
 #pragma unroll
-    for (int i = 0; i < VPW; ++i)
-        Lv[i] = (i < nv && any) ? ds.L[((size_t)t * cd.n + v0 + i) * LANES + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 *mt = ds.msg + (size_t)t * cd.E * LANES + lane;
-    uint4 *hbt = ds.hb + (size_t)t * cd.n;
-#pragma unroll
-    for (int i = 0; i < VPW; ++i) {
-        if (i >= nv) break;
-        const int deg = lo[i + 1] - lo[i];
-        const int off = lo[i] - ebeg;
-        float4 post;
-        if (!staged || deg > DVT) post = vn_var_generic<FIRST>(mt, cd.csc_slot + lo[i], deg, Lv[i], any, qmax2);
-        else post = vn_dispatch_one<DVT, FIRST>(mt, sl, off, deg, Lv[i], any, qmax2);
-        // hard decisions (retired frames were copied out before this pass; their bits may change)
-        uint4 word;
-        word.x = __ballot_sync(FULL, post.x < 0.0f) & act.x;
-        word.y = __ballot_sync(FULL, post.y < 0.0f) & act.y;
-        word.z = __ballot_sync(FULL, post.z < 0.0f) & act.z;
-        word.w = __ballot_sync(FULL, post.w < 0.0f) & act.w;
-        if (lane == 0) hbt[v0 + i] = word;
-        if (post_dbg && any) post_dbg[((size_t)t * cd.n + v0 + i) * LANES + lane] = post;
+    for (int i = 0; i < VPW_; ++i) {
+        v[i] = __shfl_sync(FULL, vv, i);
+        Lv[i] = (i < nv && any) ? ds.L[((size_t)t * cd.n + v[i]) * LANES + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    float4 *mt = ds.msg + (size_t)t * cd.E * LANES + lane;
+    int slot[VPW_][DV];
+#pragma unroll
+    for (int i = 0; i < VPW_; ++i)
+#pragma unroll
+        for (int k = 0; k < DV; ++k) slot[i][k] = __shfl_sync(FULL, sl, i * DV + k);
+    if (FIRST) {
+#pragma unroll
+        for (int i = 0; i < VPW_; ++i) {
+            if (i >= nv) break;
+            if (any) {
+                const float4 q = make_float4(clampf(Lv[i].x, qmax2), clampf(Lv[i].y, qmax2), clampf(Lv[i].z, qmax2),
+                                             clampf(Lv[i].w, qmax2));
+#pragma unroll
+                for (int k = 0; k < DV; ++k) mt[(size_t)slot[i][k] * LANES] = q;
+            }
+            vn_finish(ds, cd, t, v[i], Lv[i], act, any, lane, post_dbg);
+        }
+        return;
+    }
+    float4 r[VPW_][DV];
+#pragma unroll
+    for (int i = 0; i < VPW_; ++i)
+#pragma unroll
+        for (int k = 0; k < DV; ++k)
+            r[i][k] = (i < nv && any) ? mt[(size_t)slot[i][k] * LANES] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < VPW_; ++i) {
+        if (i >= nv) break;
+        float4 post = Lv[i];
+#pragma unroll
+        for (int k = 0; k < DV; ++k) post = add4(post, r[i][k]);
+        if (any) {
+#pragma unroll
+            for (int k = 0; k < DV; ++k) mt[(size_t)slot[i][k] * LANES] = vclamp_diff(post, r[i][k], qmax2);
+        }
+        vn_finish(ds, cd, t, v[i], post, act, any, lane, post_dbg);
+    }
+}
+
+// any degree: one variable per warp, slots read per edge (mixed / large-degree classes)
+template <bool FIRST>
+__global__ void __launch_bounds__(BLOCK) k_vn_generic(CodeDev cd, DecState ds, int cls, float qmax2,
+                                                      float4 *post_dbg) {
+    const int ti = blockIdx.y;
+    if (ti >= ds.counts[0]) return;
+    const int t = ds.active_list[ti];
+    const uint4 act = ds.tile_active[t];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int w = blockIdx.x * WARPS_PER_BLOCK + warp;
+    if (w >= cd.vc_cnt[cls]) return;
+    const int v = cd.vc_vars[cd.vc_off[cls] + w];
+    const int beg = cd.col_ptr[v], deg = cd.col_ptr[v + 1] - beg;
+    const int32_t *slots = cd.csc_slot + beg;
+    const bool any = ((act.x | act.y | act.z | act.w) >> lane) & 1u;
+    float4 *mt = ds.msg + (size_t)t * cd.E * LANES + lane;
+    float4 post = any ? ds.L[((size_t)t * cd.n + v) * LANES + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (any) {
+        if (!FIRST)
+            for (int k = 0; k < deg; ++k) post = add4(post, mt[(size_t)slots[k] * LANES]);
+        for (int k = 0; k < deg; ++k) {
+            float4 *p = mt + (size_t)slots[k] * LANES;
+            const float4 r = FIRST ? make_float4(0.f, 0.f, 0.f, 0.f) : *p;
+            *p = vclamp_diff(post, r, qmax2);
+        }
+    }
+    vn_finish(ds, cd, t, v, post, act, any, lane, post_dbg);
 }
 
 // ------------------------------------------------------------------ scheduling
@@ -582,24 +593,47 @@ void launch_cn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax
     }
 }
 
-template <bool FIRST>
-static void launch_vn_t(const CodeDev &cd, const DecState &ds, dim3 grid, float q2, float4 *post_dbg, cudaStream_t s) {
-    const int dv = cd.max_dv;
-    if (dv <= 2) k_vn<2, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, q2, post_dbg);
-    else if (dv <= 3) k_vn<3, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, q2, post_dbg);
-    else if (dv <= 4) k_vn<4, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, q2, post_dbg);
-    else if (dv <= 6) k_vn<6, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, q2, post_dbg);
-    else if (dv <= 8) k_vn<8, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, q2, post_dbg);
-    else k_vn<2, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, q2, post_dbg);  // e.g. MET: degree-1 fast path, rest generic
+template <int DV, int VPW_, bool FIRST>
+static void launch_vn_cls(const CodeDev &cd, const DecState &ds, int cls, int grid_tiles, float q2, float4 *post_dbg,
+                          cudaStream_t s) {
+    const int per_block = WARPS_PER_BLOCK * VPW_;
+    dim3 grid((cd.vc_cnt[cls] + per_block - 1) / per_block, grid_tiles);
+    k_vn_cls<DV, VPW_, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, cls, q2, post_dbg);
 }
 
-void launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float4 *post_dbg,
-               cudaStream_t s) {
-    if (grid_tiles <= 0) return;
-    const int per_block = WARPS_PER_BLOCK * VPW;
-    dim3 grid((cd.n + per_block - 1) / per_block, grid_tiles);
-    if (first) launch_vn_t<true>(cd, ds, grid, qmax * LOG2E, post_dbg, s);
-    else launch_vn_t<false>(cd, ds, grid, qmax * LOG2E, post_dbg, s);
+template <bool FIRST>
+static int launch_vn_t(const CodeDev &cd, const DecState &ds, int grid_tiles, float q2, float4 *post_dbg,
+                       cudaStream_t s) {
+    int launched = 0;
+    for (int c = 0; c < cd.n_vclass; ++c) {
+        if (cd.vc_cnt[c] <= 0) continue;
+        ++launched;
+        switch (cd.vc_deg[c]) {
+            case 1: launch_vn_cls<1, 6, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 2: launch_vn_cls<2, 4, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 3: launch_vn_cls<3, 2, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 4: launch_vn_cls<4, 2, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 5: launch_vn_cls<5, 1, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 6: launch_vn_cls<6, 1, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 7: launch_vn_cls<7, 1, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 8: launch_vn_cls<8, 1, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 9: launch_vn_cls<9, 1, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 10: launch_vn_cls<10, 1, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            default: {
+                dim3 grid((cd.vc_cnt[c] + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, grid_tiles);
+                k_vn_generic<FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, c, q2, post_dbg);
+            }
+        }
+    }
+    return launched;
+}
+
+// returns the number of kernels launched (one per variable-degree class)
+int launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float4 *post_dbg,
+              cudaStream_t s) {
+    if (grid_tiles <= 0) return 0;
+    if (first) return launch_vn_t<true>(cd, ds, grid_tiles, qmax * LOG2E, post_dbg, s);
+    return launch_vn_t<false>(cd, ds, grid_tiles, qmax * LOG2E, post_dbg, s);
 }
 
 void launch_status(const DecState &ds, int k, int max_iter, int final_pass, int32_t *host_counts, cudaStream_t s) {

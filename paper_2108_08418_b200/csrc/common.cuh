@@ -20,6 +20,8 @@ constexpr int WARPS_PER_BLOCK = 8;
 constexpr int BLOCK = 32 * WARPS_PER_BLOCK;
 // largest check degree supported (cvsr_code_load rejects larger rows with CVSR_ECODE)
 constexpr int MAX_DC = 128;
+// variable-degree classes kept separate (more distinct degrees share a generic class)
+constexpr int MAX_VCLASS = 16;
 // arena values are LLR * log2(e)
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
@@ -34,6 +36,14 @@ struct CodeDev {
     const int32_t *col_ptr;   // [n+1]  CSC by variable
     const int32_t *csc_slot;  // [E]    CSR position of each CSC entry
     int32_t max_dc, max_dv;
+    // variables bucketed by degree (VN launches per class):
+    const int32_t *vc_vars;   // [n]  variables sorted by (degree, index)
+    const int32_t *vc_slots;  // [E]  their CSR slots, class-major, deg slots per variable
+    int32_t n_vclass;
+    int32_t vc_deg[MAX_VCLASS];    // degree of class (or -1: mixed degrees, generic path)
+    int32_t vc_off[MAX_VCLASS];    // first position in vc_vars
+    int32_t vc_cnt[MAX_VCLASS];    // number of variables
+    int64_t vc_soff[MAX_VCLASS];   // first position in vc_slots
 };
 
 // Per-decode device state (lives in the context's scratch arena).

@@ -6,8 +6,8 @@ namespace cvsr {
 
 // bp_kernels.cu
 void launch_cn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, int check_only, cudaStream_t s);
-void launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float4 *post_dbg,
-               cudaStream_t s);
+int launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float4 *post_dbg,
+              cudaStream_t s);
 void launch_status(const DecState &ds, int k, int max_iter, int final_pass, int32_t *host_counts, cudaStream_t s);
 void launch_retire(const DecState &ds, int32_t n, int grid_tiles, uint32_t *bits_out, cudaStream_t s);
 void launch_to_interleaved(const float *src, float4 *dst, int32_t F, int64_t rows, int tiles, float scale,
