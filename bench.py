@@ -170,6 +170,7 @@ def main():
 
     from cvsr_inputs.awgn import torch_quadratures
     from paper_2108_08418_b200 import cvsr
+    from paper_2108_08418_b200 import dist as cdist
     from paper_2108_08418_b200.pipeline import SRPipeline
 
     rank, world, local = dist_env()
@@ -184,7 +185,8 @@ def main():
     pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, device, cfg.max_iter, cfg.q_max,
                       stream)
     # rank r owns frames [r F, (r+1) F): per-frame-chunk seeding => identical data for any GPU count
-    x, y = torch_quadratures(F, n, cfg.gamma, device, first_frame=rank * F)
+    first, _ = cdist.shard(F, rank)
+    x, y = torch_quadratures(F, n, cfg.gamma, device, first_frame=first)
     torch.cuda.synchronize()
 
     # untimed reference run for statistics (the batch is identical every step)
@@ -247,23 +249,18 @@ def main():
         e2e = {"ms": e0.elapsed_time(e1), "h2d": 2 * F * n * 4, "d2h": F * n + F}
 
     # ---- reduce over ranks (the only collective: statistics + max time)
-    sums = torch.tensor([bits_per_step, st["frames"], st["frames_ok"], undetected] + st["iters_sum"] +
-                        st["edge_iters"], dtype=torch.float64, device=device)
-    tmax = torch.tensor([t_ms, e2e["ms"] if e2e else 0.0], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    sums = sums.cpu().numpy()
-    tmax = tmax.cpu().numpy()
+    red, iters_sum, edge_iters, tmax = cdist.reduce_stats(
+        {"bits": bits_per_step, "frames": st["frames"], "frames_ok": st["frames_ok"], "undetected": undetected},
+        st["iters_sum"], st["edge_iters"], [t_ms, e2e["ms"] if e2e else 0.0], device)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         pipe.close()
         return
     m = cfg.m
-    bits_step, frames_all, ok_all, undet = sums[0], sums[1], sums[2], sums[3]
-    iters_sum = sums[4:4 + m]
-    edge_iters = sums[4 + m:4 + 2 * m]
+    bits_step, frames_all, ok_all, undet = red["bits"], red["frames"], red["frames_ok"], red["undetected"]
+    iters_sum = np.array(iters_sum)
+    edge_iters = np.array(edge_iters)
     ms_step = tmax[0] / args.steps
     value = bits_step / (ms_step * 1e-3)
     fer = 1.0 - ok_all / frames_all
@@ -293,6 +290,19 @@ def main():
                     "launches_per_step": cn_n / args.steps, "avg_launch_us": 1e3 * cn_ms / max(cn_n, 1),
                     "bytes_per_launch": cn_bytes / max(cn_n / args.steps, 1), "peak_source": peak_src,
                     "share_of_step": cn_ms / args.steps / ms_step}
+        # DRAM traffic of k_cn from the committed ncu --set full capture (profiles/ncu_traffic.json),
+        # as bytes per edge-frame scaled to this run's average launch
+        tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tj):
+            with open(tj) as f:
+                tr = json.load(f)
+            cn_caps = [k for k in tr["kernels"] if "k_cn" in k["kernel"]]
+            if cn_caps and tr.get("k_cn_edge_frames"):
+                per_ef = (cn_caps[0]["dram_read_mb"] + cn_caps[0]["dram_write_mb"]) * 1e6 / tr["k_cn_edge_frames"]
+                roofline["traffic"] = per_ef * edge_it_rank / max(cn_n / args.steps, 1)
+                roofline["traffic_note"] = (f"ncu dram read+write of one full-tile k_cn launch ({tr['source']}) = "
+                                            f"{per_ef:.2f} B per edge-frame vs 8 algorithmic, times this run's "
+                                            f"edge-frames per launch")
         it_bytes = 8.0 * edge_it_rank + 4.0 * var_it_rank
         it_ach = it_bytes * args.steps / ((cn_ms + vn_ms) * 1e-3) / 1e9
         extra["roofline_bp_iteration"] = {

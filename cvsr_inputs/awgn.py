@@ -58,21 +58,24 @@ def torch_quadratures(frames: int, n: int, gamma: float, device, seed: int = DAT
                       first_frame: int = 0, chunk: int = 64):
     """Device-side generator for benchmark-size batches (torch Philox per frame chunk).
 
-    Different bits from :func:`quadratures` (different generator) but the same
-    distribution and the same chunk-seeding rule; both implementations consume
-    whatever arrays are produced, so parity is unaffected.
+    Frames are generated in GLOBAL chunks of `chunk` frames, chunk c seeded by
+    (seed, c), so frame f's data does not depend on how frames are sharded
+    across ranks.  Different bits from :func:`quadratures` (another generator)
+    but the same distribution; both implementations consume whatever arrays
+    are produced, so parity is unaffected.
     """
     import torch
     sigma_n = float(1.0 / np.sqrt(gamma))
     x = torch.empty((frames, n), dtype=torch.float32, device=device)
     y = torch.empty((frames, n), dtype=torch.float32, device=device)
     g = torch.Generator(device=device)
-    for c0 in range(0, frames, chunk):
-        c1 = min(frames, c0 + chunk)
-        chunk_id = (first_frame + c0) // chunk
-        g.manual_seed((seed * 1000003 + chunk_id) & 0x7FFFFFFFFFFFFFFF)
-        xs = torch.randn((c1 - c0, n), generator=g, device=device, dtype=torch.float32)
-        ns = torch.randn((c1 - c0, n), generator=g, device=device, dtype=torch.float32)
-        x[c0:c1] = xs
-        y[c0:c1] = xs + sigma_n * ns
+    last = first_frame + frames
+    for cid in range(first_frame // chunk, (last + chunk - 1) // chunk):
+        g.manual_seed((seed * 1000003 + cid) & 0x7FFFFFFFFFFFFFFF)
+        xs = torch.randn((chunk, n), generator=g, device=device, dtype=torch.float32)
+        ns = torch.randn((chunk, n), generator=g, device=device, dtype=torch.float32)
+        lo, hi = max(first_frame, cid * chunk), min(last, (cid + 1) * chunk)
+        a, b = lo - cid * chunk, hi - cid * chunk
+        x[lo - first_frame:hi - first_frame] = xs[a:b]
+        y[lo - first_frame:hi - first_frame] = xs[a:b] + sigma_n * ns[a:b]
     return x, y
