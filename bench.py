@@ -192,6 +192,18 @@ def main():
     # untimed reference run for statistics (the batch is identical every step)
     st = pipe.step(x, y, want_stats=True)
     undetected = pipe.count_errors()[1]
+    # scheduling diagnostic: executed / useful frame-iterations if whole groups of g frames
+    # iterate until their slowest member stops (g = 128 tile, 32 sub-tile, 8 = one 32-B sector)
+    it_h = pipe.iters.cpu().numpy()
+    waste = {}
+    for j in range(cfg.m):
+        d = it_h[:, j].astype(np.float64)
+        if codes_l[j] is None or (d < 0).all():
+            continue
+        d = np.where(d < 0, 0, d) + 1.0  # + the final syndrome-test pass
+        waste[str(j)] = {str(g): float((d[: len(d) // g * g].reshape(-1, g).max(axis=1) * g).sum() /
+                                       d[: len(d) // g * g].sum()) for g in (128, 32, 8)}
+        waste[str(j)]["max_iters"] = int(d.max() - 1)
     # frames whose labels differ from Bob's would fail the hash check of PAPER.md:90;
     # only verified frames count as reconciled (ideal hash in simulation)
     bits_per_step = (st["frames_ok"] - undetected) * cfg.m * n
@@ -331,6 +343,7 @@ def main():
                    "l2": "inputs and message arena > L2 (no flush needed)", "parallelism": f"frames sharded x{world}"},
         "fer": fer, "beta": beta, "undetected_frames": int(undet),
         "mean_iters": [float(iters_sum[j] / max(frames_all, 1)) for j in range(m)],
+        "group_waste_rank0": waste,
         "symbols_per_s": frames_all * n / (ms_step * 1e-3),
         "decoded_slice_bits_per_s": frames_all * n * sum(c is not None for c in codes_l) / (ms_step * 1e-3),
         "paper_ops_per_s": ops / (ms_step * 1e-3),

@@ -17,36 +17,43 @@ namespace cvsr {
 
 constexpr float RSQRT2 = 0.70710678118654752f;
 
-__device__ __forceinline__ float log_q(float z) {
-    if (z >= 0.0f) return logf(0.5f * erfcxf(z * RSQRT2)) - 0.5f * z * z;
-    return log1pf(-0.5f * erfcf(-z * RSQRT2));
+// Upper-tail pieces of the standard normal at |z|: Q(|z|) = t * exp(e),
+// t = erfcx(|z|/sqrt2)/2, e = -z^2/2 (erfcx keeps t accurate in the far tail).
+struct Tail {
+    float t, e;
+};
+__device__ __forceinline__ Tail tail_of(float z) {
+    const float a = fabsf(z);
+    return Tail{0.5f * erfcxf(a * RSQRT2), -0.5f * a * a};
 }
 
-// log(1 - e^d) for d < 0
-__device__ __forceinline__ float log1m_exp(float d) { return logf(-expm1f(d)); }
-
-__device__ __forceinline__ float log_bin(const float *se, int b, int nb, float x, float inv_sigma) {
-    const bool lo_inf = (b == 0), hi_inf = (b == nb - 1);
-    if (lo_inf && hi_inf) return 0.0f;
-    const float lo = lo_inf ? 0.0f : (se[b - 1] - x) * inv_sigma;
-    const float hi = hi_inf ? 0.0f : (se[b] - x) * inv_sigma;
-    if (lo_inf) return log_q(-hi);
-    if (hi_inf) return log_q(lo);
-    if (lo >= 0.0f) {
-        const float a = log_q(lo), c = log_q(hi);
-        return a + log1m_exp(c - a);
-    }
-    if (hi <= 0.0f) {
-        const float a = log_q(-hi), c = log_q(-lo);
-        return a + log1m_exp(c - a);
-    }
-    return logf(0.5f * (erff(hi * RSQRT2) + erff(-lo * RSQRT2)));
+// log P(lo <= Z < hi), Z ~ N(0,1), lo < hi (either may be infinite).  The bin is
+// mirrored to the upper half when it lies below 0; then
+//   a >= 0 (whole bin in the upper tail): log Q(a) + log(1 - Q(b)/Q(a))
+//   a < 0 < b (straddles the mean)      : log(1 - Q(|a|) - Q(b))
+// Both forms use the same two erfcx evaluations; the selection is branch-free.
+__device__ __forceinline__ float log_bin(float lo, float hi, bool lo_inf, bool hi_inf) {
+    const bool mirror = !hi_inf && hi <= 0.0f;
+    const float a = mirror ? -hi : lo, b = mirror ? -lo : hi;
+    const bool a_inf = mirror ? false : lo_inf;   // a = -inf only if lo = -inf (not mirrored)
+    const bool b_inf = mirror ? lo_inf : hi_inf;  // b = +inf
+    const Tail ta = tail_of(a_inf ? 0.0f : a), tb = tail_of(b_inf ? 0.0f : b);
+    const float lqa = __logf(ta.t) + ta.e;                      // log Q(|a|)
+    const float lqb = b_inf ? -INFINITY : __logf(tb.t) + tb.e;  // log Q(b)
+    // tail form (a >= 0): log Q(a) + log(-expm1(log Q(b) - log Q(a)))
+    const float tail = b_inf ? lqa : lqa + __logf(-expm1f(lqb - lqa));
+    // straddle form (a < 0 < b): 1 - Q(|a|) - Q(b); a = -inf gives Q(|a|) -> 0
+    const float qa = a_inf ? 0.0f : ta.t * __expf(ta.e);
+    const float qb = b_inf ? 0.0f : tb.t * __expf(tb.e);
+    const float strad = log1pf(-(qa + qb));
+    if (a_inf && b_inf) return 0.0f;
+    return (!a_inf && a >= 0.0f) ? tail : strad;
 }
 
 __device__ __forceinline__ float log_add(float a, float b) {
     const float mx = fmaxf(a, b), mn = fminf(a, b);
     if (mx == -INFINITY) return -INFINITY;
-    return mx + log1pf(expf(mn - mx));
+    return mx + log1pf(__expf(mn - mx));
 }
 
 __device__ __forceinline__ uint32_t gray_inv(uint32_t g) {
@@ -65,7 +72,11 @@ __device__ float llr_cond(const float *se, int m, int j, uint32_t kmask, uint32_
     uint32_t sub = 0u;
     do {
         const uint32_t g = base | sub;
-        const float lp = log_bin(se, (int)gray_inv(g), nb, x, inv_sigma);
+        const int b = (int)gray_inv(g);
+        const bool lo_inf = (b == 0), hi_inf = (b == nb - 1);
+        const float lo = lo_inf ? 0.0f : (se[b - 1] - x) * inv_sigma;
+        const float hi = hi_inf ? 0.0f : (se[b] - x) * inv_sigma;
+        const float lp = log_bin(lo, hi, lo_inf, hi_inf);
         if ((g >> j) & 1u) ln1 = log_add(ln1, lp);
         else ln0 = log_add(ln0, lp);
         sub = (sub - free_mask) & free_mask;
