@@ -141,6 +141,7 @@ cvsr_status scratch_reserve(cvsr_ctx *ctx, size_t bytes, char **out) {
 }
 
 size_t decstate_bytes(int tiles, int frames, int64_t n, int64_t M, int64_t E) {
+    const size_t T = (size_t)LANES * choose_subs(frames);
     size_t b = 0;
     b += align_up((size_t)tiles * E * T * sizeof(float));
     b += align_up((size_t)tiles * n * T * sizeof(float));
@@ -158,8 +159,11 @@ DecState carve_decstate(Carve &cv, int tiles, int frames, int64_t n, int64_t M, 
     DecState ds{};
     ds.tiles = tiles;
     ds.frames = frames;
-    ds.msg = cv.take<float4>((size_t)tiles * E * T * sizeof(float));
-    ds.L = cv.take<float4>((size_t)tiles * n * T * sizeof(float));
+    ds.subs = choose_subs(frames);
+    ds.tile_frames = LANES * ds.subs;
+    const size_t T = (size_t)ds.tile_frames;
+    ds.msg = cv.take<float>((size_t)tiles * E * T * sizeof(float));
+    ds.L = cv.take<float>((size_t)tiles * n * T * sizeof(float));
     ds.hb = cv.take<uint4>((size_t)tiles * n * sizeof(uint4));
     ds.st = cv.take<uint4>((size_t)tiles * M * sizeof(uint4));
     ds.tile_active = cv.take<uint4>((size_t)tiles * sizeof(uint4));
@@ -572,14 +576,14 @@ cvsr_status cvsr_decode(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, 
     if (!llr || !synd || !bits_out || !converged_out || !iters_out) return fail(CVSR_EINVAL, "null buffer");
     DeviceGuard g(ctx->device);
     const CodeDev &cd = code->d;
-    const int tiles = (frames + T - 1) / T;
+    const int tiles = (frames + LANES * choose_subs(frames) - 1) / (LANES * choose_subs(frames));
     char *base;
     if (cvsr_status st = scratch_reserve(ctx, decstate_bytes(tiles, frames, cd.n, cd.M, cd.E), &base)) return st;
     Carve cv{base};
     DecState ds = carve_decstate(cv, tiles, frames, cd.n, cd.M, cd.E, iters_out, converged_out);
     cudaStream_t s = ctx->stream;
-    launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, LOG2E, s);
-    launch_synd_transpose(synd, frames, cd.M, ds.st, tiles, s);
+    launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, ds.subs, LOG2E, s);
+    launch_synd_transpose(synd, frames, cd.M, ds.subs, ds.st, tiles, s);
     launch_init_tiles(ds, nullptr, s);
     launch_set_counts(ds, tiles, s);
     if (cvsr_status st = check_launch(ctx, 4)) return st;
@@ -598,17 +602,17 @@ cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float 
     if (!llr || !synd) return fail(CVSR_EINVAL, "null buffer");
     DeviceGuard g(ctx->device);
     const CodeDev &cd = code->d;
-    const int tiles = (frames + T - 1) / T;
-    const size_t post_bytes = align_up((size_t)tiles * cd.n * T * sizeof(float));
+    const int tiles = (frames + LANES * choose_subs(frames) - 1) / (LANES * choose_subs(frames));
+    const size_t post_bytes = align_up((size_t)tiles * cd.n * LANES * choose_subs(frames) * sizeof(float));
     char *base;
     if (cvsr_status st = scratch_reserve(ctx, decstate_bytes(tiles, frames, cd.n, cd.M, cd.E) + post_bytes, &base))
         return st;
     Carve cv{base};
     DecState ds = carve_decstate(cv, tiles, frames, cd.n, cd.M, cd.E, nullptr, nullptr);
-    float4 *post_il = cv.take<float4>(post_bytes);
+    float *post_il = cv.take<float>(post_bytes);
     cudaStream_t s = ctx->stream;
-    launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, LOG2E, s);
-    launch_synd_transpose(synd, frames, cd.M, ds.st, tiles, s);
+    launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, ds.subs, LOG2E, s);
+    launch_synd_transpose(synd, frames, cd.M, ds.subs, ds.st, tiles, s);
     launch_init_tiles(ds, nullptr, s);
     launch_set_counts(ds, tiles, s);
     int launched = 4 + launch_vn(cd, ds, tiles, msg_clamp, true, nullptr, s);
@@ -616,13 +620,13 @@ cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float 
         launch_cn(cd, ds, tiles, msg_clamp, 0, s);
         ++launched;
         if (k == k_iters && c2v_out) {
-            launch_from_interleaved(ds.msg, c2v_out, frames, cd.E, tiles, LN2, s);
+            launch_from_interleaved(ds.msg, c2v_out, frames, cd.E, tiles, ds.subs, LN2, s);
             ++launched;
         }
         launched += launch_vn(cd, ds, tiles, msg_clamp, false, (k == k_iters) ? post_il : nullptr, s);
     }
     if (post_out) {
-        launch_from_interleaved(post_il, post_out, frames, cd.n, tiles, LN2, s);
+        launch_from_interleaved(post_il, post_out, frames, cd.n, tiles, ds.subs, LN2, s);
         ++launched;
     }
     return check_launch(ctx, launched);
@@ -661,7 +665,7 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
     }
     if (!x || !label_out || !frame_ok || !iters) return fail(CVSR_EINVAL, "null buffer");
     DeviceGuard g(ctx->device);
-    const int tiles = (frames + T - 1) / T;
+    const int tiles = (frames + LANES * choose_subs(frames) - 1) / (LANES * choose_subs(frames));
     const int Wn = words_of(n);
     size_t bytes = decstate_bytes(tiles, frames, n, maxM, maxE);
     bytes += (size_t)m * align_up((size_t)frames * Wn * 4) + 3 * align_up((size_t)frames);
@@ -692,12 +696,12 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
             CK(cudaMemsetAsync(bits_dec[j], 0, (size_t)frames * Wn * 4, s));
             launch_init_tiles(ds, alive, s);
             launch_set_counts(ds, tiles, s);
-            launch_synd_transpose(synd[j], frames, cd.M, ds.st, tiles, s);
+            launch_synd_transpose(synd[j], frames, cd.M, ds.subs, ds.st, tiles, s);
             LlrParams p;
             fill_llr_params(p, q, j, known_mask, sigma_n, opts->msg_clamp);
             for (int jj = 0; jj < m; ++jj) p.known_bits[jj] = known_bits[jj];
             prof_begin(ctx, KC_INIT);
-            launch_llr_interleaved(p, x, frames, n, tiles, ds.L, s);
+            launch_llr_interleaved(p, x, frames, n, tiles, ds.subs, ds.L, s);
             prof_end(ctx);
             launched += 4;
             if (cvsr_status st = check_launch(ctx, 0)) return st;

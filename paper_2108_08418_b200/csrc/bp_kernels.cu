@@ -1,17 +1,17 @@
 // Sum-product BP kernels for sm_100a.
 //
-// Layout ("frame-interleaved arena"): a tile holds T = 128 frames; lane l of a
-// warp owns frames {128 t + 32 s + l : s = 0..3} as one float4.  For every edge
-// slot (CSR position) the 128 frames' messages are 512 contiguous bytes, so a
-// warp moves one 512-byte line per edge with one 16-byte access per lane.
-// Messages are stored IN PLACE: the CN pass reads V2C q_e and overwrites it
-// with C2V r_e; the VN pass reads r_e and overwrites it with the next q_e.
-// Arena values are in log2 units (LLR * log2 e): every exp/log below is then a
-// single MUFU ex2/lg2; conversion happens once at the arena boundary (LLR
-// load, trace dumps).  Each warp handles CPW consecutive checks (VPW
-// consecutive variables) so that one row_ptr/col_ptr load serves several
-// rows, and the syndrome test is reduced after the message pass so that its
-// gathers overlap the message traffic.
+// Layout ("frame-interleaved arena"): a tile holds 32 S frames (S = 1, 2, 4);
+// lane l of a warp owns frames {32 S t + 32 s + l : s < S} as one float/float2/
+// float4.  For every edge slot (CSR position) the tile's messages are 128 S
+// contiguous bytes, so a warp moves one 128 S-byte line per edge with one
+// 4 S-byte access per lane.  Messages are stored IN PLACE: the CN pass reads
+// V2C q_e and overwrites it with C2V r_e; the VN pass reads r_e and overwrites
+// it with the next q_e.  Arena values are in log2 units (LLR * log2 e): every
+// exp/log below is a single MUFU ex2/lg2; conversion happens once at the arena
+// boundary (LLR load, trace dumps).  Each warp handles CPW consecutive checks
+// so that one row_ptr load serves several rows, and the syndrome test is
+// reduced after the message pass so its gathers overlap the message traffic.
+// Variables are processed per degree class (one launch per class).
 //
 // Algorithm (PAPER.md:189 BP decoder, PAPER.md:231 message passes; SURVEY.md
 // §8(c) O5 readings A-8 flooding, A-10 V2C clamp, A-12 stopping rule):
@@ -29,12 +29,12 @@
 //   The syndrome test H xhat = s of iteration k-1 is fused into CN pass k.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "vec.cuh"
 
 namespace cvsr {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int CPW = 4;  // checks per warp
-constexpr int VPW = 4;  // variables per warp
 
 __device__ __forceinline__ float ex2f(float x) {
     float y;
@@ -54,19 +54,16 @@ __device__ __forceinline__ float rcpf(float x) {
 // a (+) b = 1 - (1 - a)(1 - b)
 __device__ __forceinline__ float cplus(float a, float b) { return fmaf(b, 1.0f - a, a); }
 __device__ __forceinline__ uint32_t sgnbit(float x) { return __float_as_uint(x) >> 31; }
-
-__device__ __forceinline__ float cmp4(const float4 &v, int s) { return s == 0 ? v.x : s == 1 ? v.y : s == 2 ? v.z : v.w; }
-__device__ __forceinline__ void set4(float4 &v, int s, float x) {
-    if (s == 0) v.x = x;
-    else if (s == 1) v.y = x;
-    else if (s == 2) v.z = x;
-    else v.w = x;
-}
-__device__ __forceinline__ uint32_t cmpu(const uint4 &v, int s) { return s == 0 ? v.x : s == 1 ? v.y : s == 2 ? v.z : v.w; }
-__device__ __forceinline__ uint4 lanebits4(const uint4 &m, int lane) {
-    return make_uint4((m.x >> lane) & 1u, (m.y >> lane) & 1u, (m.z >> lane) & 1u, (m.w >> lane) & 1u);
-}
 __device__ __forceinline__ float clampf(float x, float lim) { return fminf(fmaxf(x, -lim), lim); }
+
+// this lane's active bit per sub-tile, and "any" over the lane's S frames
+template <int S>
+__device__ __forceinline__ uint32_t lane_act(const uint4 &m, int lane) {
+    uint32_t a = 0u;
+#pragma unroll
+    for (int s = 0; s < S; ++s) a |= ((cmpu(m, s) >> lane) & 1u) << s;
+    return a;
+}
 
 // ------------------------------------------------------------------ check nodes
 
@@ -95,44 +92,43 @@ __device__ __forceinline__ void cn_update(float (&q)[DC], uint32_t sbit, float q
     }
 }
 
-// One check, 4 frames per lane (al = this lane's active bit per sub-tile).
-// DC is the code's maximum check degree; a check of degree deg < DC is padded
-// with "certain" dummy edges (|q| = 200 in log2 units: w = 0, the neutral
-// element of (+), sign +), which are neither loaded nor stored.  One code body
-// per code keeps the instruction cache hot.
+// One check for the S frames of this lane.  DC is the code's maximum check
+// degree; a check of degree deg < DC is padded with "certain" dummy edges
+// (|q| = 200 in log2 units: w = 0, the neutral element of (+), sign +), which
+// are neither loaded nor stored: one code body per code keeps the i-cache hot.
 constexpr float DUMMY_Q = 200.0f;
 
-template <int DC>
-__device__ __forceinline__ void cn_check(float4 *__restrict__ m, int deg, const uint4 &sb, const uint4 &al,
-                                         float qmax2) {
-    if (!(al.x | al.y | al.z | al.w)) return;
-    float4 q[DC];
+template <int DC, int S>
+__device__ __forceinline__ void cn_check(float *__restrict__ m, int deg, uint32_t sb, uint32_t al, float qmax2) {
+    if (!al) return;
+    FV<S> q[DC];
 #pragma unroll
-    for (int k = 0; k < DC; ++k) q[k] = (k < deg) ? m[(size_t)k * LANES] : make_float4(DUMMY_Q, DUMMY_Q, DUMMY_Q, DUMMY_Q);
+    for (int k = 0; k < DC; ++k) q[k] = (k < deg) ? ldv<S>(m + (size_t)k * LANES * S) : splat<S>(DUMMY_Q);
 #pragma unroll
-    for (int s = 0; s < SUBS; ++s) {
-        if (!cmpu(al, s)) continue;
+    for (int s = 0; s < S; ++s) {
+        if (!((al >> s) & 1u)) continue;
         float a[DC];
 #pragma unroll
-        for (int k = 0; k < DC; ++k) a[k] = cmp4(q[k], s);
-        cn_update<DC>(a, cmpu(sb, s), qmax2);
+        for (int k = 0; k < DC; ++k) a[k] = q[k].c[s];
+        cn_update<DC>(a, (sb >> s) & 1u, qmax2);
 #pragma unroll
-        for (int k = 0; k < DC; ++k) set4(q[k], s, a[k]);
+        for (int k = 0; k < DC; ++k) q[k].c[s] = a[k];
     }
 #pragma unroll
     for (int k = 0; k < DC; ++k)
-        if (k < deg) m[(size_t)k * LANES] = q[k];
+        if (k < deg) stv<S>(m + (size_t)k * LANES * S, q[k]);
 }
 
-// any degree up to MAX_DC (rare): w and suffix complements in thread-local arrays
-__device__ __noinline__ void cn_check_generic(float4 *__restrict__ m, int deg, uint4 sb, uint4 al, float qmax2) {
+// any degree up to MAX_DC (codes with a check degree > 8): w and suffix
+// complements in thread-local arrays
+template <int S>
+__device__ __noinline__ void cn_check_generic(float *__restrict__ m, int deg, uint32_t sb, uint32_t al, float qmax2) {
     float wl[MAX_DC], sf[MAX_DC + 1];
-    float *mf = reinterpret_cast<float *>(m);
-    for (int s = 0; s < SUBS; ++s) {
-        if (!cmpu(al, s)) continue;
-        uint32_t par = cmpu(sb, s);
+    for (int s = 0; s < S; ++s) {
+        if (!((al >> s) & 1u)) continue;
+        uint32_t par = (sb >> s) & 1u;
         for (int k = 0; k < deg; ++k) {
-            const float qk = mf[(size_t)k * LANES * 4 + s];
+            const float qk = m[(size_t)k * LANES * S + s];
             par ^= sgnbit(qk);
             const float u = ex2f(-fabsf(qk));
             wl[k] = 2.0f * u * rcpf(1.0f + u);
@@ -141,7 +137,7 @@ __device__ __noinline__ void cn_check_generic(float4 *__restrict__ m, int deg, u
         for (int k = deg - 1; k >= 0; --k) sf[k] = cplus(sf[k + 1], wl[k]);
         float pre = 0.0f;
         for (int k = 0; k < deg; ++k) {
-            float *p = mf + (size_t)k * LANES * 4 + s;
+            float *p = m + (size_t)k * LANES * S + s;
             const float c = cplus(pre, sf[k + 1]);
             const float mag = fmaxf(fminf(lg2f((2.0f - c) * rcpf(c)), qmax2), 0.0f);
             pre = cplus(pre, wl[k]);
@@ -150,8 +146,9 @@ __device__ __noinline__ void cn_check_generic(float4 *__restrict__ m, int deg, u
     }
 }
 
-template <int DCT>  // DCT = max check degree (templated body) or 0 = generic only
-__global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT <= 5) ? 4 : 3) k_cn(CodeDev cd, DecState ds, float qmax2, int check_only) {
+template <int DCT, int S>  // DCT = max check degree (templated body) or 0 = generic
+__global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 20) ? 4 : 3)
+    k_cn(CodeDev cd, DecState ds, float qmax2, int check_only) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
     const int t = ds.active_list[ti];
@@ -181,16 +178,16 @@ __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT <= 5) ? 4 : 3) k_cn(Cod
         uint4 h = make_uint4(0u, 0u, 0u, 0u);
         if (e < eend) h = hbt[cd.col_idx[e]];
         if (!check_only) {
-            const uint4 al = lanebits4(act, lane);
-            float4 *mt = ds.msg + (size_t)t * cd.E * LANES + lane;
+            const uint32_t al = lane_act<S>(act, lane);
+            float *mt = ds.msg + (size_t)t * cd.E * LANES * S + (size_t)lane * S;
 #pragma unroll
             for (int i = 0; i < CPW; ++i) {
                 if (i < nc) {
                     const int deg = lo[i + 1] - lo[i];
-                    float4 *m = mt + (size_t)lo[i] * LANES;
-                    const uint4 sb = lanebits4(par[i], lane);
-                    if constexpr (DCT > 0) cn_check<DCT>(m, deg, sb, al, qmax2);  // DCT = max_dc >= deg
-                    else cn_check_generic(m, deg, sb, al, qmax2);
+                    float *m = mt + (size_t)lo[i] * LANES * S;
+                    const uint32_t sb = lane_act<S>(par[i], lane);
+                    if constexpr (DCT > 0) cn_check<DCT, S>(m, deg, sb, al, qmax2);  // DCT = max_dc >= deg
+                    else cn_check_generic<S>(m, deg, sb, al, qmax2);
                 }
             }
         }
@@ -200,9 +197,11 @@ __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT <= 5) ? 4 : 3) k_cn(Cod
             for (int i = 0; i < CPW; ++i) {
                 const bool in = (i < nc) && e >= lo[i] && e < lo[i + 1];
                 par[i].x ^= __reduce_xor_sync(FULL, in ? h.x : 0u);
-                par[i].y ^= __reduce_xor_sync(FULL, in ? h.y : 0u);
-                par[i].z ^= __reduce_xor_sync(FULL, in ? h.z : 0u);
-                par[i].w ^= __reduce_xor_sync(FULL, in ? h.w : 0u);
+                if (S > 1) par[i].y ^= __reduce_xor_sync(FULL, in ? h.y : 0u);
+                if (S > 2) {
+                    par[i].z ^= __reduce_xor_sync(FULL, in ? h.z : 0u);
+                    par[i].w ^= __reduce_xor_sync(FULL, in ? h.w : 0u);
+                }
             }
             e0 += 32;
             if (e0 >= eend) break;
@@ -216,7 +215,7 @@ __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT <= 5) ? 4 : 3) k_cn(Cod
             u.x |= par[i].x; u.y |= par[i].y; u.z |= par[i].z; u.w |= par[i].w;
         }
         u.x &= act.x; u.y &= act.y; u.z &= act.z; u.w &= act.w;
-        if (lane < SUBS) {
+        if (lane < S) {
             const uint32_t v = cmpu(u, lane);
             if (v) atomicOr(&s_unsat[lane], v);
         }
@@ -226,7 +225,7 @@ __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT <= 5) ? 4 : 3) k_cn(Cod
     int last = 0;
     if (lane == 0) last = (atomicAdd(&s_done, 1) == WARPS_PER_BLOCK - 1);
     last = __shfl_sync(FULL, last, 0);
-    if (last && lane < SUBS) {
+    if (last && lane < S) {
         const uint32_t v = atomicOr(&s_unsat[lane], 0u);
         if (v) atomicOr(reinterpret_cast<uint32_t *>(&ds.tile_unsat[t]) + lane, v);
     }
@@ -234,37 +233,24 @@ __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT <= 5) ? 4 : 3) k_cn(Cod
 
 // ------------------------------------------------------------------ variable nodes
 //
-// Variables are processed per degree class (one launch per class): every warp
-// takes VPW variables of degree DV, loads all their slot indices with one
-// coalesced load (class-major slot table), then issues all VPW x (DV + 1)
-// 512-byte message/LLR loads before using any of them.
+// Per degree class: every warp takes VPW variables of degree DV, loads all
+// their slot indices with one coalesced load (class-major slot table), then
+// issues all VPW x (DV + 1) line loads before using any of them.
 
-__device__ __forceinline__ float4 add4(float4 a, const float4 &b) {
-    a.x += b.x;
-    a.y += b.y;
-    a.z += b.z;
-    a.w += b.w;
-    return a;
-}
-__device__ __forceinline__ float4 vclamp_diff(const float4 &p, const float4 &r, float q) {
-    return make_float4(clampf(p.x - r.x, q), clampf(p.y - r.y, q), clampf(p.z - r.z, q), clampf(p.w - r.w, q));
-}
-
-__device__ __forceinline__ void vn_finish(const DecState &ds, const CodeDev &cd, int t, int v, const float4 &post,
-                                          const uint4 &act, bool any, int lane, float4 *post_dbg) {
+template <int S>
+__device__ __forceinline__ void vn_finish(const DecState &ds, const CodeDev &cd, int t, int v, const FV<S> &post,
+                                          const uint4 &act, uint32_t any, int lane, float *post_dbg) {
     // hard decisions (frames retired by the preceding status pass were copied out already)
-    uint4 word;
-    word.x = __ballot_sync(FULL, post.x < 0.0f) & act.x;
-    word.y = __ballot_sync(FULL, post.y < 0.0f) & act.y;
-    word.z = __ballot_sync(FULL, post.z < 0.0f) & act.z;
-    word.w = __ballot_sync(FULL, post.w < 0.0f) & act.w;
-    if (lane == 0) ds.hb[(size_t)t * cd.n + v] = word;
-    if (post_dbg && any) post_dbg[((size_t)t * cd.n + v) * LANES + lane] = post;
+    uint32_t wd[SUBS] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int s = 0; s < S; ++s) wd[s] = __ballot_sync(FULL, post.c[s] < 0.0f) & cmpu(act, s);
+    if (lane == 0) ds.hb[(size_t)t * cd.n + v] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    if (post_dbg && any) stv<S>(post_dbg + (((size_t)t * cd.n + v) * LANES + lane) * S, post);
 }
 
-template <int DV, int VPW_, bool FIRST>
+template <int DV, int VPW_, bool FIRST, int S>
 __global__ void __launch_bounds__(BLOCK, 3) k_vn_cls(CodeDev cd, DecState ds, int cls, float qmax2,
-                                                     float4 *post_dbg) {
+                                                     float *post_dbg) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
     const int t = ds.active_list[ti];
@@ -276,15 +262,15 @@ __global__ void __launch_bounds__(BLOCK, 3) k_vn_cls(CodeDev cd, DecState ds, in
     if (nv <= 0) return;
     const int vv = (lane < nv) ? cd.vc_vars[cd.vc_off[cls] + w0 + lane] : 0;
     const int sl = (lane < nv * DV) ? cd.vc_slots[cd.vc_soff[cls] + (int64_t)w0 * DV + lane] : 0;
-    const bool any = ((act.x | act.y | act.z | act.w) >> lane) & 1u;
+    const uint32_t any = lane_act<S>(act, lane);
     int v[VPW_];
-    float4 Lv[VPW_];
+    FV<S> Lv[VPW_];
 #pragma unroll
     for (int i = 0; i < VPW_; ++i) {
         v[i] = __shfl_sync(FULL, vv, i);
-        Lv[i] = (i < nv && any) ? ds.L[((size_t)t * cd.n + v[i]) * LANES + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        Lv[i] = (i < nv && any) ? ldv<S>(ds.L + (((size_t)t * cd.n + v[i]) * LANES + lane) * S) : splat<S>(0.0f);
     }
-    float4 *mt = ds.msg + (size_t)t * cd.E * LANES + lane;
+    float *mt = ds.msg + (size_t)t * cd.E * LANES * S + (size_t)lane * S;
     int slot[VPW_][DV];
 #pragma unroll
     for (int i = 0; i < VPW_; ++i)
@@ -295,39 +281,47 @@ __global__ void __launch_bounds__(BLOCK, 3) k_vn_cls(CodeDev cd, DecState ds, in
         for (int i = 0; i < VPW_; ++i) {
             if (i >= nv) break;
             if (any) {
-                const float4 q = make_float4(clampf(Lv[i].x, qmax2), clampf(Lv[i].y, qmax2), clampf(Lv[i].z, qmax2),
-                                             clampf(Lv[i].w, qmax2));
+                FV<S> q;
 #pragma unroll
-                for (int k = 0; k < DV; ++k) mt[(size_t)slot[i][k] * LANES] = q;
+                for (int s = 0; s < S; ++s) q.c[s] = clampf(Lv[i].c[s], qmax2);
+#pragma unroll
+                for (int k = 0; k < DV; ++k) stv<S>(mt + (size_t)slot[i][k] * LANES * S, q);
             }
-            vn_finish(ds, cd, t, v[i], Lv[i], act, any, lane, post_dbg);
+            vn_finish<S>(ds, cd, t, v[i], Lv[i], act, any, lane, post_dbg);
         }
         return;
     }
-    float4 r[VPW_][DV];
+    FV<S> r[VPW_][DV];
 #pragma unroll
     for (int i = 0; i < VPW_; ++i)
 #pragma unroll
         for (int k = 0; k < DV; ++k)
-            r[i][k] = (i < nv && any) ? mt[(size_t)slot[i][k] * LANES] : make_float4(0.f, 0.f, 0.f, 0.f);
+            r[i][k] = (i < nv && any) ? ldv<S>(mt + (size_t)slot[i][k] * LANES * S) : splat<S>(0.0f);
 #pragma unroll
     for (int i = 0; i < VPW_; ++i) {
         if (i >= nv) break;
-        float4 post = Lv[i];
+        FV<S> post = Lv[i];
 #pragma unroll
-        for (int k = 0; k < DV; ++k) post = add4(post, r[i][k]);
+        for (int k = 0; k < DV; ++k)
+#pragma unroll
+            for (int s = 0; s < S; ++s) post.c[s] += r[i][k].c[s];
         if (any) {
 #pragma unroll
-            for (int k = 0; k < DV; ++k) mt[(size_t)slot[i][k] * LANES] = vclamp_diff(post, r[i][k], qmax2);
+            for (int k = 0; k < DV; ++k) {
+                FV<S> q;
+#pragma unroll
+                for (int s = 0; s < S; ++s) q.c[s] = clampf(post.c[s] - r[i][k].c[s], qmax2);
+                stv<S>(mt + (size_t)slot[i][k] * LANES * S, q);
+            }
         }
-        vn_finish(ds, cd, t, v[i], post, act, any, lane, post_dbg);
+        vn_finish<S>(ds, cd, t, v[i], post, act, any, lane, post_dbg);
     }
 }
 
 // any degree: one variable per warp, slots read per edge (mixed / large-degree classes)
-template <bool FIRST>
+template <bool FIRST, int S>
 __global__ void __launch_bounds__(BLOCK) k_vn_generic(CodeDev cd, DecState ds, int cls, float qmax2,
-                                                      float4 *post_dbg) {
+                                                      float *post_dbg) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
     const int t = ds.active_list[ti];
@@ -338,19 +332,26 @@ __global__ void __launch_bounds__(BLOCK) k_vn_generic(CodeDev cd, DecState ds, i
     const int v = cd.vc_vars[cd.vc_off[cls] + w];
     const int beg = cd.col_ptr[v], deg = cd.col_ptr[v + 1] - beg;
     const int32_t *slots = cd.csc_slot + beg;
-    const bool any = ((act.x | act.y | act.z | act.w) >> lane) & 1u;
-    float4 *mt = ds.msg + (size_t)t * cd.E * LANES + lane;
-    float4 post = any ? ds.L[((size_t)t * cd.n + v) * LANES + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint32_t any = lane_act<S>(act, lane);
+    float *mt = ds.msg + (size_t)t * cd.E * LANES * S + (size_t)lane * S;
+    FV<S> post = any ? ldv<S>(ds.L + (((size_t)t * cd.n + v) * LANES + lane) * S) : splat<S>(0.0f);
     if (any) {
         if (!FIRST)
-            for (int k = 0; k < deg; ++k) post = add4(post, mt[(size_t)slots[k] * LANES]);
+            for (int k = 0; k < deg; ++k) {
+                const FV<S> r = ldv<S>(mt + (size_t)slots[k] * LANES * S);
+#pragma unroll
+                for (int s = 0; s < S; ++s) post.c[s] += r.c[s];
+            }
         for (int k = 0; k < deg; ++k) {
-            float4 *p = mt + (size_t)slots[k] * LANES;
-            const float4 r = FIRST ? make_float4(0.f, 0.f, 0.f, 0.f) : *p;
-            *p = vclamp_diff(post, r, qmax2);
+            float *p = mt + (size_t)slots[k] * LANES * S;
+            const FV<S> r = FIRST ? splat<S>(0.0f) : ldv<S>(p);
+            FV<S> q;
+#pragma unroll
+            for (int s = 0; s < S; ++s) q.c[s] = clampf(post.c[s] - r.c[s], qmax2);
+            stv<S>(p, q);
         }
     }
-    vn_finish(ds, cd, t, v, post, act, any, lane, post_dbg);
+    vn_finish<S>(ds, cd, t, v, post, act, any, lane, post_dbg);
 }
 
 // ------------------------------------------------------------------ scheduling
@@ -384,7 +385,7 @@ __device__ __forceinline__ void mark_frames(const DecState &ds, int t, int s, ui
     while (bits) {
         const int l = __ffs(bits) - 1;
         bits &= bits - 1;
-        const int f = t * T + s * LANES + l;
+        const int f = t * ds.tile_frames + s * LANES + l;
         ds.iters[f] = it;
         ds.conv[f] = cv;
     }
@@ -407,8 +408,7 @@ __global__ void __launch_bounds__(1024) k_status(DecState ds, int k, int max_ite
             if (a.x | a.y | a.z | a.w) {
                 const uint4 u = ds.tile_unsat[t];
                 ds.tile_unsat[t] = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-                for (int s = 0; s < SUBS; ++s) {
+                for (int s = 0; s < ds.subs; ++s) {
                     const uint32_t as = cmpu(a, s), us = cmpu(u, s);
                     mark_frames(ds, t, s, as & ~us, k - 1, 1);
                     if (final_pass) mark_frames(ds, t, s, as & us, max_iter, 0);
@@ -474,49 +474,53 @@ __global__ void __launch_bounds__(BLOCK) k_retire(DecState ds, int32_t n, uint32
             const uint32_t b = __ballot_sync(FULL, (ws >> f) & 1u);
             if (lane == f) mine = b;
         }
-        const int frame = t * T + s * LANES + lane;
+        const int frame = t * ds.tile_frames + s * LANES + lane;
         if (((ns >> lane) & 1u) && frame < ds.frames) bits_out[(size_t)frame * Wn + w] = mine;
     }
 }
 
-// natural [F][rows] -> interleaved [tiles][rows][32] float4 (zero-fill missing frames), times scale
-__global__ void __launch_bounds__(256) k_to_interleaved(const float *__restrict__ src, float4 *__restrict__ dst,
+// natural [F][rows] -> interleaved [tiles][rows][32][S] (zero-fill missing frames), times scale
+template <int S>
+__global__ void __launch_bounds__(256) k_to_interleaved(const float *__restrict__ src, float *__restrict__ dst,
                                                         int32_t F, int64_t rows, float scale) {
-    __shared__ float sm[T][33];
+    __shared__ float sm[LANES * S][33];
     const int t = blockIdx.y;
     const int64_t r0 = (int64_t)blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    for (int fl = ty; fl < T; fl += 8) {
-        const int f = t * T + fl;
+    for (int fl = ty; fl < LANES * S; fl += 8) {
+        const int f = t * LANES * S + fl;
         const int64_t r = r0 + tx;
         sm[fl][tx] = (f < F && r < rows) ? src[(size_t)f * rows + r] * scale : 0.0f;
     }
     __syncthreads();
     for (int rl = ty; rl < 32; rl += 8) {
         const int64_t r = r0 + rl;
-        if (r < rows)
-            dst[((size_t)t * rows + r) * LANES + tx] = make_float4(sm[tx][rl], sm[32 + tx][rl], sm[64 + tx][rl], sm[96 + tx][rl]);
+        if (r < rows) {
+            FV<S> v;
+#pragma unroll
+            for (int s = 0; s < S; ++s) v.c[s] = sm[s * LANES + tx][rl];
+            stv<S>(dst + (((size_t)t * rows + r) * LANES + tx) * S, v);
+        }
     }
 }
 
-// interleaved [tiles][rows][32] float4 -> natural [F][rows], times scale
-__global__ void __launch_bounds__(256) k_from_interleaved(const float4 *__restrict__ src, float *__restrict__ dst,
+// interleaved [tiles][rows][32][S] -> natural [F][rows], times scale
+template <int S>
+__global__ void __launch_bounds__(256) k_from_interleaved(const float *__restrict__ src, float *__restrict__ dst,
                                                           int32_t F, int64_t rows, float scale) {
-    __shared__ float sm[T][33];
+    __shared__ float sm[LANES * S][33];
     const int t = blockIdx.y;
     const int64_t r0 = (int64_t)blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int rl = ty; rl < 32; rl += 8) {
         const int64_t r = r0 + rl;
-        const float4 v = (r < rows) ? src[((size_t)t * rows + r) * LANES + tx] : make_float4(0.f, 0.f, 0.f, 0.f);
-        sm[tx][rl] = v.x;
-        sm[32 + tx][rl] = v.y;
-        sm[64 + tx][rl] = v.z;
-        sm[96 + tx][rl] = v.w;
+        const FV<S> v = (r < rows) ? ldv<S>(src + (((size_t)t * rows + r) * LANES + tx) * S) : splat<S>(0.0f);
+#pragma unroll
+        for (int s = 0; s < S; ++s) sm[s * LANES + tx][rl] = v.c[s];
     }
     __syncthreads();
-    for (int fl = ty; fl < T; fl += 8) {
-        const int f = t * T + fl;
+    for (int fl = ty; fl < LANES * S; fl += 8) {
+        const int f = t * LANES * S + fl;
         const int64_t r = r0 + tx;
         if (f < F && r < rows) dst[(size_t)f * rows + r] = sm[fl][tx] * scale;
     }
@@ -524,18 +528,16 @@ __global__ void __launch_bounds__(256) k_from_interleaved(const float4 *__restri
 
 // public syndrome [F][Wm] -> per-tile lane-bit words st[t][c] (uint4 over sub-tiles)
 __global__ void __launch_bounds__(BLOCK) k_synd_transpose(const uint32_t *__restrict__ synd, int32_t F, int32_t M,
-                                                           uint4 *__restrict__ st) {
+                                                           int subs, uint4 *__restrict__ st) {
     const int t = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Wm = words_of(M);
     const int w = blockIdx.x * WARPS_PER_BLOCK + warp;
     if (w >= Wm) return;
-    uint32_t mine[SUBS];
-#pragma unroll
-    for (int s = 0; s < SUBS; ++s) {
-        const int f = t * T + s * LANES + lane;
+    uint32_t mine[SUBS] = {0u, 0u, 0u, 0u};
+    for (int s = 0; s < subs; ++s) {
+        const int f = t * LANES * subs + s * LANES + lane;
         const uint32_t word = (f < F) ? synd[(size_t)f * Wm + w] : 0u;
-        mine[s] = 0u;
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
             const uint32_t b = __ballot_sync(FULL, (word >> k) & 1u);
@@ -550,11 +552,10 @@ __global__ void __launch_bounds__(BLOCK) k_synd_transpose(const uint32_t *__rest
 __global__ void k_init_tiles(DecState ds, const uint8_t *__restrict__ alive) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ds.tiles) return;
-    uint32_t a[SUBS];
-    for (int s = 0; s < SUBS; ++s) {
-        a[s] = 0u;
+    uint32_t a[SUBS] = {0u, 0u, 0u, 0u};
+    for (int s = 0; s < ds.subs; ++s) {
         for (int l = 0; l < LANES; ++l) {
-            const int f = t * T + s * LANES + l;
+            const int f = t * ds.tile_frames + s * LANES + l;
             if (f < ds.frames && (!alive || alive[f])) a[s] |= 1u << l;
         }
     }
@@ -575,53 +576,60 @@ __global__ void k_set_counts(DecState ds, int32_t n_active) {
 // ---------------------------------------------------------------- launchers
 
 // qmax is in natural LLR units; the arena works in log2 units.  The kernel body
-// is chosen by the code's maximum degrees (one instantiation per degree bound).
+// is chosen by the code's maximum check degree and the tile width S.
+template <int S>
+static void launch_cn_s(const CodeDev &cd, const DecState &ds, dim3 grid, float q2, int check_only, cudaStream_t s) {
+    switch (cd.max_dc) {
+        case 1: case 2: k_cn<2, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 3: k_cn<3, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 4: k_cn<4, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 5: k_cn<5, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 6: k_cn<6, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 7: k_cn<7, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 8: k_cn<8, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        default: k_cn<0, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+    }
+}
+
 void launch_cn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, int check_only, cudaStream_t s) {
     if (grid_tiles <= 0) return;
     const int per_block = WARPS_PER_BLOCK * CPW;
     dim3 grid((cd.M + per_block - 1) / per_block, grid_tiles);
     const float q2 = qmax * LOG2E;
-    switch (cd.max_dc) {
-        case 1: case 2: k_cn<2><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 3: k_cn<3><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 4: k_cn<4><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 5: k_cn<5><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 6: k_cn<6><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 7: k_cn<7><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 8: k_cn<8><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        default: k_cn<0><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-    }
+    if (ds.subs == 4) launch_cn_s<4>(cd, ds, grid, q2, check_only, s);
+    else if (ds.subs == 2) launch_cn_s<2>(cd, ds, grid, q2, check_only, s);
+    else launch_cn_s<1>(cd, ds, grid, q2, check_only, s);
 }
 
-template <int DV, int VPW_, bool FIRST>
-static void launch_vn_cls(const CodeDev &cd, const DecState &ds, int cls, int grid_tiles, float q2, float4 *post_dbg,
+template <int DV, int VPW_, bool FIRST, int S>
+static void launch_vn_cls(const CodeDev &cd, const DecState &ds, int cls, int grid_tiles, float q2, float *post_dbg,
                           cudaStream_t s) {
     const int per_block = WARPS_PER_BLOCK * VPW_;
     dim3 grid((cd.vc_cnt[cls] + per_block - 1) / per_block, grid_tiles);
-    k_vn_cls<DV, VPW_, FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, cls, q2, post_dbg);
+    k_vn_cls<DV, VPW_, FIRST, S><<<grid, BLOCK, 0, s>>>(cd, ds, cls, q2, post_dbg);
 }
 
-template <bool FIRST>
-static int launch_vn_t(const CodeDev &cd, const DecState &ds, int grid_tiles, float q2, float4 *post_dbg,
+// registers: VPW x (DV + 1) line buffers of S floats
+template <bool FIRST, int S>
+static int launch_vn_t(const CodeDev &cd, const DecState &ds, int grid_tiles, float q2, float *post_dbg,
                        cudaStream_t s) {
+    constexpr int X = 4 / S;  // more variables per warp when the lines are narrower
     int launched = 0;
     for (int c = 0; c < cd.n_vclass; ++c) {
         if (cd.vc_cnt[c] <= 0) continue;
         ++launched;
         switch (cd.vc_deg[c]) {
-            case 1: launch_vn_cls<1, 6, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
-            case 2: launch_vn_cls<2, 4, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
-            case 3: launch_vn_cls<3, 2, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
-            case 4: launch_vn_cls<4, 2, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
-            case 5: launch_vn_cls<5, 1, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
-            case 6: launch_vn_cls<6, 1, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
-            case 7: launch_vn_cls<7, 1, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
-            case 8: launch_vn_cls<8, 1, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
-            case 9: launch_vn_cls<9, 1, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
-            case 10: launch_vn_cls<10, 1, FIRST>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 1: launch_vn_cls<1, 6, FIRST, S>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 2: launch_vn_cls<2, 4, FIRST, S>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 3: launch_vn_cls<3, 2 * (X > 1 ? 2 : 1), FIRST, S>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 4: launch_vn_cls<4, 2 * (X > 1 ? 2 : 1), FIRST, S>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 5: launch_vn_cls<5, X, FIRST, S>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 6: launch_vn_cls<6, X, FIRST, S>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 7: launch_vn_cls<7, X, FIRST, S>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
+            case 8: launch_vn_cls<8, X, FIRST, S>(cd, ds, c, grid_tiles, q2, post_dbg, s); break;
             default: {
                 dim3 grid((cd.vc_cnt[c] + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, grid_tiles);
-                k_vn_generic<FIRST><<<grid, BLOCK, 0, s>>>(cd, ds, c, q2, post_dbg);
+                k_vn_generic<FIRST, S><<<grid, BLOCK, 0, s>>>(cd, ds, c, q2, post_dbg);
             }
         }
     }
@@ -629,11 +637,16 @@ static int launch_vn_t(const CodeDev &cd, const DecState &ds, int grid_tiles, fl
 }
 
 // returns the number of kernels launched (one per variable-degree class)
-int launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float4 *post_dbg,
+int launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float *post_dbg,
               cudaStream_t s) {
     if (grid_tiles <= 0) return 0;
-    if (first) return launch_vn_t<true>(cd, ds, grid_tiles, qmax * LOG2E, post_dbg, s);
-    return launch_vn_t<false>(cd, ds, grid_tiles, qmax * LOG2E, post_dbg, s);
+    const float q2 = qmax * LOG2E;
+    if (ds.subs == 4) return first ? launch_vn_t<true, 4>(cd, ds, grid_tiles, q2, post_dbg, s)
+                                   : launch_vn_t<false, 4>(cd, ds, grid_tiles, q2, post_dbg, s);
+    if (ds.subs == 2) return first ? launch_vn_t<true, 2>(cd, ds, grid_tiles, q2, post_dbg, s)
+                                   : launch_vn_t<false, 2>(cd, ds, grid_tiles, q2, post_dbg, s);
+    return first ? launch_vn_t<true, 1>(cd, ds, grid_tiles, q2, post_dbg, s)
+                 : launch_vn_t<false, 1>(cd, ds, grid_tiles, q2, post_dbg, s);
 }
 
 void launch_status(const DecState &ds, int k, int max_iter, int final_pass, int32_t *host_counts, cudaStream_t s) {
@@ -646,21 +659,26 @@ void launch_retire(const DecState &ds, int32_t n, int grid_tiles, uint32_t *bits
     k_retire<<<grid, BLOCK, 0, s>>>(ds, n, bits_out);
 }
 
-void launch_to_interleaved(const float *src, float4 *dst, int32_t F, int64_t rows, int tiles, float scale,
+void launch_to_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, int subs, float scale,
                            cudaStream_t s) {
     dim3 grid((unsigned)((rows + 31) / 32), tiles);
-    k_to_interleaved<<<grid, 256, 0, s>>>(src, dst, F, rows, scale);
+    if (subs == 4) k_to_interleaved<4><<<grid, 256, 0, s>>>(src, dst, F, rows, scale);
+    else if (subs == 2) k_to_interleaved<2><<<grid, 256, 0, s>>>(src, dst, F, rows, scale);
+    else k_to_interleaved<1><<<grid, 256, 0, s>>>(src, dst, F, rows, scale);
 }
 
-void launch_from_interleaved(const float4 *src, float *dst, int32_t F, int64_t rows, int tiles, float scale,
+void launch_from_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, int subs, float scale,
                              cudaStream_t s) {
     dim3 grid((unsigned)((rows + 31) / 32), tiles);
-    k_from_interleaved<<<grid, 256, 0, s>>>(src, dst, F, rows, scale);
+    if (subs == 4) k_from_interleaved<4><<<grid, 256, 0, s>>>(src, dst, F, rows, scale);
+    else if (subs == 2) k_from_interleaved<2><<<grid, 256, 0, s>>>(src, dst, F, rows, scale);
+    else k_from_interleaved<1><<<grid, 256, 0, s>>>(src, dst, F, rows, scale);
 }
 
-void launch_synd_transpose(const uint32_t *synd, int32_t F, int32_t M, uint4 *st, int tiles, cudaStream_t s) {
+void launch_synd_transpose(const uint32_t *synd, int32_t F, int32_t M, int subs, uint4 *st, int tiles,
+                           cudaStream_t s) {
     dim3 grid((words_of(M) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, tiles);
-    k_synd_transpose<<<grid, BLOCK, 0, s>>>(synd, F, M, st);
+    k_synd_transpose<<<grid, BLOCK, 0, s>>>(synd, F, M, subs, st);
 }
 
 void launch_init_tiles(const DecState &ds, const uint8_t *alive, cudaStream_t s) {

@@ -8,14 +8,14 @@
 
 namespace cvsr {
 
-// Frames per tile: 128 = 32 warp lanes x 4 frames per lane (one float4).
-// Frame f of tile t sits at lane (f mod 32), component ((f / 32) mod 4)
-// ("sub-tile"), i.e. f = 128 t + 32 s + lane.  Edge messages of the 128
-// frames of a tile are stored contiguously per edge slot ("frame-interleaved
-// arena"): a warp moves one 512-byte line per edge.
-constexpr int T = 128;
+// Frames per tile: 32 warp lanes x S frames per lane (S = 1, 2 or 4, chosen per
+// decode from the batch size: a float, float2 or float4 per lane).  Frame f of
+// tile t sits at lane (f mod 32), component s = (f / 32) mod S ("sub-tile"),
+// i.e. f = 32 S t + 32 s + lane.  Edge messages of the 32 S frames of a tile
+// are stored contiguously per edge slot ("frame-interleaved arena", SURVEY.md
+// §2.6 row 45): a warp moves one 128 S-byte line per edge.
 constexpr int LANES = 32;
-constexpr int SUBS = 4;
+constexpr int SUBS = 4;  // maximum S
 constexpr int WARPS_PER_BLOCK = 8;
 constexpr int BLOCK = 32 * WARPS_PER_BLOCK;
 // largest check degree supported (cvsr_code_load rejects larger rows with CVSR_ECODE)
@@ -51,9 +51,11 @@ struct CodeDev {
 struct DecState {
     int32_t tiles;
     int32_t frames;
-    float4 *msg;            // [tiles][E][32]  in-place V2C/C2V message per edge slot (log2 units)
-    float4 *L;              // [tiles][n][32]  channel LLR (log2 units)
-    uint4 *hb;              // [tiles][n]      hard decisions, bit = lane
+    int32_t subs;           // S: frames per lane
+    int32_t tile_frames;    // 32 S
+    float *msg;             // [tiles][E][32][S]  in-place V2C/C2V message per edge slot (log2 units)
+    float *L;               // [tiles][n][32][S]  channel LLR (log2 units)
+    uint4 *hb;              // [tiles][n]      hard decisions, bit = lane (components >= S unused)
     uint4 *st;              // [tiles][M]      syndrome bits, bit = lane
     uint4 *tile_active;     // [tiles] frames still iterating
     uint4 *tile_unsat;      // [tiles] frames with >= 1 unsatisfied check in this CN pass
@@ -78,5 +80,9 @@ struct LlrParams {
 };
 
 __host__ __device__ inline int32_t words_of(int64_t bits) { return (int32_t)((bits + 31) / 32); }
+
+// frames per lane for a batch: the smallest S in {1, 2, 4} whose tiles are not
+// mostly empty (S = 4 once there are more than 64 frames)
+inline int choose_subs(int32_t frames) { return frames <= 32 ? 1 : (frames <= 64 ? 2 : 4); }
 
 }  // namespace cvsr

@@ -6,15 +6,16 @@ namespace cvsr {
 
 // bp_kernels.cu
 void launch_cn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, int check_only, cudaStream_t s);
-int launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float4 *post_dbg,
+int launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float *post_dbg,
               cudaStream_t s);
 void launch_status(const DecState &ds, int k, int max_iter, int final_pass, int32_t *host_counts, cudaStream_t s);
 void launch_retire(const DecState &ds, int32_t n, int grid_tiles, uint32_t *bits_out, cudaStream_t s);
-void launch_to_interleaved(const float *src, float4 *dst, int32_t F, int64_t rows, int tiles, float scale,
+void launch_to_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, int subs, float scale,
                            cudaStream_t s);
-void launch_from_interleaved(const float4 *src, float *dst, int32_t F, int64_t rows, int tiles, float scale,
+void launch_from_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, int subs, float scale,
                              cudaStream_t s);
-void launch_synd_transpose(const uint32_t *synd, int32_t F, int32_t M, uint4 *st, int tiles, cudaStream_t s);
+void launch_synd_transpose(const uint32_t *synd, int32_t F, int32_t M, int subs, uint4 *st, int tiles,
+                           cudaStream_t s);
 void launch_init_tiles(const DecState &ds, const uint8_t *alive, cudaStream_t s);
 void launch_set_counts(const DecState &ds, int32_t n_active, cudaStream_t s);
 
@@ -29,7 +30,7 @@ void launch_count_errors(const uint8_t *a, const uint8_t *b, const uint8_t *ok, 
 void launch_llr_slice(const LlrParams &p, const float *x, const uint8_t *known_label, int32_t F, int32_t n,
                       float *out, cudaStream_t s);
 void launch_llr_biawgn(const float *y, int64_t count, float sigma2, float llr_max, float *out, cudaStream_t s);
-void launch_llr_interleaved(const LlrParams &p, const float *x, int32_t F, int32_t n, int tiles, float4 *L,
+void launch_llr_interleaved(const LlrParams &p, const float *x, int32_t F, int32_t n, int tiles, int subs, float *L,
                             cudaStream_t s);
 
 // reconcile bookkeeping (bob_kernels.cu)

@@ -12,6 +12,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "vec.cuh"
 
 namespace cvsr {
 
@@ -99,20 +100,21 @@ __global__ void k_llr_slice(LlrParams p, const float *__restrict__ x, const uint
 }
 
 // decoder feed: conditional LLR written straight into the interleaved arena
-// L[t][v][lane] (float4 over the 4 sub-tiles; fused transpose, log2 units);
-// known bits read from the packed slices.
+// L[t][v][lane][S] (fused transpose, log2 units); known bits read from the
+// packed slices.
+template <int S>
 __global__ void __launch_bounds__(256) k_llr_interleaved(LlrParams p, const float *__restrict__ x, int32_t F,
-                                                         int32_t n, float4 *__restrict__ L) {
+                                                         int32_t n, float *__restrict__ L) {
     __shared__ float se[256];
-    __shared__ float sm[T][33];
+    __shared__ float sm[LANES * S][33];
     for (int i = threadIdx.x; i < 255; i += blockDim.x) se[i] = p.edges[i];
     __syncthreads();
     const int t = blockIdx.y;
     const int v0 = blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int Wn = words_of(n);
-    for (int fl = ty; fl < T; fl += 8) {
-        const int f = t * T + fl;
+    for (int fl = ty; fl < LANES * S; fl += 8) {
+        const int f = t * LANES * S + fl;
         const int v = v0 + tx;
         float val = 0.0f;
         if (f < F && v < n) {
@@ -129,8 +131,12 @@ __global__ void __launch_bounds__(256) k_llr_interleaved(LlrParams p, const floa
     __syncthreads();
     for (int vl = ty; vl < 32; vl += 8) {
         const int v = v0 + vl;
-        if (v < n)
-            L[((size_t)t * n + v) * LANES + tx] = make_float4(sm[tx][vl], sm[32 + tx][vl], sm[64 + tx][vl], sm[96 + tx][vl]);
+        if (v < n) {
+            FV<S> o;
+#pragma unroll
+            for (int s = 0; s < S; ++s) o.c[s] = sm[s * LANES + tx][vl];
+            stv<S>(L + (((size_t)t * n + v) * LANES + tx) * S, o);
+        }
     }
 }
 
@@ -156,10 +162,12 @@ void launch_llr_biawgn(const float *y, int64_t count, float sigma2, float llr_ma
     k_llr_biawgn<<<grid_for(count, 256), 256, 0, s>>>(y, count, sigma2, llr_max, out);
 }
 
-void launch_llr_interleaved(const LlrParams &p, const float *x, int32_t F, int32_t n, int tiles, float4 *L,
+void launch_llr_interleaved(const LlrParams &p, const float *x, int32_t F, int32_t n, int tiles, int subs, float *L,
                             cudaStream_t s) {
     dim3 grid((n + 31) / 32, tiles);
-    k_llr_interleaved<<<grid, 256, 0, s>>>(p, x, F, n, L);
+    if (subs == 4) k_llr_interleaved<4><<<grid, 256, 0, s>>>(p, x, F, n, L);
+    else if (subs == 2) k_llr_interleaved<2><<<grid, 256, 0, s>>>(p, x, F, n, L);
+    else k_llr_interleaved<1><<<grid, 256, 0, s>>>(p, x, F, n, L);
 }
 
 }  // namespace cvsr
