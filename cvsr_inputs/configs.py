@@ -88,16 +88,30 @@ C3 = SRConfig(
 )
 
 # C4: standard settings: gamma = 2.21468, m = 5, delta* = 0.21359,
-# LSB-first caps (0.0006, 0.0022, 0.1670, 0.6485, 0.4918).
+# LSB-first caps (0.0006, 0.0022, 0.1670, 0.6485, 0.4918): S0, S1 disclosed; S2..S4 start
+# at 0.9*cap (0.150, 0.583, 0.442) and are backed off per tools/calibrate_rates.py.
+# N_R = 1e6 (the "~1e6" sub-block of Fig. 5), 125 frames per GPU of N = 1e9 on 8 GPUs.
 C4 = SRConfig(
     name="C4", m=5, gamma=2.214676, delta=0.21359, n=1_000_000, frames=125,
     slices=(SliceSpec(0, "disclosed"), SliceSpec(1, "disclosed"),
-            SliceSpec(2, "irregular", 0.07), SliceSpec(3, "irregular", 0.583),
+            SliceSpec(2, "irregular", 0.10), SliceSpec(3, "irregular", 0.583),
             SliceSpec(4, "irregular", 0.442)),
     order=(0, 1, 2, 3, 4),
 )
 
-CONFIGS = {"C2": C2, "C3": C3, "C4": C4}
+# C4 at the paper's experimental optimum N_R = 5e6: 25 frames per GPU
+C4b = dataclasses.replace(C4, name="C4b", n=5_000_000, frames=25)
+
+# C5: N_R sweep 2^12 .. 2^20 at N = 1e9 / 8 GPUs per GPU, C4's slices (tools/sweep_nr.py)
+C5_NR = tuple(1 << k for k in range(12, 21))
+C5_SYMBOLS_PER_GPU = 125_000_000
+
+
+def c5(n_r: int) -> SRConfig:
+    return dataclasses.replace(C4, name=f"C5[{n_r}]", n=n_r, frames=max(1, C5_SYMBOLS_PER_GPU // n_r))
+
+
+CONFIGS = {"C2": C2, "C3": C3, "C4": C4, "C4b": C4b}
 
 
 def scaled(cfg: SRConfig, n: int, frames: int) -> SRConfig:

@@ -147,7 +147,7 @@ __device__ __noinline__ void cn_check_generic(float *__restrict__ m, int deg, ui
 }
 
 template <int DCT, int S>  // DCT = max check degree (templated body) or 0 = generic
-__global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 20) ? 4 : 3)
+__global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 20) ? 4 : (DCT * S <= 32 ? 3 : 2))
     k_cn(CodeDev cd, DecState ds, float qmax2, int check_only) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
@@ -587,6 +587,9 @@ static void launch_cn_s(const CodeDev &cd, const DecState &ds, dim3 grid, float 
         case 6: k_cn<6, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
         case 7: k_cn<7, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
         case 8: k_cn<8, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 9: k_cn<9, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 10: k_cn<10, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 11: case 12: k_cn<12, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
         default: k_cn<0, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
     }
 }

@@ -45,19 +45,24 @@ def trial(cfg, frames, seed_frame):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--frames", type=int, default=2048)
+    ap.add_argument("--frames", type=int, default=0, help="0 = the config's frames per GPU")
     ap.add_argument("--grid", default="2:0.406,0.356;3:0.307,0.257,0.207")
     args = ap.parse_args()
     base = configs.CONFIGS[args.config]
     grid = {}
     for part in args.grid.split(";"):
         j, rs = part.split(":")
-        grid[int(j)] = [float(r) for r in rs.split(",")]
+        grid[int(j)] = [r if r.startswith("met") else float(r) for r in rs.split(",")]
+    frames = args.frames or base.frames
     for j, rates in grid.items():
         for r in rates:
-            sl = tuple(dataclasses.replace(s, rate=r) if s.j == j else s for s in base.slices)
+            kind = "irregular"
+            if isinstance(r, str) and r.startswith("met"):
+                kind, r = "met", float(r[3:])
+            met = (2 * r, r, 3, 6) if kind == "met" else None
+            sl = tuple(dataclasses.replace(s, rate=r, kind=kind, met=met) if s.j == j else s for s in base.slices)
             cfg = dataclasses.replace(base, slices=sl)
-            res = trial(cfg, args.frames, 10_000_000)
+            res = trial(cfg, frames, 10_000_000)
             res["vary_slice"] = j
             print(json.dumps(res), flush=True)
 
