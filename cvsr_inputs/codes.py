@@ -140,13 +140,20 @@ def irregular_rate(n: int, rate: float, seed: int = 1,
     configuration model with lambda_2 = 0.30 that subgraph has many short
     cycles, i.e. codewords of weight 3..6 supported on degree-2 variables,
     which BP converges to as undetected errors (measured: 4/16 frames of C2's
-    S2 slice).  Requires #degree-2 variables < M.  The remaining sockets are
-    matched by the seeded configuration model with duplicate repair.
+    S2 slice).  Requires #degree-2 variables < M; at high rates the excess
+    degree-2 variables become degree-3.  The remaining sockets are matched by
+    the seeded configuration model with duplicate repair.
     """
     cnt = _node_counts(lam, n)
+    M = int(round((1.0 - rate) * n))
+    if chain_degree2 and cnt.get(2, 0) >= M and 3 in cnt:
+        # high rates (M < #degree-2 variables): a cycle-free degree-2 subgraph needs fewer
+        # degree-2 variables; move the excess to degree 3 (PROPOSED, DESIGN.md R-3)
+        excess = cnt[2] - (M - max(1, M // 200))
+        cnt[2] -= excess
+        cnt[3] += excess
     var_deg = np.concatenate([np.full(c, a, np.int32) for a, c in sorted(cnt.items())])
     var_deg = var_deg[permutation(n, seed ^ 0x5EED)]
-    M = int(round((1.0 - rate) * n))
     chk_deg = _two_degree_checks(int(var_deg.sum()), M)
     chk_deg = chk_deg[permutation(M, seed ^ 0xC4EC)]
     name = f"irregular R={1 - M / n:.4f} n={n}"
