@@ -348,3 +348,29 @@ def test_reconcile_full_size_sampled(cv, ctx):
     assert np.sum(ok_g != ok_ref) <= 1
     assert np.array_equal(lab_ref[ok_ref.astype(bool)], lab_bob[ok_ref.astype(bool)])
     pipe.close()
+
+
+@pytest.mark.parametrize("name,n,frames", [("C4", 20000, 12), ("C4", 20000, 70), ("C3", 10000, 40)])
+def test_reconcile_parity_other_configs(cv, ctx, name, n, frames):
+    """C4's 5-slice structure (MET + two irregular codes, incl. a check degree > 8 path) and
+    C3's single MET slice, scaled down; 12 frames exercises 1-frame-per-lane tiles (S = 1),
+    40/70 frames S = 2 / 4."""
+    cfg = configs.scaled(configs.CONFIGS[name], n, frames)
+    if name == "C3":
+        import dataclasses
+        cfg = dataclasses.replace(cfg, gamma=0.2, max_iter=200)  # decodable at n = 1e4
+    codes_l = cfg.build_codes()
+    x, y = awgn.quadratures(frames, n, cfg.gamma, seed=23)
+    g = _run_reconcile(cv, cfg, codes_l, x, y, frames, n, cfg.max_iter)
+    lab_bob = oracle.quantise(cfg.edges(), y)
+    assert np.array_equal(g["bob"], lab_bob)
+    synd_ref = [oracle.slice_bits(lab_bob, j) if c is None else oracle.syndrome(c, lab_bob, j)
+                for j, c in enumerate(codes_l)]
+    for s_g, s_r in zip(g["synd"], synd_ref):
+        assert np.array_equal(s_g, s_r)
+    lab_ref, ok_ref, it_ref = oracle.reconcile(codes_l, cfg.order, cfg.edges(), cfg.sigma_n, x, synd_ref,
+                                               cfg.max_iter)
+    both = ok_ref.astype(bool) & g["ok"].astype(bool)
+    assert both.sum() >= 1
+    assert np.array_equal(g["label"][both], lab_ref[both])
+    assert np.sum(g["ok"] != ok_ref) <= max(1, frames // 20)
