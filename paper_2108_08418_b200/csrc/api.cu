@@ -77,6 +77,10 @@ struct cvsr_ctx {
     cudaEvent_t ring[RING] = {};
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     unsigned long long *acc = nullptr;   // device accumulators for stats [32]
+    float *llr_tab = nullptr;            // tabulated conditional LLR (grow-only)
+    size_t llr_tab_cap = 0;
+    uint32_t *bob_bits = nullptr;        // packed slice bits for the syndrome (grow-only)
+    size_t bob_bits_cap = 0;
     int64_t launches = 0;
     // optional per-kernel-class timing (CUDA events around launches)
     bool profiling = false;
@@ -333,6 +337,8 @@ void cvsr_ctx_destroy(cvsr_ctx *ctx) {
     if (ctx->t1) cudaEventDestroy(ctx->t1);
     if (ctx->acc) cudaFree(ctx->acc);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->llr_tab) cudaFree(ctx->llr_tab);
+    if (ctx->bob_bits) cudaFree(ctx->bob_bits);
     delete ctx;
 }
 
@@ -510,8 +516,47 @@ cvsr_status cvsr_syndrome(cvsr_ctx *ctx, const cvsr_code *code, const uint8_t *l
     if (frames == 0) return CVSR_OK;
     if (!label || !synd_out) return fail(CVSR_EINVAL, "null buffer");
     DeviceGuard g(ctx->device);
-    launch_syndrome(code->d, label, frames, slice_j, synd_out, ctx->stream);
-    return check_launch(ctx, 1);
+    // pack S_j first (coalesced), then gather bits from the small packed rows
+    const size_t need = (size_t)frames * words_of(code->d.n) * sizeof(uint32_t);
+    if (need > ctx->bob_bits_cap) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->bob_bits) CK(cudaFree(ctx->bob_bits));
+        ctx->bob_bits = nullptr;
+        ctx->bob_bits_cap = 0;
+        cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&ctx->bob_bits), need);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(CVSR_ENOMEM, "syndrome scratch: %s", cudaGetErrorString(e));
+        }
+        ctx->bob_bits_cap = need;
+    }
+    launch_slice_bits(label, frames, code->d.n, slice_j, ctx->bob_bits, ctx->stream);
+    launch_syndrome_bits(code->d, ctx->bob_bits, frames, synd_out, ctx->stream);
+    return check_launch(ctx, 2);
+}
+
+// builds the LLR table for p on the context stream (p.table stays null when the grid
+// would be too coarse for sigma_n; the kernels then evaluate exactly)
+static cvsr_status prepare_llr_table(cvsr_ctx *ctx, LlrParams &p, int *launched) {
+    p.table = nullptr;
+    const size_t need = ((size_t)1 << __builtin_popcount(p.known_mask)) * LLR_NTAB * sizeof(float);
+    if (need > ctx->llr_tab_cap) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->llr_tab) CK(cudaFree(ctx->llr_tab));
+        ctx->llr_tab = nullptr;
+        ctx->llr_tab_cap = 0;
+        cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&ctx->llr_tab), need);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(CVSR_ENOMEM, "LLR table: %s", cudaGetErrorString(e));
+        }
+        ctx->llr_tab_cap = need;
+    }
+    if (launch_llr_table(p, ctx->llr_tab, ctx->stream)) {
+        p.table = ctx->llr_tab;
+        ++*launched;
+    }
+    return CVSR_OK;
 }
 
 static void fill_llr_params(LlrParams &p, const cvsr_quantiser *q, int j, uint32_t mask, float sigma_n, float llr_max) {
@@ -541,8 +586,10 @@ cvsr_status cvsr_llr_slice(cvsr_ctx *ctx, const cvsr_quantiser *q, const float *
     DeviceGuard g(ctx->device);
     LlrParams p;
     fill_llr_params(p, q, slice_j, known_mask, sigma_n, llr_max);
+    int launched = 1;
+    if (cvsr_status st = prepare_llr_table(ctx, p, &launched)) return st;
     launch_llr_slice(p, x, known_label, frames, n, llr_out, ctx->stream);
-    return check_launch(ctx, 1);
+    return check_launch(ctx, launched);
 }
 
 cvsr_status cvsr_llr_biawgn(cvsr_ctx *ctx, const float *y, int64_t count, float sigma2, float llr_max,
@@ -701,6 +748,7 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
             fill_llr_params(p, q, j, known_mask, sigma_n, opts->msg_clamp);
             for (int jj = 0; jj < m; ++jj) p.known_bits[jj] = known_bits[jj];
             prof_begin(ctx, KC_INIT);
+            if (cvsr_status st = prepare_llr_table(ctx, p, &launched)) return st;
             launch_llr_interleaved(p, x, frames, n, tiles, ds.subs, ds.L, s);
             prof_end(ctx);
             launched += 4;

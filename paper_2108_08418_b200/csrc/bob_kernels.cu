@@ -80,6 +80,29 @@ __global__ void __launch_bounds__(BLOCK) k_syndrome(CodeDev cd, const uint8_t *_
     if (lane == 0) synd[(size_t)f * Wm + w] = word;
 }
 
+// K2 from packed slice bits (bits[f][Wn], an 8 KB row per frame at N_R = 2^16 stays in L1)
+__global__ void __launch_bounds__(BLOCK) k_syndrome_bits(CodeDev cd, const uint32_t *__restrict__ bits,
+                                                          uint32_t *__restrict__ synd) {
+    const int f = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int Wm = words_of(cd.M), Wn = words_of(cd.n);
+    const int w = blockIdx.x * WARPS_PER_BLOCK + warp;
+    if (w >= Wm) return;
+    const int c = w * 32 + lane;
+    uint32_t par = 0u;
+    if (c < cd.M) {
+        const uint32_t *b = bits + (size_t)f * Wn;
+        const int beg = cd.row_ptr[c], end = cd.row_ptr[c + 1];
+        for (int e = beg; e < end; ++e) {
+            const int v = cd.col_idx[e];
+            par ^= b[v >> 5] >> (v & 31);
+        }
+        par &= 1u;
+    }
+    const uint32_t word = __ballot_sync(FULLB, par);
+    if (lane == 0) synd[(size_t)f * Wm + w] = word;
+}
+
 // simulation check: counts {ok frames, ok frames with any label mismatch, mismatching bytes}
 __global__ void k_count_errors(const uint8_t *__restrict__ a, const uint8_t *__restrict__ b,
                                const uint8_t *__restrict__ ok, int32_t n, unsigned long long *counts) {
@@ -183,6 +206,11 @@ void launch_slice_bits(const uint8_t *label, int32_t F, int32_t n, int32_t j, ui
 void launch_syndrome(const CodeDev &cd, const uint8_t *label, int32_t F, int32_t j, uint32_t *synd, cudaStream_t s) {
     dim3 grid((words_of(cd.M) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, F);
     k_syndrome<<<grid, BLOCK, 0, s>>>(cd, label, j, synd);
+}
+
+void launch_syndrome_bits(const CodeDev &cd, const uint32_t *bits, int32_t F, uint32_t *synd, cudaStream_t s) {
+    dim3 grid((words_of(cd.M) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, F);
+    k_syndrome_bits<<<grid, BLOCK, 0, s>>>(cd, bits, synd);
 }
 
 void launch_count_errors(const uint8_t *a, const uint8_t *b, const uint8_t *ok, int32_t F, int32_t n,

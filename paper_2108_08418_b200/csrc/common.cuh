@@ -76,8 +76,17 @@ struct LlrParams {
     float inv_sigma;
     float llr_max;
     const uint32_t *known_bits[8];  // packed [F][Wn] per known slice (nullptr if unknown)
+    const float *table;             // [2^|K|][LLR_NTAB] unclamped L on the x grid (nullptr: exact only)
     float edges[255];
 };
+
+// Tabulated conditional LLR: L(x) for one known-bit pattern is a smooth function
+// of x; it is tabulated (exact log-domain formula) on a uniform grid and read by
+// cubic Lagrange interpolation, falling back to the exact formula outside the grid
+// or when the grid is coarse relative to sigma_n.
+constexpr int LLR_NTAB = 4096 + 3;
+constexpr float LLR_XMAX = 10.0f;
+constexpr float LLR_H = 2.0f * LLR_XMAX / 4096.0f;
 
 __host__ __device__ inline int32_t words_of(int64_t bits) { return (int32_t)((bits + 31) / 32); }
 

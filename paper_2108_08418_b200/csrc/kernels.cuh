@@ -23,10 +23,12 @@ void launch_set_counts(const DecState &ds, int32_t n_active, cudaStream_t s);
 void launch_quantise(const float *edges_host, int m, const float *y, int64_t count, uint8_t *label, cudaStream_t s);
 void launch_slice_bits(const uint8_t *label, int32_t F, int32_t n, int32_t j, uint32_t *bits, cudaStream_t s);
 void launch_syndrome(const CodeDev &cd, const uint8_t *label, int32_t F, int32_t j, uint32_t *synd, cudaStream_t s);
+void launch_syndrome_bits(const CodeDev &cd, const uint32_t *bits, int32_t F, uint32_t *synd, cudaStream_t s);
 void launch_count_errors(const uint8_t *a, const uint8_t *b, const uint8_t *ok, int32_t F, int32_t n,
                          unsigned long long *counts, cudaStream_t s);
 
 // llr_kernels.cu
+bool launch_llr_table(const LlrParams &p, float *table, cudaStream_t s);
 void launch_llr_slice(const LlrParams &p, const float *x, const uint8_t *known_label, int32_t F, int32_t n,
                       float *out, cudaStream_t s);
 void launch_llr_biawgn(const float *y, int64_t count, float sigma2, float llr_max, float *out, cudaStream_t s);

@@ -64,8 +64,8 @@ __device__ __forceinline__ uint32_t gray_inv(uint32_t g) {
     return g;
 }
 
-__device__ float llr_cond(const float *se, int m, int j, uint32_t kmask, uint32_t kappa, float x, float inv_sigma,
-                          float llr_max) {
+// unclamped ln N_0 - ln N_1 (+-1e30 when one side is empty)
+__device__ float llr_raw(const float *se, int m, int j, uint32_t kmask, uint32_t kappa, float x, float inv_sigma) {
     const int nb = 1 << m;
     const uint32_t free_mask = (uint32_t)(nb - 1) & ~kmask;
     const uint32_t base = kappa & kmask;
@@ -82,9 +82,55 @@ __device__ float llr_cond(const float *se, int m, int j, uint32_t kmask, uint32_
         else ln0 = log_add(ln0, lp);
         sub = (sub - free_mask) & free_mask;
     } while (sub);
-    if (ln0 == -INFINITY) return -llr_max;
-    if (ln1 == -INFINITY) return llr_max;
-    return fminf(fmaxf(ln0 - ln1, -llr_max), llr_max);
+    if (ln0 == -INFINITY) return -1e30f;
+    if (ln1 == -INFINITY) return 1e30f;
+    return ln0 - ln1;
+}
+
+__device__ __forceinline__ float llr_clamp(float L, float llr_max) { return fminf(fmaxf(L, -llr_max), llr_max); }
+
+__device__ float llr_cond(const float *se, int m, int j, uint32_t kmask, uint32_t kappa, float x, float inv_sigma,
+                          float llr_max) {
+    return llr_clamp(llr_raw(se, m, j, kmask, kappa, x, inv_sigma), llr_max);
+}
+
+// index of the known-bit pattern kappa among the 2^|K| patterns (bits of K in order)
+__device__ __forceinline__ int combo_of(uint32_t kmask, uint32_t kappa) {
+    int c = 0, t = 0;
+    for (uint32_t mk = kmask; mk; mk &= mk - 1, ++t) c |= (int)((kappa >> (__ffs(mk) - 1)) & 1u) << t;
+    return c;
+}
+__device__ __forceinline__ uint32_t kappa_of(uint32_t kmask, int combo) {
+    uint32_t k = 0u;
+    int t = 0;
+    for (uint32_t mk = kmask; mk; mk &= mk - 1, ++t) k |= (uint32_t)((combo >> t) & 1) << (__ffs(mk) - 1);
+    return k;
+}
+
+__global__ void k_llr_table(LlrParams p, float *__restrict__ table, int combos) {
+    __shared__ float se[256];
+    for (int i = threadIdx.x; i < 255; i += blockDim.x) se[i] = p.edges[i];
+    __syncthreads();
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= combos * LLR_NTAB) return;
+    const int combo = idx / LLR_NTAB, i = idx % LLR_NTAB;
+    const float x = -LLR_XMAX + (float)(i - 1) * LLR_H;
+    table[idx] = llr_raw(se, p.m, p.j, p.known_mask, kappa_of(p.known_mask, combo), x, p.inv_sigma);
+}
+
+// L(x) from the table (cubic Lagrange through grid points i-1..i+2) or exactly
+__device__ __forceinline__ float llr_eval(const LlrParams &p, const float *se, uint32_t kappa, float x) {
+    const float u = (x + LLR_XMAX) * (1.0f / LLR_H);
+    if (p.table && u >= 0.0f && u < 4095.0f) {
+        const int i = (int)u;
+        const float t = u - (float)i;
+        const float *f = p.table + (size_t)combo_of(p.known_mask, kappa) * LLR_NTAB + i;  // f[0] = grid point i-1
+        const float tm1 = t - 1.0f, tm2 = t - 2.0f, tp1 = t + 1.0f;
+        const float L = (-t * tm1 * tm2 * (1.0f / 6.0f)) * f[0] + (tp1 * tm1 * tm2 * 0.5f) * f[1] +
+                        (-tp1 * t * tm2 * 0.5f) * f[2] + (tp1 * t * tm1 * (1.0f / 6.0f)) * f[3];
+        return llr_clamp(L, p.llr_max);
+    }
+    return llr_cond(se, p.m, p.j, p.known_mask, kappa, x, p.inv_sigma, p.llr_max);
 }
 
 // public API: natural layout out[f][v]
@@ -95,7 +141,7 @@ __global__ void k_llr_slice(LlrParams p, const float *__restrict__ x, const uint
     __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t kappa = p.known_mask ? known_label[i] : 0u;
-        out[i] = llr_cond(se, p.m, p.j, p.known_mask, kappa, x[i], p.inv_sigma, p.llr_max);
+        out[i] = llr_eval(p, se, kappa, x[i]);
     }
 }
 
@@ -124,7 +170,7 @@ __global__ void __launch_bounds__(256) k_llr_interleaved(LlrParams p, const floa
                     if ((p.known_mask >> jj) & 1u)
                         kappa |= ((p.known_bits[jj][(size_t)f * Wn + (v >> 5)] >> (v & 31)) & 1u) << jj;
             }
-            val = llr_cond(se, p.m, p.j, p.known_mask, kappa, x[(size_t)f * n + v], p.inv_sigma, p.llr_max);
+            val = llr_eval(p, se, kappa, x[(size_t)f * n + v]);
         }
         sm[fl][tx] = val * LOG2E;  // arena: log2 units
     }
@@ -150,6 +196,15 @@ static int grid_for(int64_t work, int block) {
     int64_t g = (work + block - 1) / block;
     if (g > 148 * 32) g = 148 * 32;
     return (int)(g < 1 ? 1 : g);
+}
+
+// table for p (p.table is the destination); returns false when the grid is too coarse for sigma_n
+bool launch_llr_table(const LlrParams &p, float *table, cudaStream_t s) {
+    if (LLR_H * p.inv_sigma > 0.02f) return false;
+    const int combos = 1 << __builtin_popcount(p.known_mask);
+    const int total = combos * LLR_NTAB;
+    k_llr_table<<<(total + 255) / 256, 256, 0, s>>>(p, table, combos);
+    return true;
 }
 
 void launch_llr_slice(const LlrParams &p, const float *x, const uint8_t *known_label, int32_t F, int32_t n,
