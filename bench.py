@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--splits", type=int, default=1, help="concurrent frame ranges per GPU (streams)")
     return ap.parse_args()
 
 
@@ -182,8 +183,13 @@ def main():
     F = args.frames or cfg.frames
     n = cfg.n
     stream = torch.cuda.current_stream(device)
-    pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, device, cfg.max_iter, cfg.q_max,
-                      stream)
+    if args.splits > 1:
+        from paper_2108_08418_b200.pipeline import SplitPipeline
+        pipe = SplitPipeline(args.splits, cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, device,
+                             cfg.max_iter, cfg.q_max)
+    else:
+        pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, device, cfg.max_iter, cfg.q_max,
+                          stream)
     # rank r owns frames [r F, (r+1) F): per-frame-chunk seeding => identical data for any GPU count
     first, _ = cdist.shard(F, rank)
     x, y = torch_quadratures(F, n, cfg.gamma, device, first_frame=first)
@@ -232,12 +238,18 @@ def main():
     # roofline pass: same steps with per-kernel CUDA events on the launching stream
     prof = None
     if not args.no_profile:
-        cvsr.cvsr_ctx_set_profiling(pipe.ctx, True)
-        cvsr.cvsr_ctx_kernel_times(pipe.ctx)  # reset
+        ctxs = [p.ctx for p in pipe.parts] if args.splits > 1 else [pipe.ctx]
+        for c in ctxs:
+            cvsr.cvsr_ctx_set_profiling(c, True)
+            cvsr.cvsr_ctx_kernel_times(c)  # reset
         for _ in range(args.steps):
             pipe.step(x, y)
-        prof = cvsr.cvsr_ctx_kernel_times(pipe.ctx)
-        cvsr.cvsr_ctx_set_profiling(pipe.ctx, False)
+        prof = {}
+        for c in ctxs:
+            for k, (ms, cnt) in cvsr.cvsr_ctx_kernel_times(c).items():
+                a, b = prof.get(k, (0.0, 0))
+                prof[k] = (a + ms, b + cnt)
+            cvsr.cvsr_ctx_set_profiling(c, False)
 
     # end-to-end pass: pinned host inputs copied in, results copied out, every step
     e2e = None
@@ -349,6 +361,7 @@ def main():
         "paper_ops_per_s": ops / (ms_step * 1e-3),
         "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
         "gpu_launches": int(launches),
+        "splits": args.splits,
         "e2e": ({"value": bits_step / (tmax[1] / args.steps * 1e-3), "unit": UNIT,
                  "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
                  "ms_per_step": tmax[1] / args.steps} if e2e else None),

@@ -81,3 +81,78 @@ class SRPipeline:
                     cvsr.cvsr_code_free(h)
             cvsr.cvsr_ctx_destroy(self.ctx)
             self.ctx = 0
+
+
+class SplitPipeline:
+    """k SRPipelines over disjoint frame ranges, each on its own stream and host thread.
+
+    Frames are independent, so the k reconciles of a step may run concurrently;
+    while one split is in the low-occupancy tail of a slice (few frames still
+    iterating) the other's kernels fill the GPU.  Results are bit-identical to
+    a single pipeline (per-frame computation does not depend on batching).
+    """
+
+    def __init__(self, k: int, m: int, edges, codes: Sequence, order: Sequence[int], sigma_n: float, n: int,
+                 frames: int, device: torch.device, max_iter: int = 100, msg_clamp: float = 40.0):
+        import concurrent.futures as cf
+        self.k = k
+        self.frames, self.n, self.m = frames, n, m
+        bounds = [frames * i // k for i in range(k + 1)]
+        self.ranges = [(bounds[i], bounds[i + 1]) for i in range(k)]
+        self.streams = [torch.cuda.Stream(device) for _ in range(k)]
+        self.parts = [SRPipeline(m, edges, codes, order, sigma_n, n, b - a, device, max_iter, msg_clamp, stream=s)
+                      for (a, b), s in zip(self.ranges, self.streams)]
+        self.pool = cf.ThreadPoolExecutor(max_workers=k)
+        self.device = device
+
+    def step(self, x: torch.Tensor, y: torch.Tensor, want_stats: bool = False):
+        main = torch.cuda.current_stream(self.device)
+        ev = main.record_event()
+        for s in self.streams:
+            s.wait_event(ev)
+
+        def run(i):
+            a, b = self.ranges[i]
+            with torch.cuda.stream(self.streams[i]):
+                return self.parts[i].step(x[a:b], y[a:b], want_stats)
+
+        res = list(self.pool.map(run, range(self.k)))
+        for s in self.streams:
+            main.wait_stream(s)
+        if not want_stats:
+            return None
+        out = {key: 0 for key in ("frames", "frames_ok", "bits_reconciled")}
+        for key in ("attempted", "converged", "iters_sum", "edge_iters"):
+            out[key] = [sum(r[key][j] for r in res) for j in range(self.m)]
+        for r in res:
+            for key in ("frames", "frames_ok", "bits_reconciled"):
+                out[key] += r[key]
+        out["alice_seconds"] = max(r["alice_seconds"] for r in res)
+        return out
+
+    def count_errors(self):
+        tot = [0, 0, 0]
+        for p in self.parts:
+            c = p.count_errors()
+            tot = [a + b for a, b in zip(tot, c)]
+        return tuple(tot)
+
+    @property
+    def iters(self):
+        return torch.cat([p.iters for p in self.parts])
+
+    @property
+    def label_alice(self):
+        return torch.cat([p.label_alice for p in self.parts])
+
+    @property
+    def frame_ok(self):
+        return torch.cat([p.frame_ok for p in self.parts])
+
+    def launches(self) -> int:
+        return sum(p.launches() for p in self.parts)
+
+    def close(self) -> None:
+        for p in self.parts:
+            p.close()
+        self.pool.shutdown()
