@@ -206,6 +206,29 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
 cvsr_status cvsr_count_errors(cvsr_ctx *ctx, const uint8_t *label_alice, const uint8_t *label_bob,
                               const uint8_t *frame_ok, int32_t frames, int32_t n, int64_t *counts_out);
 
+/* ------------------------------------------------------------- session */
+/* One batch of the whole hot path (Bob + Alice) with library-owned device
+ * buffers: cvsr_session_run = cvsr_quantise(y) -> cvsr_syndrome (coded
+ * slices) / cvsr_slice_bits (disclosed slices) -> cvsr_reconcile(x).  The
+ * codes must stay loaded while the session lives.  Errors as above; on
+ * CVSR_ECUDA the session must be destroyed. */
+typedef struct cvsr_session cvsr_session;
+cvsr_status cvsr_session_create(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *codes, const int32_t *order,
+                                const cvsr_quantiser *q, float sigma_n, int32_t n, int32_t frames,
+                                const cvsr_decode_opts *opts, cvsr_session **out);
+/* x, y: DEVICE float[frames][n]; stats_out optional (synchronises). */
+cvsr_status cvsr_session_run(cvsr_session *s, const float *x, const float *y, cvsr_stats *stats_out);
+/* x_host, y_host: HOST float[frames][n] (pinned for overlap); copies them in,
+ * runs the step and copies Alice's labels (label_host uint8[frames][n],
+ * nullable), frame_ok_host uint8[frames] and iters_host int32[frames][m]
+ * (nullable) back; synchronises.  This is the end-to-end entry point. */
+cvsr_status cvsr_session_run_host(cvsr_session *s, const float *x_host, const float *y_host, uint8_t *label_host,
+                                  uint8_t *frame_ok_host, int32_t *iters_host, cvsr_stats *stats_out);
+/* device pointers of the session's result buffers (any output may be NULL) */
+cvsr_status cvsr_session_buffers(const cvsr_session *s, uint8_t **label_bob, uint8_t **label_alice,
+                                 uint8_t **frame_ok, int32_t **iters);
+void cvsr_session_destroy(cvsr_session *s);
+
 #ifdef __cplusplus
 }
 #endif

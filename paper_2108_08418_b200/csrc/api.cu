@@ -247,6 +247,9 @@ cvsr_status check_quantiser(const cvsr_quantiser *q) {
 
 }  // namespace
 
+// internal accessor for session.cu (not part of the ABI)
+cudaStream_t cvsr_internal_ctx_stream(cvsr_ctx *ctx) { return ctx->stream; }
+
 // =================================================================== ABI
 
 extern "C" {

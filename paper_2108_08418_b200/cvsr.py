@@ -80,6 +80,12 @@ _SIGS = {
     "cvsr_reconcile": ([_vp, _i32, _P(_vp), _P(_i32), _P(cvsr_quantiser), _f32, _vp, _P(_vp), _i32, _i32,
                         _P(cvsr_decode_opts), _vp, _vp, _vp, _P(cvsr_stats)], _i32),
     "cvsr_count_errors": ([_vp, _vp, _vp, _vp, _i32, _i32, _P(_i64)], _i32),
+    "cvsr_session_create": ([_vp, _i32, _P(_vp), _P(_i32), _P(cvsr_quantiser), _f32, _i32, _i32,
+                             _P(cvsr_decode_opts), _P(_vp)], _i32),
+    "cvsr_session_run": ([_vp, _vp, _vp, _P(cvsr_stats)], _i32),
+    "cvsr_session_run_host": ([_vp, _vp, _vp, _vp, _vp, _vp, _P(cvsr_stats)], _i32),
+    "cvsr_session_buffers": ([_vp, _P(_vp), _P(_vp), _P(_vp), _P(_vp)], _i32),
+    "cvsr_session_destroy": ([_vp], None),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -246,3 +252,42 @@ def cvsr_count_errors(ctx: int, label_alice, label_bob, frame_ok, frames: int, n
     out = (_i64 * 3)()
     _call("cvsr_count_errors", ctx, _ptr(label_alice), _ptr(label_bob), _ptr(frame_ok), frames, n, out)
     return tuple(int(v) for v in out)
+
+
+# ---------------------------------------------------------------- session
+
+def cvsr_session_create(ctx: int, m: int, codes: Sequence[Optional[int]], order: Sequence[int], q: cvsr_quantiser,
+                        sigma_n: float, n: int, frames: int, opts: cvsr_decode_opts) -> int:
+    h = _vp()
+    _call("cvsr_session_create", ctx, m, (_vp * m)(*[c if c else None for c in codes]), (_i32 * m)(*order),
+          ctypes.byref(q), sigma_n, n, frames, ctypes.byref(opts), ctypes.byref(h))
+    return h.value
+
+
+def cvsr_session_run(sess: int, x, y, want_stats: bool = False, m: int = 8) -> Optional[dict]:
+    st = cvsr_stats() if want_stats else None
+    _call("cvsr_session_run", sess, _ptr(x), _ptr(y), ctypes.byref(st) if st is not None else None)
+    return st.as_dict(m) if st is not None else None
+
+
+def cvsr_session_run_host(sess: int, x_host, y_host, label_host, frame_ok_host, iters_host=None,
+                          want_stats: bool = False, m: int = 8) -> Optional[dict]:
+    """Host buffers: torch CPU tensors (pinned for overlapped copies) or numpy arrays."""
+    def hp(a):
+        if a is None:
+            return None
+        return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+    st = cvsr_stats() if want_stats else None
+    _call("cvsr_session_run_host", sess, hp(x_host), hp(y_host), hp(label_host), hp(frame_ok_host), hp(iters_host),
+          ctypes.byref(st) if st is not None else None)
+    return st.as_dict(m) if st is not None else None
+
+
+def cvsr_session_buffers(sess: int):
+    a, b, c, d = _vp(), _vp(), _vp(), _vp()
+    _call("cvsr_session_buffers", sess, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d))
+    return a.value, b.value, c.value, d.value
+
+
+def cvsr_session_destroy(sess: int) -> None:
+    _lib.cvsr_session_destroy(sess)

@@ -374,3 +374,30 @@ def test_reconcile_parity_other_configs(cv, ctx, name, n, frames):
     assert both.sum() >= 1
     assert np.array_equal(g["label"][both], lab_ref[both])
     assert np.sum(g["ok"] != ok_ref) <= max(1, frames // 20)
+
+
+def test_session_host_and_device_match_pipeline(cv, ctx):
+    """cvsr_session_run / cvsr_session_run_host reproduce the composed pipeline exactly."""
+    cfg = configs.scaled(configs.C2, 4096, 40)
+    codes_l = cfg.build_codes()
+    x, y = awgn.quadratures(cfg.frames, cfg.n, cfg.gamma, seed=41)
+    g = _run_reconcile(cv, cfg, codes_l, x, y, cfg.frames, cfg.n, cfg.max_iter)
+    hs = [load(cv, ctx, c) if c is not None else None for c in codes_l]
+    sess = cv.cvsr_session_create(ctx, cfg.m, hs, cfg.order, cv.make_quantiser(cfg.edges()), cfg.sigma_n, cfg.n,
+                                  cfg.frames, cv.decode_opts(cfg.max_iter, 40.0))
+    lab = np.empty((cfg.frames, cfg.n), np.uint8)
+    ok = np.empty(cfg.frames, np.uint8)
+    it = np.empty((cfg.frames, cfg.m), np.int32)
+    st = cv.cvsr_session_run_host(sess, np.ascontiguousarray(x), np.ascontiguousarray(y), lab, ok, it,
+                                  want_stats=True, m=cfg.m)
+    assert np.array_equal(lab, g["label"]) and np.array_equal(ok, g["ok"]) and np.array_equal(it, g["iters"])
+    assert st["frames_ok"] == int(ok.sum())
+    xd, yd = dev(x), dev(y)
+    st2 = cv.cvsr_session_run(sess, xd, yd, want_stats=True, m=cfg.m)
+    assert st2["frames_ok"] == st["frames_ok"] and st2["iters_sum"] == st["iters_sum"]
+    bob, alice, okp, itp = cv.cvsr_session_buffers(sess)
+    assert cv.cvsr_count_errors(ctx, alice, bob, okp, cfg.frames, cfg.n) == g["errors"]
+    cv.cvsr_session_destroy(sess)
+    for h in hs:
+        if h:
+            cv.cvsr_code_free(h)
