@@ -34,17 +34,34 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every .cu to an object in parallel, then link libcvsr.so."""
     if not force and not stale():
         return LIB
+    import concurrent.futures as cf
+    import tempfile
+    objdir = tempfile.mkdtemp(prefix="cvsr_build_")
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc(), *flags, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(len(SOURCES), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    log = "".join(r.stderr for _, r in results)
+    for _, r in results:
+        if r.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + r.stderr[-6000:])
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), *SOURCES, "-o", tmp]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stderr[-6000:])
+    link = subprocess.run([nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
+                           *[o for o, _ in results], "-o", tmp], capture_output=True, text=True)
+    if link.returncode != 0:
+        raise RuntimeError("nvcc link failed:\n" + link.stderr[-6000:])
     if verbose:
-        print(res.stderr)
+        print(log)
     with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
-        f.write(res.stderr)
+        f.write(log)
     os.replace(tmp, LIB)
     return LIB
 

@@ -27,6 +27,8 @@
 //   VN: post_v = L_v + sum_e r_e ; q_e = clamp(post_v - r_e, +-Q_MAX);
 //       xhat_v = [post_v < 0].
 //   The syndrome test H xhat = s of iteration k-1 is fused into CN pass k.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "vec.cuh"
@@ -146,7 +148,70 @@ __device__ __noinline__ void cn_check_generic(float *__restrict__ m, int deg, ui
     }
 }
 
-template <int DCT, int S>  // DCT = max check degree (templated body) or 0 = generic
+// One group of up to CPW consecutive checks of tile t (rp: lane i <= nc holds
+// row_ptr[c0 + i]).  Returns this group's unsatisfied-lane words (syndrome test
+// of decision k-1), already masked by act.
+template <int DCT, int S>
+__device__ __forceinline__ uint4 cn_group(const CodeDev &cd, const DecState &ds, int t, const uint4 &act, int c0, int nc,
+                                          int rp, int lane, float qmax2, int check_only) {
+    int lo[CPW + 1];
+#pragma unroll
+    for (int i = 0; i <= CPW; ++i) lo[i] = __shfl_sync(FULL, rp, i <= nc ? i : nc);
+    const int ebeg = lo[0], eend = lo[nc];
+    // per-check parity accumulators, seeded with the syndrome bits s_c
+    uint4 par[CPW];
+#pragma unroll
+    for (int i = 0; i < CPW; ++i)
+        par[i] = (i < nc) ? ds.st[(size_t)t * cd.M + c0 + i] : make_uint4(0u, 0u, 0u, 0u);
+    // hard-decision word of this lane's edge (first 32 edges), issued before the message pass
+    const uint4 *hbt = ds.hb + (size_t)t * cd.n;
+    int e = ebeg + lane;
+    uint4 h = make_uint4(0u, 0u, 0u, 0u);
+    if (e < eend) h = hbt[cd.col_idx[e]];
+    if (!check_only) {
+        const uint32_t al = lane_act<S>(act, lane);
+        float *mt = ds.msg + (size_t)t * cd.E * LANES * S + (size_t)lane * S;
+#pragma unroll
+        for (int i = 0; i < CPW; ++i) {
+            if (i < nc) {
+                const int deg = lo[i + 1] - lo[i];
+                float *m = mt + (size_t)lo[i] * LANES * S;
+                const uint32_t sb = lane_act<S>(par[i], lane);
+                if constexpr (DCT > 0) cn_check<DCT, S>(m, deg, sb, al, qmax2);  // DCT = max_dc >= deg
+                else cn_check_generic<S>(m, deg, sb, al, qmax2);
+            }
+        }
+    }
+    // syndrome test of decision k-1 (H xhat = s), chunks of 32 edges
+    for (int e0 = ebeg;;) {
+#pragma unroll
+        for (int i = 0; i < CPW; ++i) {
+            const bool in = (i < nc) && e >= lo[i] && e < lo[i + 1];
+            par[i].x ^= __reduce_xor_sync(FULL, in ? h.x : 0u);
+            if (S > 1) par[i].y ^= __reduce_xor_sync(FULL, in ? h.y : 0u);
+            if (S > 2) {
+                par[i].z ^= __reduce_xor_sync(FULL, in ? h.z : 0u);
+                par[i].w ^= __reduce_xor_sync(FULL, in ? h.w : 0u);
+            }
+        }
+        e0 += 32;
+        if (e0 >= eend) break;
+        e = e0 + lane;
+        h = make_uint4(0u, 0u, 0u, 0u);
+        if (e < eend) h = hbt[cd.col_idx[e]];
+    }
+    uint4 u = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int i = 0; i < CPW; ++i) {
+        u.x |= par[i].x; u.y |= par[i].y; u.z |= par[i].z; u.w |= par[i].w;
+    }
+    u.x &= act.x; u.y &= act.y; u.z &= act.z; u.w &= act.w;
+    return u;
+}
+
+// GPW groups of CPW checks per warp: the next group's row pointers are loaded
+// and its message lines prefetched into L2 while the current group computes.
+template <int DCT, int S, int GPW>  // DCT = max check degree (templated body) or 0 = generic
 __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 20) ? 4 : (DCT * S <= 32 ? 3 : 2))
     k_cn(CodeDev cd, DecState ds, float qmax2, int check_only) {
     const int ti = blockIdx.y;
@@ -159,66 +224,31 @@ __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 20) ? 4 : (DCT *
     if (threadIdx.x < SUBS) s_unsat[threadIdx.x] = 0u;
     if (threadIdx.x == 0) s_done = 0;
     __syncthreads();
-    const int c0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * CPW;
-    const int nc = min(CPW, cd.M - c0);
-    if (nc > 0) {
-        const int rp = (lane <= nc) ? cd.row_ptr[c0 + lane] : 0;
-        int lo[CPW + 1];
-#pragma unroll
-        for (int i = 0; i <= CPW; ++i) lo[i] = __shfl_sync(FULL, rp, i <= nc ? i : nc);
-        const int ebeg = lo[0], eend = lo[nc];
-        // per-check parity accumulators, seeded with the syndrome bits s_c
-        uint4 par[CPW];
-#pragma unroll
-        for (int i = 0; i < CPW; ++i)
-            par[i] = (i < nc) ? ds.st[(size_t)t * cd.M + c0 + i] : make_uint4(0u, 0u, 0u, 0u);
-        // hard-decision word of this lane's edge (first 32 edges), issued before the message pass
-        const uint4 *hbt = ds.hb + (size_t)t * cd.n;
-        int e = ebeg + lane;
-        uint4 h = make_uint4(0u, 0u, 0u, 0u);
-        if (e < eend) h = hbt[cd.col_idx[e]];
-        if (!check_only) {
-            const uint32_t al = lane_act<S>(act, lane);
-            float *mt = ds.msg + (size_t)t * cd.E * LANES * S + (size_t)lane * S;
-#pragma unroll
-            for (int i = 0; i < CPW; ++i) {
-                if (i < nc) {
-                    const int deg = lo[i + 1] - lo[i];
-                    float *m = mt + (size_t)lo[i] * LANES * S;
-                    const uint32_t sb = lane_act<S>(par[i], lane);
-                    if constexpr (DCT > 0) cn_check<DCT, S>(m, deg, sb, al, qmax2);  // DCT = max_dc >= deg
-                    else cn_check_generic<S>(m, deg, sb, al, qmax2);
-                }
-            }
+    int c0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * CPW * GPW;
+    int nc = min(CPW, cd.M - c0);
+    int rp = (nc > 0 && lane <= nc) ? cd.row_ptr[c0 + lane] : 0;
+    uint4 u = make_uint4(0u, 0u, 0u, 0u);
+    const char *tbase = reinterpret_cast<const char *>(ds.msg + (size_t)t * cd.E * LANES * S);
+    for (int g = 0; g < GPW && nc > 0; ++g) {
+        const int c1 = c0 + CPW;
+        const int nc1 = (g + 1 < GPW) ? min(CPW, cd.M - c1) : 0;
+        const int rp1 = (nc1 > 0 && lane <= nc1) ? cd.row_ptr[c1 + lane] : 0;
+        if (GPW > 1 && nc1 > 0 && !check_only) {
+            // the next group's messages follow this group's contiguously; prefetch about as many lines
+            const int eb = __shfl_sync(FULL, rp, nc), span = eb - __shfl_sync(FULL, rp, 0);
+            const char *p0 = tbase + (size_t)eb * LANES * S * 4;
+            const int lines = span * S / 4;  // 128-byte lines
+            for (int l = lane; l < lines; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + (size_t)l * 128));
         }
-        // syndrome test of decision k-1 (H xhat = s), chunks of 32 edges
-        for (int e0 = ebeg;;) {
-#pragma unroll
-            for (int i = 0; i < CPW; ++i) {
-                const bool in = (i < nc) && e >= lo[i] && e < lo[i + 1];
-                par[i].x ^= __reduce_xor_sync(FULL, in ? h.x : 0u);
-                if (S > 1) par[i].y ^= __reduce_xor_sync(FULL, in ? h.y : 0u);
-                if (S > 2) {
-                    par[i].z ^= __reduce_xor_sync(FULL, in ? h.z : 0u);
-                    par[i].w ^= __reduce_xor_sync(FULL, in ? h.w : 0u);
-                }
-            }
-            e0 += 32;
-            if (e0 >= eend) break;
-            e = e0 + lane;
-            h = make_uint4(0u, 0u, 0u, 0u);
-            if (e < eend) h = hbt[cd.col_idx[e]];
-        }
-        uint4 u = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-        for (int i = 0; i < CPW; ++i) {
-            u.x |= par[i].x; u.y |= par[i].y; u.z |= par[i].z; u.w |= par[i].w;
-        }
-        u.x &= act.x; u.y &= act.y; u.z &= act.z; u.w &= act.w;
-        if (lane < S) {
-            const uint32_t v = cmpu(u, lane);
-            if (v) atomicOr(&s_unsat[lane], v);
-        }
+        const uint4 ug = cn_group<DCT, S>(cd, ds, t, act, c0, nc, rp, lane, qmax2, check_only);
+        u.x |= ug.x; u.y |= ug.y; u.z |= ug.z; u.w |= ug.w;
+        c0 = c1;
+        nc = nc1;
+        rp = rp1;
+    }
+    if (lane < S) {
+        const uint32_t v = cmpu(u, lane);
+        if (v) atomicOr(&s_unsat[lane], v);
     }
     // last warp of the block publishes the block's unsatisfied lanes (no barrier in the hot part)
     __threadfence_block();
@@ -577,31 +607,49 @@ __global__ void k_set_counts(DecState ds, int32_t n_active) {
 
 // qmax is in natural LLR units; the arena works in log2 units.  The kernel body
 // is chosen by the code's maximum check degree and the tile width S.
-template <int S>
+template <int S, int GPW>
 static void launch_cn_s(const CodeDev &cd, const DecState &ds, dim3 grid, float q2, int check_only, cudaStream_t s) {
     switch (cd.max_dc) {
-        case 1: case 2: k_cn<2, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 3: k_cn<3, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 4: k_cn<4, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 5: k_cn<5, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 6: k_cn<6, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 7: k_cn<7, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 8: k_cn<8, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 9: k_cn<9, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 10: k_cn<10, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 11: case 12: k_cn<12, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        default: k_cn<0, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 1: case 2: k_cn<2, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 3: k_cn<3, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 4: k_cn<4, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 5: k_cn<5, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 6: k_cn<6, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 7: k_cn<7, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 8: k_cn<8, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 9: k_cn<9, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 10: k_cn<10, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 11: case 12: k_cn<12, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        default: k_cn<0, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
     }
+}
+
+// groups of CPW checks per warp (CVSR_CN_GPW = 1 or 4; experiment switch, default CN_GPW_DEFAULT)
+constexpr int CN_GPW_DEFAULT = 1;
+static int cn_gpw() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("CVSR_CN_GPW");
+        v = (e && atoi(e) == 4) ? 4 : (e && atoi(e) == 1) ? 1 : CN_GPW_DEFAULT;
+    }
+    return v;
 }
 
 void launch_cn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, int check_only, cudaStream_t s) {
     if (grid_tiles <= 0) return;
-    const int per_block = WARPS_PER_BLOCK * CPW;
+    const int gpw = cn_gpw();
+    const int per_block = WARPS_PER_BLOCK * CPW * gpw;
     dim3 grid((cd.M + per_block - 1) / per_block, grid_tiles);
     const float q2 = qmax * LOG2E;
-    if (ds.subs == 4) launch_cn_s<4>(cd, ds, grid, q2, check_only, s);
-    else if (ds.subs == 2) launch_cn_s<2>(cd, ds, grid, q2, check_only, s);
-    else launch_cn_s<1>(cd, ds, grid, q2, check_only, s);
+    if (gpw == 4) {
+        if (ds.subs == 4) launch_cn_s<4, 4>(cd, ds, grid, q2, check_only, s);
+        else if (ds.subs == 2) launch_cn_s<2, 4>(cd, ds, grid, q2, check_only, s);
+        else launch_cn_s<1, 4>(cd, ds, grid, q2, check_only, s);
+    } else {
+        if (ds.subs == 4) launch_cn_s<4, 1>(cd, ds, grid, q2, check_only, s);
+        else if (ds.subs == 2) launch_cn_s<2, 1>(cd, ds, grid, q2, check_only, s);
+        else launch_cn_s<1, 1>(cd, ds, grid, q2, check_only, s);
+    }
 }
 
 template <int DV, int VPW_, bool FIRST, int S>
