@@ -209,9 +209,7 @@ __device__ __forceinline__ uint4 cn_group(const CodeDev &cd, const DecState &ds,
     return u;
 }
 
-// GPW groups of CPW checks per warp: the next group's row pointers are loaded
-// and its message lines prefetched into L2 while the current group computes.
-template <int DCT, int S, int GPW>  // DCT = max check degree (templated body) or 0 = generic
+template <int DCT, int S>  // DCT = max check degree (templated body) or 0 = generic
 __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 20) ? 4 : (DCT * S <= 32 ? 3 : 2))
     k_cn(CodeDev cd, DecState ds, float qmax2, int check_only) {
     const int ti = blockIdx.y;
@@ -224,31 +222,15 @@ __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 20) ? 4 : (DCT *
     if (threadIdx.x < SUBS) s_unsat[threadIdx.x] = 0u;
     if (threadIdx.x == 0) s_done = 0;
     __syncthreads();
-    int c0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * CPW * GPW;
-    int nc = min(CPW, cd.M - c0);
-    int rp = (nc > 0 && lane <= nc) ? cd.row_ptr[c0 + lane] : 0;
-    uint4 u = make_uint4(0u, 0u, 0u, 0u);
-    const char *tbase = reinterpret_cast<const char *>(ds.msg + (size_t)t * cd.E * LANES * S);
-    for (int g = 0; g < GPW && nc > 0; ++g) {
-        const int c1 = c0 + CPW;
-        const int nc1 = (g + 1 < GPW) ? min(CPW, cd.M - c1) : 0;
-        const int rp1 = (nc1 > 0 && lane <= nc1) ? cd.row_ptr[c1 + lane] : 0;
-        if (GPW > 1 && nc1 > 0 && !check_only) {
-            // the next group's messages follow this group's contiguously; prefetch about as many lines
-            const int eb = __shfl_sync(FULL, rp, nc), span = eb - __shfl_sync(FULL, rp, 0);
-            const char *p0 = tbase + (size_t)eb * LANES * S * 4;
-            const int lines = span * S / 4;  // 128-byte lines
-            for (int l = lane; l < lines; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + (size_t)l * 128));
+    const int c0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * CPW;
+    const int nc = min(CPW, cd.M - c0);
+    if (nc > 0) {
+        const int rp = (lane <= nc) ? cd.row_ptr[c0 + lane] : 0;
+        const uint4 u = cn_group<DCT, S>(cd, ds, t, act, c0, nc, rp, lane, qmax2, check_only);
+        if (lane < S) {
+            const uint32_t v = cmpu(u, lane);
+            if (v) atomicOr(&s_unsat[lane], v);
         }
-        const uint4 ug = cn_group<DCT, S>(cd, ds, t, act, c0, nc, rp, lane, qmax2, check_only);
-        u.x |= ug.x; u.y |= ug.y; u.z |= ug.z; u.w |= ug.w;
-        c0 = c1;
-        nc = nc1;
-        rp = rp1;
-    }
-    if (lane < S) {
-        const uint32_t v = cmpu(u, lane);
-        if (v) atomicOr(&s_unsat[lane], v);
     }
     // last warp of the block publishes the block's unsatisfied lanes (no barrier in the hot part)
     __threadfence_block();
@@ -607,49 +589,31 @@ __global__ void k_set_counts(DecState ds, int32_t n_active) {
 
 // qmax is in natural LLR units; the arena works in log2 units.  The kernel body
 // is chosen by the code's maximum check degree and the tile width S.
-template <int S, int GPW>
+template <int S>
 static void launch_cn_s(const CodeDev &cd, const DecState &ds, dim3 grid, float q2, int check_only, cudaStream_t s) {
     switch (cd.max_dc) {
-        case 1: case 2: k_cn<2, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 3: k_cn<3, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 4: k_cn<4, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 5: k_cn<5, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 6: k_cn<6, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 7: k_cn<7, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 8: k_cn<8, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 9: k_cn<9, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 10: k_cn<10, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        case 11: case 12: k_cn<12, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
-        default: k_cn<0, S, GPW><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 1: case 2: k_cn<2, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 3: k_cn<3, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 4: k_cn<4, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 5: k_cn<5, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 6: k_cn<6, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 7: k_cn<7, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 8: k_cn<8, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 9: k_cn<9, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 10: k_cn<10, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        case 11: case 12: k_cn<12, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
+        default: k_cn<0, S><<<grid, BLOCK, 0, s>>>(cd, ds, q2, check_only); break;
     }
-}
-
-// groups of CPW checks per warp (CVSR_CN_GPW = 1 or 4; experiment switch, default CN_GPW_DEFAULT)
-constexpr int CN_GPW_DEFAULT = 1;
-static int cn_gpw() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("CVSR_CN_GPW");
-        v = (e && atoi(e) == 4) ? 4 : (e && atoi(e) == 1) ? 1 : CN_GPW_DEFAULT;
-    }
-    return v;
 }
 
 void launch_cn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, int check_only, cudaStream_t s) {
     if (grid_tiles <= 0) return;
-    const int gpw = cn_gpw();
-    const int per_block = WARPS_PER_BLOCK * CPW * gpw;
+    const int per_block = WARPS_PER_BLOCK * CPW;
     dim3 grid((cd.M + per_block - 1) / per_block, grid_tiles);
     const float q2 = qmax * LOG2E;
-    if (gpw == 4) {
-        if (ds.subs == 4) launch_cn_s<4, 4>(cd, ds, grid, q2, check_only, s);
-        else if (ds.subs == 2) launch_cn_s<2, 4>(cd, ds, grid, q2, check_only, s);
-        else launch_cn_s<1, 4>(cd, ds, grid, q2, check_only, s);
-    } else {
-        if (ds.subs == 4) launch_cn_s<4, 1>(cd, ds, grid, q2, check_only, s);
-        else if (ds.subs == 2) launch_cn_s<2, 1>(cd, ds, grid, q2, check_only, s);
-        else launch_cn_s<1, 1>(cd, ds, grid, q2, check_only, s);
-    }
+    if (ds.subs == 4) launch_cn_s<4>(cd, ds, grid, q2, check_only, s);
+    else if (ds.subs == 2) launch_cn_s<2>(cd, ds, grid, q2, check_only, s);
+    else launch_cn_s<1>(cd, ds, grid, q2, check_only, s);
 }
 
 template <int DV, int VPW_, bool FIRST, int S>
