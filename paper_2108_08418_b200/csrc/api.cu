@@ -2,6 +2,7 @@
 // layout (B1), the BP iteration scheduler (B3) and the multi-stage slice
 // driver (PAPER.md:114 steps 4-6).
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -144,13 +145,35 @@ cvsr_status scratch_reserve(cvsr_ctx *ctx, size_t bytes, char **out) {
     return CVSR_OK;
 }
 
-size_t decstate_bytes(int tiles, int frames, int64_t n, int64_t M, int64_t E) {
-    const size_t T = (size_t)LANES * choose_subs(frames);
+// fused iteration scheduler (k_iter) on/off: CVSR_FUSED=0 selects the kernel-per-pass path
+bool fused_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("CVSR_FUSED");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// frames per lane: choose_subs(frames), narrowed in fused mode so that one tile's
+// message lines (E x 128 S bytes) stay well inside L2 for the CN -> VN hand-off
+int pick_subs(int32_t frames, int64_t E) {
+    int s = choose_subs(frames);
+    if (fused_enabled())
+        while (s > 1 && (double)E * LANES * s * 4 > 64.0e6) s >>= 1;
+    return s;
+}
+
+int tiles_for(int32_t frames, int subs) { return (frames + LANES * subs - 1) / (LANES * subs); }
+
+size_t decstate_bytes(int tiles, int frames, int subs, int64_t n, int64_t M, int64_t E) {
+    const size_t T = (size_t)LANES * subs;
     size_t b = 0;
     b += align_up((size_t)tiles * E * T * sizeof(float));
     b += align_up((size_t)tiles * n * T * sizeof(float));
-    b += align_up((size_t)tiles * n * sizeof(uint4));
+    b += 2 * align_up((size_t)tiles * n * sizeof(uint4));
     b += align_up((size_t)tiles * M * sizeof(uint4));
+    b += 2 * align_up((size_t)tiles * sizeof(int32_t)) + align_up(sizeof(int32_t));
     b += 5 * align_up((size_t)tiles * sizeof(uint4));
     b += align_up(16 * sizeof(int32_t));
     b += align_up((size_t)frames * sizeof(int32_t));
@@ -158,17 +181,21 @@ size_t decstate_bytes(int tiles, int frames, int64_t n, int64_t M, int64_t E) {
     return b;
 }
 
-DecState carve_decstate(Carve &cv, int tiles, int frames, int64_t n, int64_t M, int64_t E, int32_t *iters_user,
+DecState carve_decstate(Carve &cv, int tiles, int frames, int subs, int64_t n, int64_t M, int64_t E, int32_t *iters_user,
                         uint8_t *conv_user) {
     DecState ds{};
     ds.tiles = tiles;
     ds.frames = frames;
-    ds.subs = choose_subs(frames);
+    ds.subs = subs;
     ds.tile_frames = LANES * ds.subs;
     const size_t T = (size_t)ds.tile_frames;
     ds.msg = cv.take<float>((size_t)tiles * E * T * sizeof(float));
     ds.L = cv.take<float>((size_t)tiles * n * T * sizeof(float));
     ds.hb = cv.take<uint4>((size_t)tiles * n * sizeof(uint4));
+    ds.hb2 = cv.take<uint4>((size_t)tiles * n * sizeof(uint4));
+    ds.cn_done = cv.take<int32_t>((size_t)tiles * sizeof(int32_t));
+    ds.cn_ready = cv.take<int32_t>((size_t)tiles * sizeof(int32_t));
+    ds.fused_work = cv.take<int32_t>(sizeof(int32_t));
     ds.st = cv.take<uint4>((size_t)tiles * M * sizeof(uint4));
     ds.tile_active = cv.take<uint4>((size_t)tiles * sizeof(uint4));
     ds.tile_unsat = cv.take<uint4>((size_t)tiles * sizeof(uint4));
@@ -187,33 +214,51 @@ DecState carve_decstate(Carve &cv, int tiles, int frames, int64_t n, int64_t M, 
 // ds.L, ds.st, tile state and counts initialised.  Host control: iterations
 // are launched LOOKAHEAD ahead of a mapped-memory progress counter written by
 // the status kernel; the counter also bounds the grid's tile dimension.
-cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds, int max_iter, float qmax,
+cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0, int max_iter, float qmax,
                        uint32_t *bits_out) {
     cudaStream_t s = ctx->stream;
     const CodeDev &cd = code->d;
     volatile int32_t *hc = ctx->host_counts;
-    const int32_t epoch = ++ctx->epoch;
-    (void)epoch;
     // the mapped counter is only read after an event of THIS run completed;
-    // every status kernel of this run writes it, so stale values are impossible.
+    // every status/list kernel of this run writes it, so stale values are impossible.
+    const bool fused = fused_enabled();
+    const FusedPlan plan = fused ? make_plan(cd, ds0.subs) : FusedPlan{};
+    uint4 *hbuf[2] = {ds0.hb, ds0.hb2};
+    DecState ds = ds0;
     prof_begin(ctx, KC_INIT);
-    int launched = launch_vn(cd, ds, ds.tiles, qmax, true, nullptr, s);
+    int launched = launch_vn(cd, ds, ds.tiles, qmax, true, nullptr, s);  // decision 0 -> hbuf[0]
     prof_end(ctx);
     int bound = ds.tiles;
     for (int k = 1; k <= max_iter + 1; ++k) {
         const int final_pass = (k == max_iter + 1);
-        prof_begin(ctx, KC_CN);
-        launch_cn(cd, ds, bound, qmax, final_pass, s);
-        prof_end(ctx);
-        prof_begin(ctx, KC_CTRL);
-        launch_status(ds, k, max_iter, final_pass, ctx->host_counts_dev, s);
-        launch_retire(ds, cd.n, bound, bits_out, s);
-        prof_end(ctx);
-        launched += 3;
-        if (!final_pass) {
-            prof_begin(ctx, KC_VN);
-            launched += launch_vn(cd, ds, bound, qmax, false, nullptr, s);
+        if (fused && !final_pass) {
+            // CN_k (tests decision k-1 in hbuf[(k-1)&1]) + per-tile status + VN_k (writes hbuf[k&1])
+            DecState dsc = ds0, dsv = ds0;
+            dsc.hb = hbuf[(k - 1) & 1];
+            dsv.hb = hbuf[k & 1];
+            prof_begin(ctx, KC_CN);
+            launch_iter(cd, dsc, dsv, plan, k, qmax, s);
             prof_end(ctx);
+            prof_begin(ctx, KC_CTRL);
+            launch_list(dsc, ctx->host_counts_dev, s);
+            launch_retire(dsc, cd.n, bound, bits_out, s);
+            prof_end(ctx);
+            launched += 3;
+        } else {
+            ds.hb = hbuf[fused ? ((k - 1) & 1) : 0];
+            prof_begin(ctx, KC_CN);
+            launch_cn(cd, ds, bound, qmax, final_pass, s);
+            prof_end(ctx);
+            prof_begin(ctx, KC_CTRL);
+            launch_status(ds, k, max_iter, final_pass, ctx->host_counts_dev, s);
+            launch_retire(ds, cd.n, bound, bits_out, s);
+            prof_end(ctx);
+            launched += 3;
+            if (!final_pass) {
+                prof_begin(ctx, KC_VN);
+                launched += launch_vn(cd, ds, bound, qmax, false, nullptr, s);
+                prof_end(ctx);
+            }
         }
         CK(cudaEventRecord(ctx->ring[k % RING], s));
         if (k >= LOOKAHEAD && !final_pass) {
@@ -626,11 +671,12 @@ cvsr_status cvsr_decode(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, 
     if (!llr || !synd || !bits_out || !converged_out || !iters_out) return fail(CVSR_EINVAL, "null buffer");
     DeviceGuard g(ctx->device);
     const CodeDev &cd = code->d;
-    const int tiles = (frames + LANES * choose_subs(frames) - 1) / (LANES * choose_subs(frames));
+    const int subs = pick_subs(frames, cd.E);
+    const int tiles = tiles_for(frames, subs);
     char *base;
-    if (cvsr_status st = scratch_reserve(ctx, decstate_bytes(tiles, frames, cd.n, cd.M, cd.E), &base)) return st;
+    if (cvsr_status st = scratch_reserve(ctx, decstate_bytes(tiles, frames, subs, cd.n, cd.M, cd.E), &base)) return st;
     Carve cv{base};
-    DecState ds = carve_decstate(cv, tiles, frames, cd.n, cd.M, cd.E, iters_out, converged_out);
+    DecState ds = carve_decstate(cv, tiles, frames, subs, cd.n, cd.M, cd.E, iters_out, converged_out);
     cudaStream_t s = ctx->stream;
     launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, ds.subs, LOG2E, s);
     launch_synd_transpose(synd, frames, cd.M, ds.subs, ds.st, tiles, s);
@@ -652,13 +698,14 @@ cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float 
     if (!llr || !synd) return fail(CVSR_EINVAL, "null buffer");
     DeviceGuard g(ctx->device);
     const CodeDev &cd = code->d;
-    const int tiles = (frames + LANES * choose_subs(frames) - 1) / (LANES * choose_subs(frames));
-    const size_t post_bytes = align_up((size_t)tiles * cd.n * LANES * choose_subs(frames) * sizeof(float));
+    const int subs = choose_subs(frames);
+    const int tiles = tiles_for(frames, subs);
+    const size_t post_bytes = align_up((size_t)tiles * cd.n * LANES * subs * sizeof(float));
     char *base;
-    if (cvsr_status st = scratch_reserve(ctx, decstate_bytes(tiles, frames, cd.n, cd.M, cd.E) + post_bytes, &base))
+    if (cvsr_status st = scratch_reserve(ctx, decstate_bytes(tiles, frames, subs, cd.n, cd.M, cd.E) + post_bytes, &base))
         return st;
     Carve cv{base};
-    DecState ds = carve_decstate(cv, tiles, frames, cd.n, cd.M, cd.E, nullptr, nullptr);
+    DecState ds = carve_decstate(cv, tiles, frames, subs, cd.n, cd.M, cd.E, nullptr, nullptr);
     float *post_il = cv.take<float>(post_bytes);
     cudaStream_t s = ctx->stream;
     launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, ds.subs, LOG2E, s);
@@ -715,14 +762,15 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
     }
     if (!x || !label_out || !frame_ok || !iters) return fail(CVSR_EINVAL, "null buffer");
     DeviceGuard g(ctx->device);
-    const int tiles = (frames + LANES * choose_subs(frames) - 1) / (LANES * choose_subs(frames));
+    const int subs = pick_subs(frames, maxE);
+    const int tiles = tiles_for(frames, subs);
     const int Wn = words_of(n);
-    size_t bytes = decstate_bytes(tiles, frames, n, maxM, maxE);
+    size_t bytes = decstate_bytes(tiles, frames, subs, n, maxM, maxE);
     bytes += (size_t)m * align_up((size_t)frames * Wn * 4) + 3 * align_up((size_t)frames);
     char *base;
     if (cvsr_status st = scratch_reserve(ctx, bytes, &base)) return st;
     Carve cv{base};
-    DecState ds = carve_decstate(cv, tiles, frames, n, maxM, maxE, nullptr, nullptr);
+    DecState ds = carve_decstate(cv, tiles, frames, subs, n, maxM, maxE, nullptr, nullptr);
     uint32_t *bits_dec[8] = {};
     for (int j = 0; j < m; ++j) bits_dec[j] = cv.take<uint32_t>((size_t)frames * Wn * 4);
     uint8_t *alive = cv.take<uint8_t>((size_t)frames);

@@ -260,15 +260,12 @@ __device__ __forceinline__ void vn_finish(const DecState &ds, const CodeDev &cd,
     if (post_dbg && any) stv<S>(post_dbg + (((size_t)t * cd.n + v) * LANES + lane) * S, post);
 }
 
+// one block-chunk of a variable-degree class for tile t (chunk = block index within the class)
 template <int DV, int VPW_, bool FIRST, int S>
-__global__ void __launch_bounds__(BLOCK, 3) k_vn_cls(CodeDev cd, DecState ds, int cls, float qmax2,
-                                                     float *post_dbg) {
-    const int ti = blockIdx.y;
-    if (ti >= ds.counts[0]) return;
-    const int t = ds.active_list[ti];
-    const uint4 act = ds.tile_active[t];
+__device__ __forceinline__ void vn_chunk(const CodeDev &cd, const DecState &ds, int cls, int t, const uint4 &act,
+                                         int chunk, float qmax2, float *post_dbg) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int w0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * VPW_;
+    const int w0 = (chunk * WARPS_PER_BLOCK + warp) * VPW_;
     const int cnt = cd.vc_cnt[cls];
     const int nv = min(VPW_, cnt - w0);
     if (nv <= 0) return;
@@ -330,16 +327,22 @@ __global__ void __launch_bounds__(BLOCK, 3) k_vn_cls(CodeDev cd, DecState ds, in
     }
 }
 
-// any degree: one variable per warp, slots read per edge (mixed / large-degree classes)
-template <bool FIRST, int S>
-__global__ void __launch_bounds__(BLOCK) k_vn_generic(CodeDev cd, DecState ds, int cls, float qmax2,
-                                                      float *post_dbg) {
+template <int DV, int VPW_, bool FIRST, int S>
+__global__ void __launch_bounds__(BLOCK, 3) k_vn_cls(CodeDev cd, DecState ds, int cls, float qmax2,
+                                                     float *post_dbg) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
     const int t = ds.active_list[ti];
     const uint4 act = ds.tile_active[t];
+    vn_chunk<DV, VPW_, FIRST, S>(cd, ds, cls, t, act, blockIdx.x, qmax2, post_dbg);
+}
+
+// any degree: one variable per warp, slots read per edge (mixed / large-degree classes)
+template <bool FIRST, int S>
+__device__ __noinline__ void vn_generic_chunk(const CodeDev &cd, const DecState &ds, int cls, int t, uint4 act,
+                                              int chunk, float qmax2, float *post_dbg) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int w = blockIdx.x * WARPS_PER_BLOCK + warp;
+    const int w = chunk * WARPS_PER_BLOCK + warp;
     if (w >= cd.vc_cnt[cls]) return;
     const int v = cd.vc_vars[cd.vc_off[cls] + w];
     const int beg = cd.col_ptr[v], deg = cd.col_ptr[v + 1] - beg;
@@ -364,6 +367,15 @@ __global__ void __launch_bounds__(BLOCK) k_vn_generic(CodeDev cd, DecState ds, i
         }
     }
     vn_finish<S>(ds, cd, t, v, post, act, any, lane, post_dbg);
+}
+
+template <bool FIRST, int S>
+__global__ void __launch_bounds__(BLOCK) k_vn_generic(CodeDev cd, DecState ds, int cls, float qmax2,
+                                                      float *post_dbg) {
+    const int ti = blockIdx.y;
+    if (ti >= ds.counts[0]) return;
+    const int t = ds.active_list[ti];
+    vn_generic_chunk<FIRST, S>(cd, ds, cls, t, ds.tile_active[t], blockIdx.x, qmax2, post_dbg);
 }
 
 // ------------------------------------------------------------------ scheduling
@@ -454,6 +466,160 @@ __global__ void __launch_bounds__(1024) k_status(DecState ds, int k, int max_ite
         ds.counts[0] = n_act;
         ds.counts[1] = n_ret;
         ds.counts[2] = s_lanes;
+        if (host_counts) {
+            volatile int32_t *h = host_counts;
+            h[0] = n_act;
+            h[1] = n_ret;
+            h[2] = s_lanes;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ fused iteration
+//
+// One persistent launch per BP iteration: blocks grab work items in order
+// [CN chunks of tile t0][VN chunks of t0][CN of t1][VN of t1]...; the last CN
+// block of a tile performs that tile's convergence bookkeeping (status) and
+// releases the tile; VN blocks of the tile wait for the release.  Processing
+// one tile's VN right after its CN means the tile's freshly written C2V lines
+// are read back from L2 and overwritten in L2 by the next V2C values, so most
+// of the CN -> VN hand-off never reaches HBM (tiles are sized to fit L2).
+// Items are grabbed in order and a VN block only waits for CN items that were
+// grabbed earlier by running blocks, so the wait always terminates.
+
+__host__ __device__ constexpr int vpw_for(int d, int S) {
+    return d == 1 ? 6 : d == 2 ? 4 : (d <= 4 ? (S < 4 ? 4 : 2) : 4 / S);
+}
+
+template <bool FIRST, int S>
+__device__ __forceinline__ void vn_dispatch(const CodeDev &cd, const DecState &ds, int c, int t, const uint4 &act,
+                                            int chunk, float qmax2, float *post_dbg) {
+    switch (cd.vc_deg[c]) {
+        case 1: vn_chunk<1, vpw_for(1, S), FIRST, S>(cd, ds, c, t, act, chunk, qmax2, post_dbg); break;
+        case 2: vn_chunk<2, vpw_for(2, S), FIRST, S>(cd, ds, c, t, act, chunk, qmax2, post_dbg); break;
+        case 3: vn_chunk<3, vpw_for(3, S), FIRST, S>(cd, ds, c, t, act, chunk, qmax2, post_dbg); break;
+        case 4: vn_chunk<4, vpw_for(4, S), FIRST, S>(cd, ds, c, t, act, chunk, qmax2, post_dbg); break;
+        case 5: vn_chunk<5, vpw_for(5, S), FIRST, S>(cd, ds, c, t, act, chunk, qmax2, post_dbg); break;
+        case 6: vn_chunk<6, vpw_for(6, S), FIRST, S>(cd, ds, c, t, act, chunk, qmax2, post_dbg); break;
+        case 7: vn_chunk<7, vpw_for(7, S), FIRST, S>(cd, ds, c, t, act, chunk, qmax2, post_dbg); break;
+        case 8: vn_chunk<8, vpw_for(8, S), FIRST, S>(cd, ds, c, t, act, chunk, qmax2, post_dbg); break;
+        default: vn_generic_chunk<FIRST, S>(cd, ds, c, t, act, chunk, qmax2, post_dbg); break;
+    }
+}
+
+template <int DCT, int S>
+__global__ void __launch_bounds__(BLOCK, 2) k_iter(CodeDev cd, DecState dsc, DecState dsv, FusedPlan plan, int k,
+                                                   float qmax2) {
+    __shared__ int s_item, s_last;
+    __shared__ uint32_t s_unsat[SUBS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_items = dsc.counts[0] * plan.items_per_tile;
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(dsc.fused_work, 1);
+        if (threadIdx.x < SUBS) s_unsat[threadIdx.x] = 0u;
+        __syncthreads();
+        const int item = s_item;
+        if (item >= n_items) break;
+        const int ti = item / plan.items_per_tile;
+        int r = item - ti * plan.items_per_tile;
+        const int t = dsc.active_list[ti];
+        if (r < plan.n_cn) {
+            const uint4 act = __ldcg(&dsc.tile_active[t]);
+            const int c0 = (r * WARPS_PER_BLOCK + warp) * CPW;
+            const int nc = min(CPW, cd.M - c0);
+            if (nc > 0) {
+                const int rp = (lane <= nc) ? cd.row_ptr[c0 + lane] : 0;
+                const uint4 u = cn_group<DCT, S>(cd, dsc, t, act, c0, nc, rp, lane, qmax2, 0);
+                if (lane < S) {
+                    const uint32_t v = cmpu(u, lane);
+                    if (v) atomicOr(&s_unsat[lane], v);
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+#pragma unroll
+                for (int q = 0; q < S; ++q)
+                    if (s_unsat[q]) atomicOr(reinterpret_cast<uint32_t *>(&dsc.tile_unsat[t]) + q, s_unsat[q]);
+                __threadfence();
+                s_last = (atomicAdd(&dsc.cn_done[t], 1) == plan.n_cn - 1);
+            }
+            __syncthreads();
+            if (s_last) {
+                // status of tile t: frames whose decision k-1 satisfied every check stop (D = k-1)
+                __threadfence();
+                const uint4 a = __ldcg(&dsc.tile_active[t]);
+                const uint4 u = __ldcg(&dsc.tile_unsat[t]);
+                if (threadIdx.x < LANES * S) {
+                    const int q = threadIdx.x >> 5;
+                    if (((cmpu(a, q) & ~cmpu(u, q)) >> lane) & 1u) {
+                        const int f = t * dsc.tile_frames + q * LANES + lane;
+                        dsc.iters[f] = k - 1;
+                        dsc.conv[f] = 1;
+                    }
+                }
+                if (threadIdx.x == 0) {
+                    dsc.tile_newly[t] = make_uint4(a.x & ~u.x, a.y & ~u.y, a.z & ~u.z, a.w & ~u.w);
+                    dsc.tile_active[t] = make_uint4(a.x & u.x, a.y & u.y, a.z & u.z, a.w & u.w);
+                    dsc.tile_unsat[t] = make_uint4(0u, 0u, 0u, 0u);
+                    __threadfence();
+                    atomicExch(&dsc.cn_ready[t], k);
+                }
+            }
+        } else {
+            r -= plan.n_cn;
+            int c = 0;
+            while (c < plan.n_cls - 1 && r >= plan.cls_chunks[c]) r -= plan.cls_chunks[c++];
+            if (threadIdx.x == 0) {
+                while (atomicAdd(&dsv.cn_ready[t], 0) != k) __nanosleep(64);
+                __threadfence();
+            }
+            __syncthreads();
+            const uint4 act = __ldcg(&dsv.tile_active[t]);
+            if (act.x | act.y | act.z | act.w) vn_dispatch<false, S>(cd, dsv, c, t, act, r, qmax2, nullptr);
+        }
+        __syncthreads();
+    }
+}
+
+// after a fused iteration: active / retire lists of the processed tiles, counters reset
+__global__ void __launch_bounds__(1024) k_list(DecState ds, int32_t *host_counts) {
+    __shared__ int s_warp[33];
+    __shared__ int s_lanes;
+    if (threadIdx.x == 0) s_lanes = 0;
+    __syncthreads();
+    int n_act = 0, n_ret = 0;
+    for (int t0 = 0; t0 < ds.tiles; t0 += blockDim.x) {
+        const int t = t0 + threadIdx.x;
+        uint4 rem = make_uint4(0u, 0u, 0u, 0u), newly = make_uint4(0u, 0u, 0u, 0u);
+        if (t < ds.tiles) {
+            if (ds.cn_done[t] > 0) {  // processed this iteration
+                rem = ds.tile_active[t];
+                newly = ds.tile_newly[t];
+                ds.cn_done[t] = 0;
+            } else {
+                ds.tile_newly[t] = make_uint4(0u, 0u, 0u, 0u);
+            }
+        }
+        const bool ra = (rem.x | rem.y | rem.z | rem.w) != 0u;
+        const bool rn = (newly.x | newly.y | newly.z | newly.w) != 0u;
+        int tot;
+        const int pa = block_scan_flag(ra, s_warp, &tot);
+        if (ra) ds.active_list[n_act + pa] = t;
+        n_act += tot;
+        const int pr = block_scan_flag(rn, s_warp, &tot);
+        if (rn) ds.retire_list[n_ret + pr] = t;
+        n_ret += tot;
+        int v = __popc(rem.x) + __popc(rem.y) + __popc(rem.z) + __popc(rem.w);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_lanes, v);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ds.counts[0] = n_act;
+        ds.counts[1] = n_ret;
+        ds.counts[2] = s_lanes;
+        *ds.fused_work = 0;
         if (host_counts) {
             volatile int32_t *h = host_counts;
             h[0] = n_act;
@@ -575,6 +741,11 @@ __global__ void k_init_tiles(DecState ds, const uint8_t *__restrict__ alive) {
     ds.tile_unsat[t] = make_uint4(0u, 0u, 0u, 0u);
     ds.tile_newly[t] = make_uint4(0u, 0u, 0u, 0u);
     ds.active_list[t] = t;
+    if (ds.cn_done) {
+        ds.cn_done[t] = 0;
+        ds.cn_ready[t] = -1;
+        if (t == 0) *ds.fused_work = 0;
+    }
 }
 
 __global__ void k_set_counts(DecState ds, int32_t n_active) {
@@ -662,6 +833,61 @@ int launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax,
                                    : launch_vn_t<false, 2>(cd, ds, grid_tiles, q2, post_dbg, s);
     return first ? launch_vn_t<true, 1>(cd, ds, grid_tiles, q2, post_dbg, s)
                  : launch_vn_t<false, 1>(cd, ds, grid_tiles, q2, post_dbg, s);
+}
+
+FusedPlan make_plan(const CodeDev &cd, int subs) {
+    FusedPlan p{};
+    p.n_cn = (cd.M + WARPS_PER_BLOCK * CPW - 1) / (WARPS_PER_BLOCK * CPW);
+    p.n_cls = cd.n_vclass;
+    p.items_per_tile = p.n_cn;
+    for (int c = 0; c < cd.n_vclass; ++c) {
+        const int d = cd.vc_deg[c];
+        const int vpw = (d >= 1 && d <= 8) ? vpw_for(d, subs) : 1;
+        p.cls_chunks[c] = (cd.vc_cnt[c] + WARPS_PER_BLOCK * vpw - 1) / (WARPS_PER_BLOCK * vpw);
+        p.items_per_tile += p.cls_chunks[c];
+    }
+    return p;
+}
+
+template <int DCT, int S>
+static void launch_iter_t(const CodeDev &cd, const DecState &dsc, const DecState &dsv, const FusedPlan &plan, int k,
+                          float q2, cudaStream_t s) {
+    static int grid = 0;
+    if (!grid) {
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iter<DCT, S>, BLOCK, 0);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+    }
+    k_iter<DCT, S><<<grid, BLOCK, 0, s>>>(cd, dsc, dsv, plan, k, q2);
+}
+
+template <int S>
+static void launch_iter_s(const CodeDev &cd, const DecState &dsc, const DecState &dsv, const FusedPlan &plan, int k,
+                          float q2, cudaStream_t s) {
+    switch (cd.max_dc) {
+        case 1: case 2: launch_iter_t<2, S>(cd, dsc, dsv, plan, k, q2, s); break;
+        case 3: launch_iter_t<3, S>(cd, dsc, dsv, plan, k, q2, s); break;
+        case 4: launch_iter_t<4, S>(cd, dsc, dsv, plan, k, q2, s); break;
+        case 5: launch_iter_t<5, S>(cd, dsc, dsv, plan, k, q2, s); break;
+        case 6: launch_iter_t<6, S>(cd, dsc, dsv, plan, k, q2, s); break;
+        case 7: launch_iter_t<7, S>(cd, dsc, dsv, plan, k, q2, s); break;
+        case 8: launch_iter_t<8, S>(cd, dsc, dsv, plan, k, q2, s); break;
+        default: launch_iter_t<0, S>(cd, dsc, dsv, plan, k, q2, s); break;
+    }
+}
+
+void launch_iter(const CodeDev &cd, const DecState &dsc, const DecState &dsv, const FusedPlan &plan, int k,
+                 float qmax, cudaStream_t s) {
+    const float q2 = qmax * LOG2E;
+    if (dsc.subs == 4) launch_iter_s<4>(cd, dsc, dsv, plan, k, q2, s);
+    else if (dsc.subs == 2) launch_iter_s<2>(cd, dsc, dsv, plan, k, q2, s);
+    else launch_iter_s<1>(cd, dsc, dsv, plan, k, q2, s);
+}
+
+void launch_list(const DecState &ds, int32_t *host_counts, cudaStream_t s) {
+    k_list<<<1, 1024, 0, s>>>(ds, host_counts);
 }
 
 void launch_status(const DecState &ds, int k, int max_iter, int final_pass, int32_t *host_counts, cudaStream_t s) {

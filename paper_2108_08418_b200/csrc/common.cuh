@@ -65,6 +65,19 @@ struct DecState {
     int32_t *counts;        // [4]: n_active, n_retire, total active lanes, pad
     int32_t *iters;         // [frames] D of the current decode
     uint8_t *conv;          // [frames]
+    // fused-iteration scheduler (k_iter): second hard-decision buffer, work counter, per-tile sync
+    uint4 *hb2;             // [tiles][n]
+    int32_t *fused_work;    // [1]
+    int32_t *cn_done;       // [tiles] CN chunks finished this iteration
+    int32_t *cn_ready;      // [tiles] iteration whose CN + status of the tile completed
+};
+
+// work items of one fused iteration per tile: CN chunks then per-class VN chunks
+struct FusedPlan {
+    int32_t n_cn;
+    int32_t n_cls;
+    int32_t cls_chunks[MAX_VCLASS];
+    int32_t items_per_tile;
 };
 
 // Conditional-LLR parameters for the reconcile LLR kernel.

@@ -8,6 +8,10 @@ namespace cvsr {
 void launch_cn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, int check_only, cudaStream_t s);
 int launch_vn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, float *post_dbg,
               cudaStream_t s);
+FusedPlan make_plan(const CodeDev &cd, int subs);
+void launch_iter(const CodeDev &cd, const DecState &dsc, const DecState &dsv, const FusedPlan &plan, int k,
+                 float qmax, cudaStream_t s);
+void launch_list(const DecState &ds, int32_t *host_counts, cudaStream_t s);
 void launch_status(const DecState &ds, int k, int max_iter, int final_pass, int32_t *host_counts, cudaStream_t s);
 void launch_retire(const DecState &ds, int32_t n, int grid_tiles, uint32_t *bits_out, cudaStream_t s);
 void launch_to_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, int subs, float scale,
