@@ -159,8 +159,13 @@ bool fused_enabled() {
 // message lines (E x 128 S bytes) stay well inside L2 for the CN -> VN hand-off
 int pick_subs(int32_t frames, int64_t E) {
     int s = choose_subs(frames);
+    static double cap = -1.0;
+    if (cap < 0.0) {
+        const char *e = getenv("CVSR_FUSED_MB");  // experiment switch: per-tile L2 budget (MB)
+        cap = e ? atof(e) : 40.0;
+    }
     if (fused_enabled())
-        while (s > 1 && (double)E * LANES * s * 4 > 64.0e6) s >>= 1;
+        while (s > 1 && (double)E * LANES * s * 4 > cap * 1.0e6) s >>= 1;
     return s;
 }
 

@@ -508,22 +508,43 @@ __device__ __forceinline__ void vn_dispatch(const CodeDev &cd, const DecState &d
 }
 
 template <int DCT, int S>
-__global__ void __launch_bounds__(BLOCK, 2) k_iter(CodeDev cd, DecState dsc, DecState dsv, FusedPlan plan, int k,
+__global__ void __launch_bounds__(BLOCK, 3) k_iter(CodeDev cd, DecState dsc, DecState dsv, FusedPlan plan, int k,
                                                    float qmax2) {
     __shared__ int s_item, s_last;
     __shared__ uint32_t s_unsat[SUBS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_items = dsc.counts[0] * plan.items_per_tile;
+    const int n_act = dsc.counts[0];
+    const int n_cn = plan.n_cn, n_vn = plan.items_per_tile - plan.n_cn;
+    const int n_items = n_act * plan.items_per_tile;
     for (;;) {
         if (threadIdx.x == 0) s_item = atomicAdd(dsc.fused_work, 1);
         if (threadIdx.x < SUBS) s_unsat[threadIdx.x] = 0u;
         __syncthreads();
         const int item = s_item;
         if (item >= n_items) break;
-        const int ti = item / plan.items_per_tile;
-        int r = item - ti * plan.items_per_tile;
+        // phase 0: CN(t_0); phase j in [1, n_act): CN(t_j) then VN(t_{j-1}); phase n_act: VN(t_{n_act-1}).
+        // A tile's VN items come one CN phase after its CN items, so they rarely wait.
+        int ti, r;
+        bool is_cn;
+        if (item < n_cn) {
+            ti = 0;
+            r = item;
+            is_cn = true;
+        } else {
+            const int i2 = item - n_cn;
+            const int j = i2 / (n_cn + n_vn) + 1;
+            r = i2 - (j - 1) * (n_cn + n_vn);
+            if (j < n_act && r < n_cn) {
+                ti = j;
+                is_cn = true;
+            } else {
+                ti = j - 1;
+                r = (j < n_act) ? r - n_cn : r;
+                is_cn = false;
+            }
+        }
         const int t = dsc.active_list[ti];
-        if (r < plan.n_cn) {
+        if (is_cn) {
             const uint4 act = __ldcg(&dsc.tile_active[t]);
             const int c0 = (r * WARPS_PER_BLOCK + warp) * CPW;
             const int nc = min(CPW, cd.M - c0);
@@ -566,7 +587,6 @@ __global__ void __launch_bounds__(BLOCK, 2) k_iter(CodeDev cd, DecState dsc, Dec
                 }
             }
         } else {
-            r -= plan.n_cn;
             int c = 0;
             while (c < plan.n_cls - 1 && r >= plan.cls_chunks[c]) r -= plan.cls_chunks[c++];
             if (threadIdx.x == 0) {
