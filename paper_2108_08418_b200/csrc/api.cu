@@ -145,12 +145,16 @@ cvsr_status scratch_reserve(cvsr_ctx *ctx, size_t bytes, char **out) {
     return CVSR_OK;
 }
 
-// fused iteration scheduler (k_iter) on/off: CVSR_FUSED=0 selects the kernel-per-pass path
+// Experimental fused iteration scheduler (k_iter), opt-in with CVSR_FUSED=1.  Measured
+// on B200 for C2 it is slower than the per-pass kernels (170 ms vs 105 ms per step:
+// the C2V lines do not survive in L2 between a tile's CN and VN phases, DRAM traffic
+// per iteration rose from 7.8 to 10 GB, and the persistent grid runs at 24 warps/SM
+// with per-item barriers), so the default is the per-pass path.
 bool fused_enabled() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("CVSR_FUSED");
-        v = (e && e[0] == '0') ? 0 : 1;
+        v = (e && e[0] == '1') ? 1 : 0;
     }
     return v == 1;
 }

@@ -401,3 +401,16 @@ def test_session_host_and_device_match_pipeline(cv, ctx):
     for h in hs:
         if h:
             cv.cvsr_code_free(h)
+
+
+def test_fused_scheduler_subprocess():
+    """The experimental fused iteration scheduler (CVSR_FUSED=1) passes the smoke parity check."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CVSR_FUSED="1")
+    res = subprocess.run([sys.executable, "-c", "import __graft_entry__ as g; g.smoke()"], cwd=root, env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    assert "smoke OK" in res.stdout
