@@ -221,7 +221,10 @@ cvsr_status cvsr_session_run(cvsr_session *s, const float *x, const float *y, cv
 /* x_host, y_host: HOST float[frames][n] (pinned for overlap); copies them in,
  * runs the step and copies Alice's labels (label_host uint8[frames][n],
  * nullable), frame_ok_host uint8[frames] and iters_host int32[frames][m]
- * (nullable) back; synchronises.  This is the end-to-end entry point. */
+ * (nullable) back; synchronises.  This is the end-to-end entry point.  For
+ * batches of >= 512 frames the work is split into 4 frame chunks so that the
+ * next chunk's host-to-device copy and the previous chunk's device-to-host
+ * copy overlap the current chunk's kernels; results do not depend on it. */
 cvsr_status cvsr_session_run_host(cvsr_session *s, const float *x_host, const float *y_host, uint8_t *label_host,
                                   uint8_t *frame_ok_host, int32_t *iters_host, cvsr_stats *stats_out);
 /* device pointers of the session's result buffers (any output may be NULL) */

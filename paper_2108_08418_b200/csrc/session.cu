@@ -18,6 +18,8 @@ struct cvsr_session {
     float sigma_n = 0.0f;
     cvsr_decode_opts opts{};
     void *mem = nullptr;
+    cudaStream_t copy = nullptr;       // H2D / D2H stream of run_host
+    cudaEvent_t ev_in[8] = {}, ev_out[8] = {};
     float *x = nullptr, *y = nullptr;
     uint8_t *label_bob = nullptr, *label_alice = nullptr, *frame_ok = nullptr;
     int32_t *iters = nullptr;
@@ -87,41 +89,94 @@ cvsr_status cvsr_session_create(cvsr_ctx *ctx, int32_t m, const cvsr_code *const
     s->iters = reinterpret_cast<int32_t *>(take((size_t)frames * m * 4));
     for (int j = 0; j < m; ++j)
         s->synd[j] = reinterpret_cast<uint32_t *>(take((size_t)frames * cvsr::words_of(codes[j] ? s->n_checks[j] : n) * 4));
+    if (cudaStreamCreateWithFlags(&s->copy, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaFree(s->mem);
+        delete s;
+        return CVSR_ECUDA;
+    }
+    for (int i = 0; i < 8; ++i) {
+        cudaEventCreateWithFlags(&s->ev_in[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&s->ev_out[i], cudaEventDisableTiming);
+    }
     *out = s;
     return CVSR_OK;
 }
 
-cvsr_status cvsr_session_run(cvsr_session *s, const float *x, const float *y, cvsr_stats *stats_out) {
-    if (!s || !x || !y) return CVSR_EINVAL;
-    if (cvsr_status st = cvsr_quantise(s->ctx, &s->q, y, (int64_t)s->frames * s->n, s->label_bob)) return st;
-    for (int j = 0; j < s->m; ++j) {
-        cvsr_status st = s->codes[j] ? cvsr_syndrome(s->ctx, s->codes[j], s->label_bob, s->frames, j, s->synd[j])
-                                     : cvsr_slice_bits(s->ctx, s->label_bob, s->frames, s->n, j, s->synd[j]);
-        if (st) return st;
-    }
+// Bob + Alice for frames [f0, f0 + nf) of the session's buffers
+static cvsr_status run_range(cvsr_session *s, const float *x, const float *y, int32_t f0, int32_t nf,
+                             cvsr_stats *stats_out) {
+    const size_t off = (size_t)f0 * s->n;
+    if (cvsr_status st = cvsr_quantise(s->ctx, &s->q, y + off, (int64_t)nf * s->n, s->label_bob + off)) return st;
     const uint32_t *sy[8];
-    for (int j = 0; j < s->m; ++j) sy[j] = s->synd[j];
-    return cvsr_reconcile(s->ctx, s->m, s->codes, s->order, &s->q, s->sigma_n, x, sy, s->frames, s->n, &s->opts,
-                          s->label_alice, s->frame_ok, s->iters, stats_out);
+    for (int j = 0; j < s->m; ++j) {
+        const int32_t W = cvsr::words_of(s->codes[j] ? s->n_checks[j] : s->n);
+        uint32_t *dst = s->synd[j] + (size_t)f0 * W;
+        cvsr_status st = s->codes[j] ? cvsr_syndrome(s->ctx, s->codes[j], s->label_bob + off, nf, j, dst)
+                                     : cvsr_slice_bits(s->ctx, s->label_bob + off, nf, s->n, j, dst);
+        if (st) return st;
+        sy[j] = dst;
+    }
+    return cvsr_reconcile(s->ctx, s->m, s->codes, s->order, &s->q, s->sigma_n, x + off, sy, nf, s->n, &s->opts,
+                          s->label_alice + off, s->frame_ok + f0, s->iters + (size_t)f0 * s->m, stats_out);
 }
 
+cvsr_status cvsr_session_run(cvsr_session *s, const float *x, const float *y, cvsr_stats *stats_out) {
+    if (!s || !x || !y) return CVSR_EINVAL;
+    return run_range(s, x, y, 0, s->frames, stats_out);
+}
+
+// The batch is processed in up to 4 frame chunks: chunk c+1's inputs are copied in
+// (copy stream) while chunk c is reconciled (context stream), and chunk c's results
+// are copied out while chunk c+1 runs.  Per-frame results do not depend on the
+// chunking.  stats_out (if requested) is accumulated over the chunks.
 cvsr_status cvsr_session_run_host(cvsr_session *s, const float *x_host, const float *y_host, uint8_t *label_host,
                                   uint8_t *frame_ok_host, int32_t *iters_host, cvsr_stats *stats_out) {
     if (!s || !x_host || !y_host || !frame_ok_host) return CVSR_EINVAL;
     cudaStream_t st = cvsr_internal_ctx_stream(s->ctx);
-    const size_t xb = (size_t)s->frames * s->n * 4;
-    if (cudaMemcpyAsync(s->x, x_host, xb, cudaMemcpyHostToDevice, st) != cudaSuccess) return CVSR_ECUDA;
-    if (cudaMemcpyAsync(s->y, y_host, xb, cudaMemcpyHostToDevice, st) != cudaSuccess) return CVSR_ECUDA;
-    if (cvsr_status r = cvsr_session_run(s, s->x, s->y, stats_out)) return r;
-    if (label_host &&
-        cudaMemcpyAsync(label_host, s->label_alice, (size_t)s->frames * s->n, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-        return CVSR_ECUDA;
-    if (cudaMemcpyAsync(frame_ok_host, s->frame_ok, s->frames, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-        return CVSR_ECUDA;
-    if (iters_host && cudaMemcpyAsync(iters_host, s->iters, (size_t)s->frames * s->m * 4, cudaMemcpyDeviceToHost,
-                                      st) != cudaSuccess)
-        return CVSR_ECUDA;
+    cudaStream_t cs = s->copy;
+    const int chunks = s->frames >= 4 * 128 ? 4 : 1;
+    int32_t b[9];
+    for (int c = 0; c <= chunks; ++c) b[c] = (int32_t)((int64_t)s->frames * c / chunks);
+    if (stats_out) memset(stats_out, 0, sizeof(*stats_out));
+    // inputs must not be overwritten while the previous call's work still reads them
     if (cudaStreamSynchronize(st) != cudaSuccess) return CVSR_ECUDA;
+    auto h2d = [&](int c) -> bool {
+        const size_t off = (size_t)b[c] * s->n, bytes = (size_t)(b[c + 1] - b[c]) * s->n * 4;
+        return cudaMemcpyAsync(s->x + off, x_host + off, bytes, cudaMemcpyHostToDevice, cs) == cudaSuccess &&
+               cudaMemcpyAsync(s->y + off, y_host + off, bytes, cudaMemcpyHostToDevice, cs) == cudaSuccess &&
+               cudaEventRecord(s->ev_in[c], cs) == cudaSuccess;
+    };
+    if (!h2d(0)) return CVSR_ECUDA;
+    for (int c = 0; c < chunks; ++c) {
+        if (c + 1 < chunks && !h2d(c + 1)) return CVSR_ECUDA;
+        if (cudaStreamWaitEvent(st, s->ev_in[c], 0) != cudaSuccess) return CVSR_ECUDA;
+        cvsr_stats cst;
+        if (cvsr_status r = run_range(s, s->x, s->y, b[c], b[c + 1] - b[c], stats_out ? &cst : nullptr)) return r;
+        if (stats_out) {
+            stats_out->frames += cst.frames;
+            stats_out->frames_ok += cst.frames_ok;
+            stats_out->bits_reconciled += cst.bits_reconciled;
+            for (int j = 0; j < 8; ++j) {
+                stats_out->attempted[j] += cst.attempted[j];
+                stats_out->converged[j] += cst.converged[j];
+                stats_out->iters_sum[j] += cst.iters_sum[j];
+                stats_out->edge_iters[j] += cst.edge_iters[j];
+            }
+            stats_out->alice_seconds += cst.alice_seconds;
+        }
+        if (cudaEventRecord(s->ev_out[c], st) != cudaSuccess || cudaStreamWaitEvent(cs, s->ev_out[c], 0) != cudaSuccess)
+            return CVSR_ECUDA;
+        const int32_t f0 = b[c], nf = b[c + 1] - b[c];
+        if (label_host && cudaMemcpyAsync(label_host + (size_t)f0 * s->n, s->label_alice + (size_t)f0 * s->n,
+                                          (size_t)nf * s->n, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+            return CVSR_ECUDA;
+        if (cudaMemcpyAsync(frame_ok_host + f0, s->frame_ok + f0, nf, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+            return CVSR_ECUDA;
+        if (iters_host && cudaMemcpyAsync(iters_host + (size_t)f0 * s->m, s->iters + (size_t)f0 * s->m,
+                                          (size_t)nf * s->m * 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+            return CVSR_ECUDA;
+    }
+    if (cudaStreamSynchronize(cs) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) return CVSR_ECUDA;
     return CVSR_OK;
 }
 
@@ -138,6 +193,14 @@ cvsr_status cvsr_session_buffers(const cvsr_session *s, uint8_t **label_bob, uin
 void cvsr_session_destroy(cvsr_session *s) {
     if (!s) return;
     cvsr_ctx_sync(s->ctx);
+    if (s->copy) {
+        cudaStreamSynchronize(s->copy);
+        cudaStreamDestroy(s->copy);
+    }
+    for (int i = 0; i < 8; ++i) {
+        if (s->ev_in[i]) cudaEventDestroy(s->ev_in[i]);
+        if (s->ev_out[i]) cudaEventDestroy(s->ev_out[i]);
+    }
     cudaFree(s->mem);
     delete s;
 }

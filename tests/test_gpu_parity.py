@@ -376,9 +376,11 @@ def test_reconcile_parity_other_configs(cv, ctx, name, n, frames):
     assert np.sum(g["ok"] != ok_ref) <= max(1, frames // 20)
 
 
-def test_session_host_and_device_match_pipeline(cv, ctx):
-    """cvsr_session_run / cvsr_session_run_host reproduce the composed pipeline exactly."""
-    cfg = configs.scaled(configs.C2, 4096, 40)
+@pytest.mark.parametrize("n,frames", [(4096, 40), (2048, 520)])
+def test_session_host_and_device_match_pipeline(cv, ctx, n, frames):
+    """cvsr_session_run / cvsr_session_run_host (chunked when frames >= 512) reproduce the
+    composed pipeline exactly."""
+    cfg = configs.scaled(configs.C2, n, frames)
     codes_l = cfg.build_codes()
     x, y = awgn.quadratures(cfg.frames, cfg.n, cfg.gamma, seed=41)
     g = _run_reconcile(cv, cfg, codes_l, x, y, cfg.frames, cfg.n, cfg.max_iter)
