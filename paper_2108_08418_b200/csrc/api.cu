@@ -175,6 +175,44 @@ int pick_subs(int32_t frames, int64_t E) {
 
 int tiles_for(int32_t frames, int subs) { return (frames + LANES * subs - 1) / (LANES * subs); }
 
+// frame compaction (second arena) on/off: CVSR_COMPACT=0 disables
+bool compact_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("CVSR_COMPACT");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1 && !fused_enabled();
+}
+
+// second arena for frame compaction (see bp_kernels.cu "frame compaction")
+struct CompactArena {
+    float *msg = nullptr, *L = nullptr;
+    uint4 *hb = nullptr, *st = nullptr;
+    int32_t *slot_frame[2] = {nullptr, nullptr};
+    int32_t *dst_src = nullptr;
+};
+
+size_t compact_bytes(int tiles, int subs, int64_t n, int64_t M, int64_t E) {
+    const size_t T = (size_t)LANES * subs;
+    return align_up((size_t)tiles * E * T * 4) + align_up((size_t)tiles * n * T * 4) +
+           align_up((size_t)tiles * n * sizeof(uint4)) + align_up((size_t)tiles * M * sizeof(uint4)) +
+           3 * align_up((size_t)tiles * T * sizeof(int32_t));
+}
+
+CompactArena carve_compact(Carve &cv, int tiles, int subs, int64_t n, int64_t M, int64_t E) {
+    const size_t T = (size_t)LANES * subs;
+    CompactArena c;
+    c.msg = cv.take<float>((size_t)tiles * E * T * 4);
+    c.L = cv.take<float>((size_t)tiles * n * T * 4);
+    c.hb = cv.take<uint4>((size_t)tiles * n * sizeof(uint4));
+    c.st = cv.take<uint4>((size_t)tiles * M * sizeof(uint4));
+    c.slot_frame[0] = cv.take<int32_t>((size_t)tiles * T * sizeof(int32_t));
+    c.slot_frame[1] = cv.take<int32_t>((size_t)tiles * T * sizeof(int32_t));
+    c.dst_src = cv.take<int32_t>((size_t)tiles * T * sizeof(int32_t));
+    return c;
+}
+
 size_t decstate_bytes(int tiles, int frames, int subs, int64_t n, int64_t M, int64_t E) {
     const size_t T = (size_t)LANES * subs;
     size_t b = 0;
@@ -224,7 +262,7 @@ DecState carve_decstate(Carve &cv, int tiles, int frames, int subs, int64_t n, i
 // are launched LOOKAHEAD ahead of a mapped-memory progress counter written by
 // the status kernel; the counter also bounds the grid's tile dimension.
 cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0, int max_iter, float qmax,
-                       uint32_t *bits_out) {
+                       uint32_t *bits_out, const CompactArena *ca = nullptr) {
     cudaStream_t s = ctx->stream;
     const CodeDev &cd = code->d;
     volatile int32_t *hc = ctx->host_counts;
@@ -234,6 +272,10 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
     const FusedPlan plan = fused ? make_plan(cd, ds0.subs) : FusedPlan{};
     uint4 *hbuf[2] = {ds0.hb, ds0.hb2};
     DecState ds = ds0;
+    ds.slot_frame = nullptr;
+    // compaction arenas: index 0 = ds0's buffers, 1 = ca's; slot_frame alternates between ca's two maps
+    int arena = 0, n_compact = 0;
+    const int T = ds0.tile_frames;
     prof_begin(ctx, KC_INIT);
     int launched = launch_vn(cd, ds, ds.tiles, qmax, true, nullptr, s);  // decision 0 -> hbuf[0]
     prof_end(ctx);
@@ -276,6 +318,31 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
             const int32_t lanes = hc[2];
             if (lanes == 0) break;
             bound = std::min(bound, std::max(na, 1));
+            // compaction: the active frames fill at most half of the active tiles (counts of
+            // iteration k - LOOKAHEAD + 1 are upper bounds of the current ones)
+            if (ca && k < max_iter && na >= 2 && (int64_t)lanes * 2 <= (int64_t)na * T) {
+                DecState dst = ds;
+                if (arena == 0) {
+                    dst.msg = ca->msg;
+                    dst.L = ca->L;
+                    dst.hb = ca->hb;
+                    dst.st = ca->st;
+                } else {
+                    dst.msg = ds0.msg;
+                    dst.L = ds0.L;
+                    dst.hb = ds0.hb;
+                    dst.st = ds0.st;
+                }
+                dst.slot_frame = ca->slot_frame[n_compact & 1];
+                prof_begin(ctx, KC_CTRL);
+                launched += launch_compact(cd, ds, dst, ca->dst_src, std::max(1, (lanes + T - 1) / T),
+                                           ctx->host_counts_dev, s);
+                prof_end(ctx);
+                ds = dst;
+                arena ^= 1;
+                ++n_compact;
+                bound = std::max(1, (lanes + T - 1) / T);
+            }
         }
     }
     return check_launch(ctx, launched);
@@ -682,17 +749,23 @@ cvsr_status cvsr_decode(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, 
     const CodeDev &cd = code->d;
     const int subs = pick_subs(frames, cd.E);
     const int tiles = tiles_for(frames, subs);
+    const bool comp = compact_enabled() && tiles >= 2;
     char *base;
-    if (cvsr_status st = scratch_reserve(ctx, decstate_bytes(tiles, frames, subs, cd.n, cd.M, cd.E), &base)) return st;
+    if (cvsr_status st = scratch_reserve(ctx, decstate_bytes(tiles, frames, subs, cd.n, cd.M, cd.E) +
+                                                  (comp ? compact_bytes(tiles, subs, cd.n, cd.M, cd.E) : 0),
+                                         &base))
+        return st;
     Carve cv{base};
     DecState ds = carve_decstate(cv, tiles, frames, subs, cd.n, cd.M, cd.E, iters_out, converged_out);
+    CompactArena ca;
+    if (comp) ca = carve_compact(cv, tiles, subs, cd.n, cd.M, cd.E);
     cudaStream_t s = ctx->stream;
     launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, ds.subs, LOG2E, s);
     launch_synd_transpose(synd, frames, cd.M, ds.subs, ds.st, tiles, s);
     launch_init_tiles(ds, nullptr, s);
     launch_set_counts(ds, tiles, s);
     if (cvsr_status st = check_launch(ctx, 4)) return st;
-    return run_decode(ctx, code, ds, opts->max_iter, opts->msg_clamp, bits_out);
+    return run_decode(ctx, code, ds, opts->max_iter, opts->msg_clamp, bits_out, comp ? &ca : nullptr);
 }
 
 cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, const uint32_t *synd,
@@ -773,13 +846,17 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
     DeviceGuard g(ctx->device);
     const int subs = pick_subs(frames, maxE);
     const int tiles = tiles_for(frames, subs);
+    const bool comp = compact_enabled() && tiles >= 2;
     const int Wn = words_of(n);
     size_t bytes = decstate_bytes(tiles, frames, subs, n, maxM, maxE);
+    if (comp) bytes += compact_bytes(tiles, subs, n, maxM, maxE);
     bytes += (size_t)m * align_up((size_t)frames * Wn * 4) + 3 * align_up((size_t)frames);
     char *base;
     if (cvsr_status st = scratch_reserve(ctx, bytes, &base)) return st;
     Carve cv{base};
     DecState ds = carve_decstate(cv, tiles, frames, subs, n, maxM, maxE, nullptr, nullptr);
+    CompactArena ca;
+    if (comp) ca = carve_compact(cv, tiles, subs, n, maxM, maxE);
     uint32_t *bits_dec[8] = {};
     for (int j = 0; j < m; ++j) bits_dec[j] = cv.take<uint32_t>((size_t)frames * Wn * 4);
     uint8_t *alive = cv.take<uint8_t>((size_t)frames);
@@ -813,7 +890,8 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
             prof_end(ctx);
             launched += 4;
             if (cvsr_status st = check_launch(ctx, 0)) return st;
-            if (cvsr_status st = run_decode(ctx, codes[j], ds, opts->max_iter, opts->msg_clamp, bits_dec[j]))
+            if (cvsr_status st = run_decode(ctx, codes[j], ds, opts->max_iter, opts->msg_clamp, bits_dec[j],
+                                            comp ? &ca : nullptr))
                 return st;
             launch_slice_done(ds, m, j, 0, alive, attempt, iters, s);
             ++launched;

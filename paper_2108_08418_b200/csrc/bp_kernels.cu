@@ -409,7 +409,8 @@ __device__ __forceinline__ void mark_frames(const DecState &ds, int t, int s, ui
     while (bits) {
         const int l = __ffs(bits) - 1;
         bits &= bits - 1;
-        const int f = t * ds.tile_frames + s * LANES + l;
+        const int slot = t * ds.tile_frames + s * LANES + l;
+        const int f = ds.slot_frame ? ds.slot_frame[slot] : slot;
         ds.iters[f] = it;
         ds.conv[f] = cv;
     }
@@ -672,8 +673,9 @@ __global__ void __launch_bounds__(BLOCK) k_retire(DecState ds, int32_t n, uint32
             const uint32_t b = __ballot_sync(FULL, (ws >> f) & 1u);
             if (lane == f) mine = b;
         }
-        const int frame = t * ds.tile_frames + s * LANES + lane;
-        if (((ns >> lane) & 1u) && frame < ds.frames) bits_out[(size_t)frame * Wn + w] = mine;
+        const int slot = t * ds.tile_frames + s * LANES + lane;
+        const int frame = ds.slot_frame ? ds.slot_frame[slot] : slot;
+        if (((ns >> lane) & 1u) && frame >= 0 && frame < ds.frames) bits_out[(size_t)frame * Wn + w] = mine;
     }
 }
 
@@ -774,6 +776,116 @@ __global__ void k_set_counts(DecState ds, int32_t n_active) {
         ds.counts[1] = 0;
         ds.counts[2] = 0;
     }
+}
+
+// ------------------------------------------------------------------ frame compaction
+//
+// When most frames of the active tiles have converged, the still-active frames
+// are moved densely into a second arena (same layout), so the remaining
+// iterations touch fewer tiles and sectors.  All active frames are at the same
+// iteration (flooding), so a move carries only their state: messages, LLRs,
+// syndrome bits and current hard decisions; slot_frame keeps the frame ids.
+
+// Single block: rank the active slots of the source tiles (in slot order) and
+// set up the destination tiles: dst_src[r] = source slot of destination slot r.
+__global__ void __launch_bounds__(1024) k_compact_plan(DecState src, DecState dst, int32_t *dst_src,
+                                                       int32_t *host_counts) {
+    __shared__ int s_warp[33];
+    const int T = src.tile_frames;
+    const int n_act_tiles = src.counts[0];
+    int base = 0;
+    for (int i0 = 0; i0 < n_act_tiles * T; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        bool a = false;
+        int slot = 0;
+        if (i < n_act_tiles * T) {
+            const int t = src.active_list[i / T];
+            const int r = i % T;
+            slot = t * T + r;
+            a = (cmpu(src.tile_active[t], r / LANES) >> (r % LANES)) & 1u;
+        }
+        int tot;
+        const int rk = block_scan_flag(a, s_warp, &tot);
+        if (a) {
+            dst_src[base + rk] = slot;
+            dst.slot_frame[base + rk] = src.slot_frame ? src.slot_frame[slot] : slot;
+        }
+        base += tot;
+    }
+    __syncthreads();
+    const int A = base, tiles_new = (A + T - 1) / T;
+    for (int r = A + threadIdx.x; r < tiles_new * T; r += blockDim.x) {
+        dst_src[r] = -1;
+        dst.slot_frame[r] = -1;
+    }
+    for (int t = threadIdx.x; t < tiles_new; t += blockDim.x) {
+        uint32_t m[SUBS] = {0u, 0u, 0u, 0u};
+        for (int q = 0; q < src.subs; ++q) {
+            const int lo = t * T + q * LANES;
+            const int cnt = min(max(A - lo, 0), LANES);
+            m[q] = cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u);
+        }
+        dst.tile_active[t] = make_uint4(m[0], m[1], m[2], m[3]);
+        dst.tile_unsat[t] = make_uint4(0u, 0u, 0u, 0u);
+        dst.tile_newly[t] = make_uint4(0u, 0u, 0u, 0u);
+        dst.active_list[t] = t;
+    }
+    if (threadIdx.x == 0) {
+        dst.counts[0] = tiles_new;
+        dst.counts[1] = 0;
+        dst.counts[2] = A;
+        if (host_counts) {
+            volatile int32_t *h = host_counts;
+            h[0] = tiles_new;
+            h[1] = 0;
+            h[2] = A;
+        }
+    }
+}
+
+// dst[t'][row][lane][s] = src[slot dst_src(t', s, lane)] for float rows (messages, LLRs)
+template <int S>
+__global__ void __launch_bounds__(256) k_compact_rows(const float *__restrict__ src, float *__restrict__ dst,
+                                                      int64_t rows, const int32_t *__restrict__ dst_src,
+                                                      const int32_t *__restrict__ counts) {
+    const int t = blockIdx.y;
+    if (t >= counts[0]) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    FV<S> v;
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+        const int so = dst_src[t * LANES * S + q * LANES + lane];
+        v.c[q] = 0.0f;
+        if (so >= 0) {
+            const int st = so / (LANES * S), rem = so % (LANES * S);
+            v.c[q] = src[(((size_t)st * rows + r) * LANES + (rem % LANES)) * S + rem / LANES];
+        }
+    }
+    stv<S>(dst + (((size_t)t * rows + r) * LANES + lane) * S, v);
+}
+
+// dst[t'][row] bit (s, lane) = src bit of slot dst_src(t', s, lane) for uint4 bit rows (st, hb)
+__global__ void __launch_bounds__(256) k_compact_bits(const uint4 *__restrict__ src, uint4 *__restrict__ dst,
+                                                      int64_t rows, int subs, const int32_t *__restrict__ dst_src,
+                                                      const int32_t *__restrict__ counts) {
+    const int t = blockIdx.y;
+    if (t >= counts[0]) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    uint32_t w[SUBS] = {0u, 0u, 0u, 0u};
+    for (int q = 0; q < subs; ++q) {
+        const int so = dst_src[t * LANES * subs + q * LANES + lane];
+        uint32_t b = 0u;
+        if (so >= 0) {
+            const int st = so / (LANES * subs), rem = so % (LANES * subs);
+            b = (cmpu(src[(size_t)st * rows + r], rem / LANES) >> (rem % LANES)) & 1u;
+        }
+        w[q] = __ballot_sync(FULL, b);
+    }
+    if (lane == 0) dst[(size_t)t * rows + r] = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -944,6 +1056,27 @@ void launch_synd_transpose(const uint32_t *synd, int32_t F, int32_t M, int subs,
 
 void launch_init_tiles(const DecState &ds, const uint8_t *alive, cudaStream_t s) {
     k_init_tiles<<<(ds.tiles + 127) / 128, 128, 0, s>>>(ds, alive);
+}
+
+// move the active frames of `src` densely into `dst` (state after a VN pass); returns launches
+int launch_compact(const CodeDev &cd, const DecState &src, const DecState &dst, int32_t *dst_src, int max_tiles,
+                   int32_t *host_counts, cudaStream_t s) {
+    k_compact_plan<<<1, 1024, 0, s>>>(src, dst, dst_src, host_counts);
+    const dim3 gE((unsigned)((cd.E + 7) / 8), max_tiles), gN((unsigned)((cd.n + 7) / 8), max_tiles),
+        gM((unsigned)((cd.M + 7) / 8), max_tiles);
+    if (src.subs == 4) {
+        k_compact_rows<4><<<gE, 256, 0, s>>>(src.msg, dst.msg, cd.E, dst_src, dst.counts);
+        k_compact_rows<4><<<gN, 256, 0, s>>>(src.L, dst.L, cd.n, dst_src, dst.counts);
+    } else if (src.subs == 2) {
+        k_compact_rows<2><<<gE, 256, 0, s>>>(src.msg, dst.msg, cd.E, dst_src, dst.counts);
+        k_compact_rows<2><<<gN, 256, 0, s>>>(src.L, dst.L, cd.n, dst_src, dst.counts);
+    } else {
+        k_compact_rows<1><<<gE, 256, 0, s>>>(src.msg, dst.msg, cd.E, dst_src, dst.counts);
+        k_compact_rows<1><<<gN, 256, 0, s>>>(src.L, dst.L, cd.n, dst_src, dst.counts);
+    }
+    k_compact_bits<<<gM, 256, 0, s>>>(src.st, dst.st, cd.M, src.subs, dst_src, dst.counts);
+    k_compact_bits<<<gN, 256, 0, s>>>(src.hb, dst.hb, cd.n, src.subs, dst_src, dst.counts);
+    return 6;
 }
 
 void launch_set_counts(const DecState &ds, int32_t n_active, cudaStream_t s) {

@@ -70,6 +70,8 @@ struct DecState {
     int32_t *fused_work;    // [1]
     int32_t *cn_done;       // [tiles] CN chunks finished this iteration
     int32_t *cn_ready;      // [tiles] iteration whose CN + status of the tile completed
+    // frame compaction: frame id of each slot (slot = 32 S t + 32 s + lane), nullptr = identity
+    int32_t *slot_frame;
 };
 
 // work items of one fused iteration per tile: CN chunks then per-class VN chunks

@@ -416,3 +416,48 @@ def test_fused_scheduler_subprocess():
                          capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
     assert "smoke OK" in res.stdout
+
+
+def test_decode_many_frames_compaction_invariance(cv, ctx):
+    """600 frames (5 tiles): late iterations compact the active frames into fewer tiles;
+    per-frame results must equal decoding each 100-frame slice separately (1 tile, no
+    compaction) and, on oracle-converged frames, the oracle."""
+    code = codes.regular(1024, 3, 6, seed=1)
+    u, llr, synd = _channel(code, 600, 1.5, seed=21)
+    full = gpu_decode(cv, ctx, code, llr, synd)
+    for a in range(0, 600, 100):
+        part = gpu_decode(cv, ctx, code, llr[a:a + 100], synd[a:a + 100])
+        for x, y in zip(full, part):
+            assert np.array_equal(x[a:a + 100], y)
+    b_ref, c_ref, i_ref = oracle.bp_decode(code, llr[:200].astype(np.float64), synd[:200])
+    ok = c_ref.astype(bool)
+    assert np.array_equal(full[0][:200][ok], b_ref[ok])
+
+
+def test_compaction_switch_subprocess():
+    """CVSR_COMPACT=0 and =1 give bit-identical reconcile results (C2 structure, 520 frames)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prog = (
+        "import numpy as np, torch\n"
+        "from cvsr_inputs import awgn, configs\n"
+        "from paper_2108_08418_b200.pipeline import SRPipeline\n"
+        "cfg = configs.scaled(configs.C2, 2048, 520)\n"
+        "cl = cfg.build_codes()\n"
+        "x, y = awgn.quadratures(cfg.frames, cfg.n, cfg.gamma, seed=5)\n"
+        "p = SRPipeline(cfg.m, cfg.edges(), cl, cfg.order, cfg.sigma_n, cfg.n, cfg.frames, torch.device('cuda:0'))\n"
+        "p.step(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())\n"
+        "torch.cuda.synchronize()\n"
+        "np.save(__import__('sys').argv[1], np.concatenate([p.label_alice.cpu().numpy().ravel(),"
+        " p.iters.cpu().numpy().ravel().astype(np.uint8), p.frame_ok.cpu().numpy()]))\n")
+    import tempfile
+    outs = []
+    for flag in ("0", "1"):
+        f = tempfile.mktemp(suffix=".npy")
+        res = subprocess.run([sys.executable, "-c", prog, f], cwd=root, env=dict(os.environ, CVSR_COMPACT=flag),
+                             capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
