@@ -818,7 +818,8 @@ __global__ void __launch_bounds__(1024) k_compact_plan(DecState src, DecState ds
         dst_src[r] = -1;
         dst.slot_frame[r] = -1;
     }
-    for (int t = threadIdx.x; t < tiles_new; t += blockDim.x) {
+    // every tile of the arena gets fresh state: tiles past tiles_new become empty
+    for (int t = threadIdx.x; t < src.tiles; t += blockDim.x) {
         uint32_t m[SUBS] = {0u, 0u, 0u, 0u};
         for (int q = 0; q < src.subs; ++q) {
             const int lo = t * T + q * LANES;
@@ -828,7 +829,7 @@ __global__ void __launch_bounds__(1024) k_compact_plan(DecState src, DecState ds
         dst.tile_active[t] = make_uint4(m[0], m[1], m[2], m[3]);
         dst.tile_unsat[t] = make_uint4(0u, 0u, 0u, 0u);
         dst.tile_newly[t] = make_uint4(0u, 0u, 0u, 0u);
-        dst.active_list[t] = t;
+        if (t < tiles_new) dst.active_list[t] = t;
     }
     if (threadIdx.x == 0) {
         dst.counts[0] = tiles_new;
