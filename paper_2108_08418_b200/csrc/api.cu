@@ -296,7 +296,7 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
             prof_end(ctx);
             launched += 3;
         } else {
-            ds.hb = hbuf[fused ? ((k - 1) & 1) : 0];
+            if (fused) ds.hb = hbuf[(k - 1) & 1];  // (per-pass path: ds.hb follows compaction)
             prof_begin(ctx, KC_CN);
             launch_cn(cd, ds, bound, qmax, final_pass, s);
             prof_end(ctx);
