@@ -185,6 +185,16 @@ bool compact_enabled() {
     return v == 1 && !fused_enabled();
 }
 
+// compact when the active frames fill at most this fraction of the active tiles
+double compact_frac() {
+    static double v = -1.0;
+    if (v < 0.0) {
+        const char *e = getenv("CVSR_COMPACT_FRAC");  // tuning switch
+        v = e ? atof(e) : 0.65;
+    }
+    return v;
+}
+
 // second arena for frame compaction (see bp_kernels.cu "frame compaction")
 struct CompactArena {
     float *msg = nullptr, *L = nullptr;
@@ -320,7 +330,7 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
             bound = std::min(bound, std::max(na, 1));
             // compaction: the active frames fill at most half of the active tiles (counts of
             // iteration k - LOOKAHEAD + 1 are upper bounds of the current ones)
-            if (ca && k < max_iter && na >= 2 && (int64_t)lanes * 2 <= (int64_t)na * T) {
+            if (ca && k < max_iter && na >= 2 && (double)lanes <= compact_frac() * (double)na * T) {
                 DecState dst = ds;
                 if (arena == 0) {
                     dst.msg = ca->msg;
