@@ -163,6 +163,12 @@ bool fused_enabled() {
 // message lines (E x 128 S bytes) stay well inside L2 for the CN -> VN hand-off
 int pick_subs(int32_t frames, int64_t E) {
     int s = choose_subs(frames);
+    static int forced = -1;
+    if (forced < 0) {
+        const char *e = getenv("CVSR_SUBS");  // tuning switch: force 1, 2 or 4 frames per lane
+        forced = e ? atoi(e) : 0;
+    }
+    if (forced == 1 || forced == 2 || forced == 4) return std::min(forced, s == 4 ? 4 : std::max(s, forced));
     static double cap = -1.0;
     if (cap < 0.0) {
         const char *e = getenv("CVSR_FUSED_MB");  // experiment switch: per-tile L2 budget (MB)

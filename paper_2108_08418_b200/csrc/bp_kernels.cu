@@ -158,11 +158,13 @@ __device__ __forceinline__ uint4 cn_group(const CodeDev &cd, const DecState &ds,
 #pragma unroll
     for (int i = 0; i <= CPW; ++i) lo[i] = __shfl_sync(FULL, rp, i <= nc ? i : nc);
     const int ebeg = lo[0], eend = lo[nc];
-    // per-check parity accumulators, seeded with the syndrome bits s_c
-    uint4 par[CPW];
+    // this lane's syndrome bits (S per check) for the CN signs; the full syndrome words are
+    // re-read (cache hit) for the parity test after the message pass, keeping registers low
+    const uint4 *stt = ds.st + (size_t)t * cd.M + c0;
+    uint32_t sbits = 0u;
 #pragma unroll
     for (int i = 0; i < CPW; ++i)
-        par[i] = (i < nc) ? ds.st[(size_t)t * cd.M + c0 + i] : make_uint4(0u, 0u, 0u, 0u);
+        if (i < nc) sbits |= lane_act<S>(stt[i], lane) << (i * S);
     // hard-decision word of this lane's edge (first 32 edges), issued before the message pass
     const uint4 *hbt = ds.hb + (size_t)t * cd.n;
     int e = ebeg + lane;
@@ -176,13 +178,16 @@ __device__ __forceinline__ uint4 cn_group(const CodeDev &cd, const DecState &ds,
             if (i < nc) {
                 const int deg = lo[i + 1] - lo[i];
                 float *m = mt + (size_t)lo[i] * LANES * S;
-                const uint32_t sb = lane_act<S>(par[i], lane);
+                const uint32_t sb = (sbits >> (i * S)) & ((1u << S) - 1u);
                 if constexpr (DCT > 0) cn_check<DCT, S>(m, deg, sb, al, qmax2);  // DCT = max_dc >= deg
                 else cn_check_generic<S>(m, deg, sb, al, qmax2);
             }
         }
     }
     // syndrome test of decision k-1 (H xhat = s), chunks of 32 edges
+    uint4 par[CPW];
+#pragma unroll
+    for (int i = 0; i < CPW; ++i) par[i] = (i < nc) ? stt[i] : make_uint4(0u, 0u, 0u, 0u);
     for (int e0 = ebeg;;) {
 #pragma unroll
         for (int i = 0; i < CPW; ++i) {
@@ -210,7 +215,7 @@ __device__ __forceinline__ uint4 cn_group(const CodeDev &cd, const DecState &ds,
 }
 
 template <int DCT, int S>  // DCT = max check degree (templated body) or 0 = generic
-__global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 20) ? 4 : (DCT * S <= 32 ? 3 : 2))
+__global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 24) ? 4 : (DCT * S <= 32 ? 3 : 2))
     k_cn(CodeDev cd, DecState ds, float qmax2, int check_only) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
