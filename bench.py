@@ -175,10 +175,12 @@ def main():
     from paper_2108_08418_b200.pipeline import SRPipeline
 
     rank, world, local = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    # under torchrun (any world size) the statistics go through a real NCCL process group
+    distributed = "WORLD_SIZE" in os.environ
+    if distributed:
+        dist.init_process_group("nccl", device_id=device)
     cfg, codes_l = build_workload(args.config)
     F = args.frames or cfg.frames
     n = cfg.n
@@ -215,7 +217,7 @@ def main():
     bits_per_step = (st["frames_ok"] - undetected) * cfg.m * n
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -282,7 +284,7 @@ def main():
         {"bits": bits_per_step, "frames": st["frames"], "frames_ok": st["frames_ok"], "undetected": undetected},
         st["iters_sum"], st["edge_iters"], [t_ms, e2e["ms"] if e2e else 0.0], device)
     if rank != 0:
-        if world > 1:
+        if distributed:
             dist.destroy_process_group()
         pipe.close()
         return
@@ -375,7 +377,7 @@ def main():
     }
     print(json.dumps(line), flush=True)
     pipe.close()
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 
