@@ -384,8 +384,9 @@ cvsr_status check_quantiser(const cvsr_quantiser *q) {
 
 }  // namespace
 
-// internal accessor for session.cu (not part of the ABI)
+// internal accessors for session.cu (not part of the ABI)
 cudaStream_t cvsr_internal_ctx_stream(cvsr_ctx *ctx) { return ctx->stream; }
+cvsr_status cvsr_internal_fail(cvsr_status st, const char *msg) { return fail(st, "%s", msg); }
 
 // =================================================================== ABI
 

@@ -30,16 +30,18 @@ namespace {
 size_t al(size_t b) { return (b + 255) & ~size_t(255); }
 }  // namespace
 
-cudaStream_t cvsr_internal_ctx_stream(cvsr_ctx *ctx);  // api.cu
+cudaStream_t cvsr_internal_ctx_stream(cvsr_ctx *ctx);          // api.cu
+cvsr_status cvsr_internal_fail(cvsr_status st, const char *msg);  // api.cu (sets cvsr_last_error)
 
 extern "C" {
 
 cvsr_status cvsr_session_create(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *codes, const int32_t *order,
                                 const cvsr_quantiser *q, float sigma_n, int32_t n, int32_t frames,
                                 const cvsr_decode_opts *opts, cvsr_session **out) {
-    if (!ctx || !codes || !order || !q || !opts || !out) return CVSR_EINVAL;
+    if (!ctx || !codes || !order || !q || !opts || !out) return cvsr_internal_fail(CVSR_EINVAL, "null argument");
     *out = nullptr;
-    if (m < 1 || m > 8 || q->m != m || n <= 0 || frames <= 0) return CVSR_ESHAPE;
+    if (m < 1 || m > 8 || q->m != m || n <= 0 || frames <= 0)
+        return cvsr_internal_fail(CVSR_ESHAPE, "session: bad m / n / frames");
     cvsr_session *s = new cvsr_session();
     s->ctx = ctx;
     s->m = m;
@@ -61,7 +63,7 @@ cvsr_status cvsr_session_create(cvsr_ctx *ctx, int32_t m, const cvsr_code *const
             }
             if (nv != n) {
                 delete s;
-                return CVSR_ESHAPE;
+                return cvsr_internal_fail(CVSR_ESHAPE, "session: code length differs from n");
             }
         }
         s->n_checks[j] = nc;
@@ -73,7 +75,7 @@ cvsr_status cvsr_session_create(cvsr_ctx *ctx, int32_t m, const cvsr_code *const
     if (cudaMalloc(&s->mem, bytes) != cudaSuccess) {
         cudaGetLastError();
         delete s;
-        return CVSR_ENOMEM;
+        return cvsr_internal_fail(CVSR_ENOMEM, "session buffers");
     }
     char *p = static_cast<char *>(s->mem);
     auto take = [&](size_t b) {
@@ -92,7 +94,7 @@ cvsr_status cvsr_session_create(cvsr_ctx *ctx, int32_t m, const cvsr_code *const
     if (cudaStreamCreateWithFlags(&s->copy, cudaStreamNonBlocking) != cudaSuccess) {
         cudaFree(s->mem);
         delete s;
-        return CVSR_ECUDA;
+        return cvsr_internal_fail(CVSR_ECUDA, "session copy stream");
     }
     for (int i = 0; i < 8; ++i) {
         cudaEventCreateWithFlags(&s->ev_in[i], cudaEventDisableTiming);
@@ -121,7 +123,7 @@ static cvsr_status run_range(cvsr_session *s, const float *x, const float *y, in
 }
 
 cvsr_status cvsr_session_run(cvsr_session *s, const float *x, const float *y, cvsr_stats *stats_out) {
-    if (!s || !x || !y) return CVSR_EINVAL;
+    if (!s || !x || !y) return cvsr_internal_fail(CVSR_EINVAL, "null session or buffer");
     return run_range(s, x, y, 0, s->frames, stats_out);
 }
 
@@ -131,7 +133,7 @@ cvsr_status cvsr_session_run(cvsr_session *s, const float *x, const float *y, cv
 // chunking.  stats_out (if requested) is accumulated over the chunks.
 cvsr_status cvsr_session_run_host(cvsr_session *s, const float *x_host, const float *y_host, uint8_t *label_host,
                                   uint8_t *frame_ok_host, int32_t *iters_host, cvsr_stats *stats_out) {
-    if (!s || !x_host || !y_host || !frame_ok_host) return CVSR_EINVAL;
+    if (!s || !x_host || !y_host || !frame_ok_host) return cvsr_internal_fail(CVSR_EINVAL, "null session or buffer");
     cudaStream_t st = cvsr_internal_ctx_stream(s->ctx);
     cudaStream_t cs = s->copy;
     const int chunks = s->frames >= 4 * 128 ? 4 : 1;
@@ -139,17 +141,17 @@ cvsr_status cvsr_session_run_host(cvsr_session *s, const float *x_host, const fl
     for (int c = 0; c <= chunks; ++c) b[c] = (int32_t)((int64_t)s->frames * c / chunks);
     if (stats_out) memset(stats_out, 0, sizeof(*stats_out));
     // inputs must not be overwritten while the previous call's work still reads them
-    if (cudaStreamSynchronize(st) != cudaSuccess) return CVSR_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return cvsr_internal_fail(CVSR_ECUDA, "session: CUDA copy or synchronisation failed");
     auto h2d = [&](int c) -> bool {
         const size_t off = (size_t)b[c] * s->n, bytes = (size_t)(b[c + 1] - b[c]) * s->n * 4;
         return cudaMemcpyAsync(s->x + off, x_host + off, bytes, cudaMemcpyHostToDevice, cs) == cudaSuccess &&
                cudaMemcpyAsync(s->y + off, y_host + off, bytes, cudaMemcpyHostToDevice, cs) == cudaSuccess &&
                cudaEventRecord(s->ev_in[c], cs) == cudaSuccess;
     };
-    if (!h2d(0)) return CVSR_ECUDA;
+    if (!h2d(0)) return cvsr_internal_fail(CVSR_ECUDA, "session: CUDA copy or synchronisation failed");
     for (int c = 0; c < chunks; ++c) {
-        if (c + 1 < chunks && !h2d(c + 1)) return CVSR_ECUDA;
-        if (cudaStreamWaitEvent(st, s->ev_in[c], 0) != cudaSuccess) return CVSR_ECUDA;
+        if (c + 1 < chunks && !h2d(c + 1)) return cvsr_internal_fail(CVSR_ECUDA, "session: CUDA copy or synchronisation failed");
+        if (cudaStreamWaitEvent(st, s->ev_in[c], 0) != cudaSuccess) return cvsr_internal_fail(CVSR_ECUDA, "session: CUDA copy or synchronisation failed");
         cvsr_stats cst;
         if (cvsr_status r = run_range(s, s->x, s->y, b[c], b[c + 1] - b[c], stats_out ? &cst : nullptr)) return r;
         if (stats_out) {
@@ -165,24 +167,24 @@ cvsr_status cvsr_session_run_host(cvsr_session *s, const float *x_host, const fl
             stats_out->alice_seconds += cst.alice_seconds;
         }
         if (cudaEventRecord(s->ev_out[c], st) != cudaSuccess || cudaStreamWaitEvent(cs, s->ev_out[c], 0) != cudaSuccess)
-            return CVSR_ECUDA;
+            return cvsr_internal_fail(CVSR_ECUDA, "session: CUDA copy or synchronisation failed");
         const int32_t f0 = b[c], nf = b[c + 1] - b[c];
         if (label_host && cudaMemcpyAsync(label_host + (size_t)f0 * s->n, s->label_alice + (size_t)f0 * s->n,
                                           (size_t)nf * s->n, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
-            return CVSR_ECUDA;
+            return cvsr_internal_fail(CVSR_ECUDA, "session: CUDA copy or synchronisation failed");
         if (cudaMemcpyAsync(frame_ok_host + f0, s->frame_ok + f0, nf, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
-            return CVSR_ECUDA;
+            return cvsr_internal_fail(CVSR_ECUDA, "session: CUDA copy or synchronisation failed");
         if (iters_host && cudaMemcpyAsync(iters_host + (size_t)f0 * s->m, s->iters + (size_t)f0 * s->m,
                                           (size_t)nf * s->m * 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
-            return CVSR_ECUDA;
+            return cvsr_internal_fail(CVSR_ECUDA, "session: CUDA copy or synchronisation failed");
     }
-    if (cudaStreamSynchronize(cs) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) return CVSR_ECUDA;
+    if (cudaStreamSynchronize(cs) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) return cvsr_internal_fail(CVSR_ECUDA, "session: CUDA copy or synchronisation failed");
     return CVSR_OK;
 }
 
 cvsr_status cvsr_session_buffers(const cvsr_session *s, uint8_t **label_bob, uint8_t **label_alice,
                                  uint8_t **frame_ok, int32_t **iters) {
-    if (!s) return CVSR_EINVAL;
+    if (!s) return cvsr_internal_fail(CVSR_EINVAL, "null session");
     if (label_bob) *label_bob = s->label_bob;
     if (label_alice) *label_alice = s->label_alice;
     if (frame_ok) *frame_ok = s->frame_ok;
