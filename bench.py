@@ -197,9 +197,13 @@ def main():
     x, y = torch_quadratures(F, n, cfg.gamma, device, first_frame=first)
     torch.cuda.synchronize()
 
+    # per-step hash keys (a fresh public key for every verification)
+    key_rng = np.random.default_rng(1000 + rank)
+    keys = [int(k) for k in key_rng.integers(1, (1 << 61) - 2, size=args.warmup + 3 * args.steps + 1)]
     # untimed reference run for statistics (the batch is identical every step)
-    st = pipe.step(x, y, want_stats=True)
+    st = pipe.step(x, y, want_stats=True, key=keys.pop())
     undetected = pipe.count_errors()[1]
+    verified = int(pipe.verified.sum().item())
     # scheduling diagnostic: executed / useful frame-iterations if whole groups of g frames
     # iterate until their slowest member stops (g = 128 tile, 32 sub-tile, 8 = one 32-B sector)
     it_h = pipe.iters.cpu().numpy()
@@ -212,9 +216,11 @@ def main():
         waste[str(j)] = {str(g): float((d[: len(d) // g * g].reshape(-1, g).max(axis=1) * g).sum() /
                                        d[: len(d) // g * g].sum()) for g in (128, 32, 8)}
         waste[str(j)]["max_iters"] = int(d.max() - 1)
-    # frames whose labels differ from Bob's would fail the hash check of PAPER.md:90;
-    # only verified frames count as reconciled (ideal hash in simulation)
-    bits_per_step = (st["frames_ok"] - undetected) * cfg.m * n
+    # only frames that pass the hash check of PAPER.md:90 (cvsr_verify, inside every step) count
+    if verified != st["frames_ok"] - undetected:
+        raise RuntimeError(f"hash check disagrees with the label comparison: {verified} vs "
+                           f"{st['frames_ok']} - {undetected}")
+    bits_per_step = verified * cfg.m * n
 
     def barrier():
         if distributed:
@@ -222,7 +228,7 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        pipe.step(x, y)
+        pipe.step(x, y, key=keys.pop())
     barrier()
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
@@ -230,7 +236,7 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        pipe.step(x, y)
+        pipe.step(x, y, key=keys.pop())
     ev1.record(stream)
     barrier()
     clk = clocks.stop()
@@ -245,7 +251,7 @@ def main():
             cvsr.cvsr_ctx_set_profiling(c, True)
             cvsr.cvsr_ctx_kernel_times(c)  # reset
         for _ in range(args.steps):
-            pipe.step(x, y)
+            pipe.step(x, y, key=keys.pop())
         prof = {}
         for c in ctxs:
             for k, (ms, cnt) in cvsr.cvsr_ctx_kernel_times(c).items():
@@ -265,6 +271,7 @@ def main():
         ectx = cvsr.cvsr_ctx_create(local, stream)
         sess = cvsr.cvsr_session_create(ectx, cfg.m, code_h, cfg.order, cvsr.make_quantiser(cfg.edges()),
                                         cfg.sigma_n, n, F, cvsr.decode_opts(cfg.max_iter, cfg.q_max))
+        cvsr.cvsr_session_set_verify(sess, 0x5DEECE66D)
         for _ in range(max(1, args.warmup)):
             cvsr.cvsr_session_run_host(sess, xh, yh, lab_h, ok_h)
         barrier()

@@ -200,6 +200,27 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
                            int32_t frames, int32_t n, const cvsr_decode_opts *opts, uint8_t *label_out,
                            uint8_t *frame_ok, int32_t *iters, cvsr_stats *stats_out);
 
+/* Verification hash (Step 5: both parties "apply the same hash
+ * function to their reconciled strings and exchange the hash results"):
+ * hash_out[f] = sum_{i<W} w_i * key^(i+1) mod p, p = 2^61 - 1, where w_i is the
+ * i-th little-endian 32-bit word of frame f's labels (uint8[frames][n],
+ * zero-padded to W = ceil(n/4) words).  A universal hash: two different
+ * strings collide with probability <= W/p over a uniformly random key in
+ * [1, p-1].  key must be in [1, 2^61 - 2]; hash_out uint64[frames] (device). */
+cvsr_status cvsr_frame_hash(cvsr_ctx *ctx, const uint8_t *label, int32_t frames, int32_t n, uint64_t key,
+                            uint64_t *hash_out);
+
+/* Both sides of the PAPER.md:90 check in one launch (simulation: Bob's labels
+ * are on the same device): hashes label_alice and label_bob (uint8[frames][n])
+ * with cvsr_frame_hash's definition and key, and writes
+ * verified_out[f] = frame_ok[f] && h_alice[f] == h_bob[f]  (uint8, 0/1).
+ * verified_out may alias frame_ok.  hash_alice_out / hash_bob_out
+ * (uint64[frames]) may be NULL.  A frame that fails is discarded (reading R-6:
+ * per-sub-block abort instead of restarting the whole protocol). */
+cvsr_status cvsr_verify(cvsr_ctx *ctx, const uint8_t *label_alice, const uint8_t *label_bob, const uint8_t *frame_ok,
+                        int32_t frames, int32_t n, uint64_t key, uint8_t *verified_out, uint64_t *hash_alice_out,
+                        uint64_t *hash_bob_out);
+
 /* Simulation-only check against Bob's labels (both uint8[frames][n]):
  * counts_out HOST int64[3] = {frames ok, ok frames whose labels differ from
  * Bob's (undetected errors), differing label bytes over ok frames}.  Syncs. */
@@ -227,6 +248,14 @@ cvsr_status cvsr_session_run(cvsr_session *s, const float *x, const float *y, cv
  * copy overlap the current chunk's kernels; results do not depend on it. */
 cvsr_status cvsr_session_run_host(cvsr_session *s, const float *x_host, const float *y_host, uint8_t *label_host,
                                   uint8_t *frame_ok_host, int32_t *iters_host, cvsr_stats *stats_out);
+
+/* Hash verification inside the session step: key != 0 makes
+ * every later run / run_host call end with cvsr_verify on the session's
+ * labels, so frame_ok (device buffer and frame_ok_host) reports
+ * "converged AND hashes equal".  key = 0 turns it off (default).  stats_out
+ * counts are taken before the hash check.  key must be 0 or in [1, 2^61 - 2]. */
+cvsr_status cvsr_session_set_verify(cvsr_session *s, uint64_t key);
+
 /* device pointers of the session's result buffers (any output may be NULL) */
 cvsr_status cvsr_session_buffers(const cvsr_session *s, uint8_t **label_bob, uint8_t **label_alice,
                                  uint8_t **frame_ok, int32_t **iters);

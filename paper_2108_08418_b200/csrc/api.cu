@@ -945,6 +945,33 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
     return CVSR_OK;
 }
 
+cvsr_status cvsr_frame_hash(cvsr_ctx *ctx, const uint8_t *label, int32_t frames, int32_t n, uint64_t key,
+                            uint64_t *hash_out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (frames < 0 || n <= 0) return fail(CVSR_ESHAPE, "frames=%d n=%d", frames, n);
+    if (key == 0 || key >= ((1ull << 61) - 1ull)) return fail(CVSR_EINVAL, "key must be in [1, 2^61 - 2]");
+    if (frames == 0) return CVSR_OK;
+    if (!label || !hash_out) return fail(CVSR_EINVAL, "null buffer");
+    DeviceGuard g(ctx->device);
+    launch_frame_hash(label, frames, n, key, reinterpret_cast<unsigned long long *>(hash_out), ctx->stream);
+    return check_launch(ctx, 1);
+}
+
+cvsr_status cvsr_verify(cvsr_ctx *ctx, const uint8_t *label_alice, const uint8_t *label_bob, const uint8_t *frame_ok,
+                        int32_t frames, int32_t n, uint64_t key, uint8_t *verified_out, uint64_t *hash_alice_out,
+                        uint64_t *hash_bob_out) {
+    if (cvsr_status st = check_ctx(ctx)) return st;
+    if (frames < 0 || n <= 0) return fail(CVSR_ESHAPE, "frames=%d n=%d", frames, n);
+    if (key == 0 || key >= ((1ull << 61) - 1ull)) return fail(CVSR_EINVAL, "key must be in [1, 2^61 - 2]");
+    if (frames == 0) return CVSR_OK;
+    if (!label_alice || !label_bob || !frame_ok || !verified_out) return fail(CVSR_EINVAL, "null buffer");
+    DeviceGuard g(ctx->device);
+    launch_verify(label_alice, label_bob, frame_ok, frames, n, key, verified_out,
+                  reinterpret_cast<unsigned long long *>(hash_alice_out),
+                  reinterpret_cast<unsigned long long *>(hash_bob_out), ctx->stream);
+    return check_launch(ctx, 1);
+}
+
 cvsr_status cvsr_count_errors(cvsr_ctx *ctx, const uint8_t *label_alice, const uint8_t *label_bob,
                               const uint8_t *frame_ok, int32_t frames, int32_t n, int64_t *counts_out) {
     if (cvsr_status st = check_ctx(ctx)) return st;

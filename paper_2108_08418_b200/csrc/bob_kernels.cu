@@ -245,3 +245,100 @@ void launch_frame_stats(const uint8_t *alive, const uint8_t *attempt, const int3
 }
 
 }  // namespace cvsr
+
+namespace cvsr {
+
+// ---------------------------------------------------------------- verification hash
+// Polynomial hash over GF(p), p = 2^61 - 1 ("apply the same hash
+// function to their reconciled strings and exchange the hash results"):
+//   h_f = sum_{i=0}^{W-1} w_i * key^(i+1) mod p,
+// w_i = the i-th little-endian 32-bit word of frame f's label bytes (zero-padded).
+constexpr unsigned long long P61 = (1ull << 61) - 1ull;
+
+__device__ __forceinline__ unsigned long long mulmod61(unsigned long long a, unsigned long long b) {
+    const unsigned long long lo = a * b, hi = __umul64hi(a, b);
+    unsigned long long r = (lo & P61) + ((lo >> 61) | (hi << 3));
+    r = (r & P61) + (r >> 61);
+    return r >= P61 ? r - P61 : r;
+}
+
+__device__ __forceinline__ unsigned long long addmod61(unsigned long long a, unsigned long long b) {
+    const unsigned long long r = a + b;
+    return r >= P61 ? r - P61 : r;
+}
+
+__device__ unsigned long long powmod61(unsigned long long b, unsigned long long e) {
+    unsigned long long r = 1ull;
+    while (e) {
+        if (e & 1ull) r = mulmod61(r, b);
+        b = mulmod61(b, b);
+        e >>= 1;
+    }
+    return r;
+}
+
+__device__ __forceinline__ uint32_t label_word(const uint8_t *__restrict__ lab, int n, int i, bool aligned) {
+    const int b0 = 4 * i;
+    if (aligned) return __ldg(reinterpret_cast<const uint32_t *>(lab) + i);
+    uint32_t w = 0u;
+    for (int k = 0; k < 4 && b0 + k < n; ++k) w |= (uint32_t)lab[b0 + k] << (8 * k);
+    return w;
+}
+
+// Block per frame; word i goes to thread t = i mod T (coalesced loads), and
+//   h = sum_t key^(t+1) * sum_k w_{t+kT} (key^T)^k,
+// each inner sum by Horner in K = key^T, then a block reduction.  Exact modular
+// arithmetic, so the result is independent of T and bit-identical to the definition.
+// NL = 2 hashes label_a and label_b together and writes ok[f] &= (h_a == h_b).
+template <int NL>
+__global__ void __launch_bounds__(256) k_frame_hash(const uint8_t *__restrict__ label_a,
+                                                   const uint8_t *__restrict__ label_b, int32_t n,
+                                                   unsigned long long key, unsigned long long *__restrict__ out_a,
+                                                   unsigned long long *__restrict__ out_b,
+                                                   const uint8_t *__restrict__ ok_in, uint8_t *__restrict__ ok_out) {
+    const int f = blockIdx.x, T = blockDim.x, t = threadIdx.x;
+    const int W = (n + 3) / 4;
+    const bool aligned = (n & 3) == 0;
+    const uint8_t *la = label_a + (size_t)f * n;
+    const uint8_t *lb = NL == 2 ? label_b + (size_t)f * n : nullptr;
+    const unsigned long long K = powmod61(key, (unsigned long long)T);
+    unsigned long long ha = 0ull, hb = 0ull;
+    const int kmax = t < W ? (W - 1 - t) / T : -1;
+    for (int k = kmax; k >= 0; --k) {
+        const int i = t + k * T;
+        ha = addmod61(mulmod61(ha, K), label_word(la, n, i, aligned));
+        if (NL == 2) hb = addmod61(mulmod61(hb, K), label_word(lb, n, i, aligned));
+    }
+    const unsigned long long kt = powmod61(key, (unsigned long long)(t + 1));
+    __shared__ unsigned long long s[2][256];
+    s[0][t] = mulmod61(ha, kt);
+    if (NL == 2) s[1][t] = mulmod61(hb, kt);
+    __syncthreads();
+    for (int o = T / 2; o > 0; o >>= 1) {
+        if (t < o) {
+            s[0][t] = addmod61(s[0][t], s[0][t + o]);
+            if (NL == 2) s[1][t] = addmod61(s[1][t], s[1][t + o]);
+        }
+        __syncthreads();
+    }
+    if (t == 0) {
+        if (out_a) out_a[f] = s[0][0];
+        if (NL == 2) {
+            if (out_b) out_b[f] = s[1][0];
+            ok_out[f] = (uint8_t)(ok_in[f] && s[0][0] == s[1][0]);
+        }
+    }
+}
+
+void launch_frame_hash(const uint8_t *label, int32_t F, int32_t n, unsigned long long key, unsigned long long *out,
+                       cudaStream_t s) {
+    k_frame_hash<1><<<F, 256, 0, s>>>(label, nullptr, n, key, out, nullptr, nullptr, nullptr);
+}
+
+void launch_verify(const uint8_t *label_a, const uint8_t *label_b, const uint8_t *ok_in, int32_t F, int32_t n,
+                   unsigned long long key, uint8_t *ok_out, unsigned long long *ha, unsigned long long *hb,
+                   cudaStream_t s) {
+    k_frame_hash<2><<<F, 256, 0, s>>>(label_a, label_b, n, key, ha, hb, ok_in, ok_out);
+}
+
+}  // namespace cvsr

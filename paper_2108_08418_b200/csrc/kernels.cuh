@@ -30,6 +30,11 @@ void launch_quantise(const float *edges_host, int m, const float *y, int64_t cou
 void launch_slice_bits(const uint8_t *label, int32_t F, int32_t n, int32_t j, uint32_t *bits, cudaStream_t s);
 void launch_syndrome(const CodeDev &cd, const uint8_t *label, int32_t F, int32_t j, uint32_t *synd, cudaStream_t s);
 void launch_syndrome_bits(const CodeDev &cd, const uint32_t *bits, int32_t F, uint32_t *synd, cudaStream_t s);
+void launch_frame_hash(const uint8_t *label, int32_t F, int32_t n, unsigned long long key, unsigned long long *out,
+                       cudaStream_t s);
+void launch_verify(const uint8_t *label_a, const uint8_t *label_b, const uint8_t *ok_in, int32_t F, int32_t n,
+                   unsigned long long key, uint8_t *ok_out, unsigned long long *ha, unsigned long long *hb,
+                   cudaStream_t s);
 void launch_count_errors(const uint8_t *a, const uint8_t *b, const uint8_t *ok, int32_t F, int32_t n,
                          unsigned long long *counts, cudaStream_t s);
 

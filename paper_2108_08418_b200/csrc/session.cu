@@ -17,6 +17,7 @@ struct cvsr_session {
     cvsr_quantiser q{};
     float sigma_n = 0.0f;
     cvsr_decode_opts opts{};
+    uint64_t verify_key = 0;           // != 0: frame_ok &= hash check (cvsr_session_set_verify)
     void *mem = nullptr;
     cudaStream_t copy = nullptr;       // H2D / D2H stream of run_host
     cudaEvent_t ev_in[8] = {}, ev_out[8] = {};
@@ -118,8 +119,20 @@ static cvsr_status run_range(cvsr_session *s, const float *x, const float *y, in
         if (st) return st;
         sy[j] = dst;
     }
-    return cvsr_reconcile(s->ctx, s->m, s->codes, s->order, &s->q, s->sigma_n, x + off, sy, nf, s->n, &s->opts,
-                          s->label_alice + off, s->frame_ok + f0, s->iters + (size_t)f0 * s->m, stats_out);
+    if (cvsr_status st = cvsr_reconcile(s->ctx, s->m, s->codes, s->order, &s->q, s->sigma_n, x + off, sy, nf, s->n,
+                                        &s->opts, s->label_alice + off, s->frame_ok + f0,
+                                        s->iters + (size_t)f0 * s->m, stats_out))
+        return st;
+    if (!s->verify_key) return CVSR_OK;
+    return cvsr_verify(s->ctx, s->label_alice + off, s->label_bob + off, s->frame_ok + f0, nf, s->n, s->verify_key,
+                       s->frame_ok + f0, nullptr, nullptr);
+}
+
+cvsr_status cvsr_session_set_verify(cvsr_session *s, uint64_t key) {
+    if (!s) return cvsr_internal_fail(CVSR_EINVAL, "null session");
+    if (key >= ((1ull << 61) - 1ull)) return cvsr_internal_fail(CVSR_EINVAL, "key must be 0 or in [1, 2^61 - 2]");
+    s->verify_key = key;
+    return CVSR_OK;
 }
 
 cvsr_status cvsr_session_run(cvsr_session *s, const float *x, const float *y, cvsr_stats *stats_out) {

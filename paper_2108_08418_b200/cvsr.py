@@ -80,6 +80,9 @@ _SIGS = {
     "cvsr_reconcile": ([_vp, _i32, _P(_vp), _P(_i32), _P(cvsr_quantiser), _f32, _vp, _P(_vp), _i32, _i32,
                         _P(cvsr_decode_opts), _vp, _vp, _vp, _P(cvsr_stats)], _i32),
     "cvsr_count_errors": ([_vp, _vp, _vp, _vp, _i32, _i32, _P(_i64)], _i32),
+    "cvsr_frame_hash": ([_vp, _vp, _i32, _i32, ctypes.c_uint64, _vp], _i32),
+    "cvsr_session_set_verify": ([_vp, ctypes.c_uint64], _i32),
+    "cvsr_verify": ([_vp, _vp, _vp, _vp, _i32, _i32, ctypes.c_uint64, _vp, _vp, _vp], _i32),
     "cvsr_session_create": ([_vp, _i32, _P(_vp), _P(_i32), _P(cvsr_quantiser), _f32, _i32, _i32,
                              _P(cvsr_decode_opts), _P(_vp)], _i32),
     "cvsr_session_run": ([_vp, _vp, _vp, _P(cvsr_stats)], _i32),
@@ -246,6 +249,21 @@ def cvsr_reconcile(ctx: int, m: int, codes: Sequence[Optional[int]], order: Sequ
           ctypes.byref(opts), _ptr(label_out), _ptr(frame_ok), _ptr(iters),
           ctypes.byref(st) if st is not None else None)
     return st.as_dict(m) if st is not None else None
+
+
+def cvsr_frame_hash(ctx: int, label, frames: int, n: int, key: int, hash_out) -> None:
+    _call("cvsr_frame_hash", ctx, _ptr(label), frames, n, key, _ptr(hash_out))
+
+
+def cvsr_session_set_verify(sess: int, key: int) -> None:
+    _call("cvsr_session_set_verify", sess, key)
+
+
+def cvsr_verify(ctx: int, label_alice, label_bob, frame_ok, frames: int, n: int, key: int, verified_out,
+                hash_alice_out=None, hash_bob_out=None) -> None:
+    _call("cvsr_verify", ctx, _ptr(label_alice), _ptr(label_bob), _ptr(frame_ok), frames, n, key,
+          _ptr(verified_out), _ptr(hash_alice_out) if hash_alice_out is not None else None,
+          _ptr(hash_bob_out) if hash_bob_out is not None else None)
 
 
 def cvsr_count_errors(ctx: int, label_alice, label_bob, frame_ok, frames: int, n: int):

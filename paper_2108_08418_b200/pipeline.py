@@ -47,6 +47,9 @@ class SRPipeline:
                      for c in codes]
         self.label_alice = torch.empty((frames, n), dtype=torch.uint8, **kw)
         self.frame_ok = torch.empty((frames,), dtype=torch.uint8, **kw)
+        self.verified = torch.empty((frames,), dtype=torch.uint8, **kw)
+        self.hash_alice = torch.empty((frames,), dtype=torch.int64, **kw)
+        self.hash_bob = torch.empty((frames,), dtype=torch.int64, **kw)
         self.iters = torch.empty((frames, m), dtype=torch.int32, **kw)
         self.codes = list(codes)
 
@@ -63,9 +66,19 @@ class SRPipeline:
                                    self.frames, self.n, self.opts, self.label_alice, self.frame_ok, self.iters,
                                    want_stats=want_stats)
 
-    def step(self, x: torch.Tensor, y: torch.Tensor, want_stats: bool = False) -> Optional[dict]:
+    def verify(self, key: int) -> None:
+        """PAPER.md:90 hash check: verified = frame_ok AND hash(Alice) == hash(Bob) (keyed per call)."""
+        cvsr.cvsr_verify(self.ctx, self.label_alice, self.label_bob, self.frame_ok, self.frames, self.n, key,
+                         self.verified, self.hash_alice, self.hash_bob)
+
+    def step(self, x: torch.Tensor, y: torch.Tensor, want_stats: bool = False,
+             key: Optional[int] = None) -> Optional[dict]:
+        """Bob, Alice and (key given) the hash verification of one batch."""
         self.bob(y)
-        return self.alice(x, want_stats)
+        st = self.alice(x, want_stats)
+        if key is not None:
+            self.verify(key)
+        return st
 
     def count_errors(self):
         return cvsr.cvsr_count_errors(self.ctx, self.label_alice, self.label_bob, self.frame_ok, self.frames, self.n)
@@ -105,7 +118,7 @@ class SplitPipeline:
         self.pool = cf.ThreadPoolExecutor(max_workers=k)
         self.device = device
 
-    def step(self, x: torch.Tensor, y: torch.Tensor, want_stats: bool = False):
+    def step(self, x: torch.Tensor, y: torch.Tensor, want_stats: bool = False, key: Optional[int] = None):
         main = torch.cuda.current_stream(self.device)
         ev = main.record_event()
         for s in self.streams:
@@ -114,7 +127,7 @@ class SplitPipeline:
         def run(i):
             a, b = self.ranges[i]
             with torch.cuda.stream(self.streams[i]):
-                return self.parts[i].step(x[a:b], y[a:b], want_stats)
+                return self.parts[i].step(x[a:b], y[a:b], want_stats, key)
 
         res = list(self.pool.map(run, range(self.k)))
         for s in self.streams:
@@ -144,6 +157,10 @@ class SplitPipeline:
     @property
     def label_alice(self):
         return torch.cat([p.label_alice for p in self.parts])
+
+    @property
+    def verified(self):
+        return torch.cat([p.verified for p in self.parts])
 
     @property
     def frame_ok(self):

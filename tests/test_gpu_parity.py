@@ -461,3 +461,65 @@ def test_compaction_switch_subprocess():
         assert res.returncode == 0, res.stderr[-2000:]
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+# ----------------------------------------------------------------- verification hash (R-6)
+@pytest.mark.parametrize("n", [1, 3, 5, 255, 1024, 4097, 65536])
+def test_frame_hash_and_verify_bitexact(cv, ctx, n):
+    """cvsr_frame_hash / cvsr_verify equal the oracle's polynomial hash bit for bit (aligned and
+    ragged n); verified = frame_ok AND equal hashes; a single flipped label bit is caught."""
+    from oracle import verify
+    rng = np.random.default_rng(n)
+    F = 6 if n < 65536 else 3
+    lab_b = rng.integers(0, 32, size=(F, n), dtype=np.uint8)
+    lab_a = lab_b.copy()
+    lab_a[1, rng.integers(0, n)] ^= np.uint8(1 << rng.integers(0, 5))       # frame 1 wrong
+    ok = np.ones(F, np.uint8)
+    ok[2] = 0                                                               # frame 2 not converged
+    da, db, dok = dev(lab_a), dev(lab_b), dev(ok)
+    for key in (1, 1 << 32, int(rng.integers(1, verify.P61 - 1)), verify.P61 - 2):
+        h = torch.empty(F, dtype=torch.int64, device="cuda")
+        cv.cvsr_frame_hash(ctx, da, F, n, key, h)
+        ref_a = verify.frame_hash(lab_a, key)
+        assert np.array_equal(h.cpu().numpy().astype(np.uint64), ref_a)
+        ha, hb = torch.empty_like(h), torch.empty_like(h)
+        ver = torch.empty(F, dtype=torch.uint8, device="cuda")
+        cv.cvsr_verify(ctx, da, db, dok, F, n, key, ver, ha, hb)
+        assert np.array_equal(ha.cpu().numpy().astype(np.uint64), ref_a)
+        assert np.array_equal(hb.cpu().numpy().astype(np.uint64), verify.frame_hash(lab_b, key))
+        want = ok.copy()
+        want[1] = 0
+        assert np.array_equal(ver.cpu().numpy(), want)
+    with pytest.raises(cv.CvsrError):
+        cv.cvsr_frame_hash(ctx, da, F, n, 0, h)
+    cv.cvsr_frame_hash(ctx, da, 0, n, 5, h)   # empty batch is a no-op
+
+
+def test_reconcile_then_verify(cv, ctx):
+    """After reconciliation the hash check passes exactly on the frames whose labels equal Bob's
+    (the session's in-place variant agrees)."""
+    cfg = configs.scaled(configs.C2, 4096, 48)
+    codes_l = cfg.build_codes()
+    x, y = awgn.quadratures(cfg.frames, cfg.n, cfg.gamma, seed=5)
+    from paper_2108_08418_b200.pipeline import SRPipeline
+    pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, cfg.n, cfg.frames, torch.device("cuda:0"),
+                      max_iter=cfg.max_iter)
+    pipe.step(dev(x), dev(y), key=0x1234567)
+    torch.cuda.synchronize()
+    same = (pipe.label_alice == pipe.label_bob).all(dim=1).cpu().numpy()
+    ok = pipe.frame_ok.cpu().numpy().astype(bool)
+    assert np.array_equal(pipe.verified.cpu().numpy().astype(bool), ok & same)
+    hs = [load(cv, ctx, c) if c is not None else None for c in codes_l]
+    sess = cv.cvsr_session_create(ctx, cfg.m, hs, cfg.order, cv.make_quantiser(cfg.edges()), cfg.sigma_n, cfg.n,
+                                  cfg.frames, cv.decode_opts(cfg.max_iter, 40.0))
+    cv.cvsr_session_set_verify(sess, 0x1234567)
+    lab = np.empty((cfg.frames, cfg.n), np.uint8)
+    okh = np.empty(cfg.frames, np.uint8)
+    it = np.empty((cfg.frames, cfg.m), np.int32)
+    cv.cvsr_session_run_host(sess, np.ascontiguousarray(x), np.ascontiguousarray(y), lab, okh, it)
+    assert np.array_equal(okh, pipe.verified.cpu().numpy())
+    cv.cvsr_session_destroy(sess)
+    for h in hs:
+        if h:
+            cv.cvsr_code_free(h)
+    pipe.close()

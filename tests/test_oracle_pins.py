@@ -329,3 +329,43 @@ def test_bp_36_threshold_trend():
         return 1 - conv.mean()
     assert fer(4096, 2.0) < fer(256, 2.0)
     assert fer(2048, 0.3) > 0.9
+
+
+# ----------------------------------------------------------------- verification hash (R-6)
+def test_hash_key1_is_word_checksum():
+    """key = 1: h = sum of the little-endian 32-bit words mod p (numpy '<u4' view, padding zeros)."""
+    from oracle import verify
+    rng = np.random.default_rng(7)
+    for n in (1, 3, 4, 5, 17, 1024):
+        lab = rng.integers(0, 256, size=(3, n), dtype=np.uint8)
+        pad = np.zeros((3, (-n) % 4), np.uint8)
+        words = np.concatenate([lab, pad], axis=1).copy().view("<u4").astype(object)
+        want = [int(sum(r)) % verify.P61 for r in words]
+        assert list(map(int, verify.frame_hash(lab, 1))) == want
+
+
+def test_hash_key_2pow32_is_shifted_integer():
+    """key = 2^32: h = 2^32 * int.from_bytes(label, 'little') mod p (exponent offset i+1, byte order)."""
+    from oracle import verify
+    rng = np.random.default_rng(8)
+    for n in (1, 2, 7, 8, 33, 1000):
+        lab = rng.integers(0, 256, size=(4, n), dtype=np.uint8)
+        want = [((1 << 32) * int.from_bytes(r.tobytes(), "little")) % verify.P61 for r in lab]
+        assert list(map(int, verify.frame_hash(lab, 1 << 32))) == want
+
+
+def test_hash_zero_and_collision_bound():
+    """Zero string hashes to 0 for every key; distinct strings differ at random keys (<= W/p collisions)."""
+    from oracle import verify
+    rng = np.random.default_rng(9)
+    z = np.zeros((2, 37), np.uint8)
+    for key in (1, 2, 12345, verify.P61 - 2):
+        assert not verify.frame_hash(z, key).any()
+    lab = rng.integers(0, 32, size=(1, 512), dtype=np.uint8)
+    for t in range(20):
+        other = lab.copy()
+        other[0, rng.integers(0, 512)] ^= np.uint8(1 << rng.integers(0, 5))
+        key = int(rng.integers(1, verify.P61 - 1))
+        assert verify.frame_hash(lab, key)[0] != verify.frame_hash(other, key)[0]
+    with pytest.raises(ValueError):
+        verify.frame_hash(lab, 0)
