@@ -33,10 +33,12 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every .cu to an object in parallel, then link libcvsr.so."""
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile every .cu to an object in parallel, then link libcvsr.so (or `out`,
+    with extra -D `defines`, for A/B variants)."""
+    if out is None and not force and not stale():
         return LIB
+    target = out or LIB
     import concurrent.futures as cf
     import tempfile
     objdir = tempfile.mkdtemp(prefix="cvsr_build_")
@@ -44,7 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [nvcc(), *flags, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        cmd = [nvcc(), *flags, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c", src,
+               "-o", obj]
         return obj, subprocess.run(cmd, capture_output=True, text=True)
 
     with cf.ThreadPoolExecutor(max_workers=max(1, min(len(SOURCES), os.cpu_count() or 1))) as ex:
@@ -53,17 +56,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for _, r in results:
         if r.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + r.stderr[-6000:])
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = target + f".tmp{os.getpid()}"
     link = subprocess.run([nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
                            *[o for o, _ in results], "-o", tmp], capture_output=True, text=True)
     if link.returncode != 0:
         raise RuntimeError("nvcc link failed:\n" + link.stderr[-6000:])
     if verbose:
         print(log)
-    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
-        f.write(log)
-    os.replace(tmp, LIB)
-    return LIB
+    if out is None:
+        with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+            f.write(log)
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -16,13 +16,17 @@
 // Algorithm (PAPER.md:189 BP decoder, PAPER.md:231 message passes; SURVEY.md
 // §8(c) O5 readings A-8 flooding, A-10 V2C clamp, A-12 stopping rule):
 //   CN: r_e = (1 - 2 s_c) * BOXPLUS_{e' != e} q_e'.  With t = tanh(|q|/2) the
-//       magnitude is 2 atanh(P_e), P_e = prod_{e' != e} t_e'.  It is evaluated
-//       through complements, which never cancel:
-//         w = 1 - t = 2u / (1 + u),  u = e^-|q|
-//         c_e = 1 - P_e = (+)_{e' != e} w_e',   a (+) b = a + b - ab  (prefix/suffix)
-//         |r_e| = ln((1 + P_e) / (1 - P_e)) = ln((2 - c_e) / c_e)
-//       (4 MUFU per edge; a zero message gives w = 1, c = 1, r = 0 exactly; a
-//       degree-1 check gives c = 0, |r| = +inf -> Q_MAX, the empty-fold rule).
+//       magnitude is 2 atanh(P_e), P_e = prod_{e' != e} t_e'.  With u = e^-|q|,
+//       t = (1 - u) / (1 + u) = N / D, and the product is carried as the pair
+//       (S, Delta) = (prod D + prod N, prod D - prod N) (up to a common factor):
+//         edge e = (1, u_e),   (S1, d1) x (S2, d2) = (S1 S2 + d1 d2, S1 d2 + d1 S2)
+//         |r_e| = ln((1 + P_e) / (1 - P_e)) = ln S_e - ln Delta_e   (prefix/suffix)
+//       All terms are non-negative, so nothing cancels; 3 MUFU per edge (ex2 and
+//       two lg2), no reciprocal and no "total minus own".  A zero message gives
+//       S = Delta, r = 0 exactly; a degree-1 check gives Delta = 0, |r| = +inf ->
+//       Q_MAX, the empty-fold rule.  (Checks of degree > 12 use the complement
+//       form w = 1 - t, c = 1 - prod(1 - w), |r| = ln((2 - c)/c) in cn_check_generic,
+//       whose products cannot overflow for any degree.)
 //       Sign = syndrome bit XOR the other edges' signs.
 //   VN: post_v = L_v + sum_e r_e ; q_e = clamp(post_v - r_e, +-Q_MAX);
 //       xhat_v = [post_v < 0].
@@ -69,27 +73,42 @@ __device__ __forceinline__ uint32_t lane_act(const uint4 &m, int lane) {
 
 // ------------------------------------------------------------------ check nodes
 
-// q (log2 units) -> r (log2 units), in registers
+// q (log2 units) -> r (log2 units), in registers.
+// "Sum/difference" form of the tanh rule: with u = 2^-|q| every edge is the pair
+// (1, u) ~ (D + N, D - N) of t = N / D = (1 - u) / (1 + u), and a product of t's
+// is tracked as (S, Delta) = (prod D + prod N, prod D - prod N) up to a common
+// factor:  (S1, d1) x (S2, d2) = (S1 S2 + d1 d2, S1 d2 + d1 S2).  Every term is
+// non-negative (no cancellation), the leave-one-out pairs come from prefix and
+// suffix products, and |r| = ln((1 + P) / (1 - P)) = lg2(S) - lg2(Delta) in log2
+// units: 3 MUFU per edge (ex2, 2 lg2) and no reciprocal.  A zero message gives
+// S = Delta, r = 0 exactly; an empty fold (degree-1 check) gives Delta = 0,
+// |r| = +inf -> Q_MAX.
 template <int DC>
 __device__ __forceinline__ void cn_update(float (&q)[DC], uint32_t sbit, float qmax2) {
-    float w[DC];
+    float u[DC];
     uint32_t par = sbit;
 #pragma unroll
     for (int i = 0; i < DC; ++i) {
-        const float u = ex2f(-fabsf(q[i]));
-        w[i] = 2.0f * u * rcpf(1.0f + u);
+        u[i] = ex2f(-fabsf(q[i]));
         par ^= sgnbit(q[i]);
     }
-    float pre[DC];
-    pre[0] = 0.0f;
+    float ps[DC], pd[DC];
+    ps[0] = 1.0f;
+    pd[0] = 0.0f;
 #pragma unroll
-    for (int i = 1; i < DC; ++i) pre[i] = cplus(pre[i - 1], w[i - 1]);
-    float suf = 0.0f;
+    for (int i = 1; i < DC; ++i) {
+        ps[i] = fmaf(u[i - 1], pd[i - 1], ps[i - 1]);
+        pd[i] = fmaf(u[i - 1], ps[i - 1], pd[i - 1]);
+    }
+    float ss = 1.0f, sd = 0.0f;
 #pragma unroll
     for (int i = DC - 1; i >= 0; --i) {
-        const float c = cplus(pre[i], suf);
-        const float mag = fmaxf(fminf(lg2f((2.0f - c) * rcpf(c)), qmax2), 0.0f);
-        suf = cplus(suf, w[i]);
+        const float S = fmaf(ps[i], ss, pd[i] * sd);
+        const float D = fmaf(ps[i], sd, pd[i] * ss);
+        const float mag = fmaxf(fminf(lg2f(S) - lg2f(D), qmax2), 0.0f);
+        const float ns = fmaf(u[i], sd, ss);
+        sd = fmaf(u[i], ss, sd);
+        ss = ns;
         q[i] = (par ^ sgnbit(q[i])) ? -mag : mag;
     }
 }
@@ -100,12 +119,9 @@ __device__ __forceinline__ void cn_update(float (&q)[DC], uint32_t sbit, float q
 // are neither loaded nor stored: one code body per code keeps the i-cache hot.
 constexpr float DUMMY_Q = 200.0f;
 
+// the S frames of this lane (frames that are not active keep their message)
 template <int DC, int S>
-__device__ __forceinline__ void cn_check(float *__restrict__ m, int deg, uint32_t sb, uint32_t al, float qmax2) {
-    if (!al) return;
-    FV<S> q[DC];
-#pragma unroll
-    for (int k = 0; k < DC; ++k) q[k] = (k < deg) ? ldv<S>(m + (size_t)k * LANES * S) : splat<S>(DUMMY_Q);
+__device__ __forceinline__ void cn_lanes(FV<S> (&q)[DC], uint32_t sb, uint32_t al, float qmax2) {
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         if (!((al >> s) & 1u)) continue;
@@ -116,6 +132,15 @@ __device__ __forceinline__ void cn_check(float *__restrict__ m, int deg, uint32_
 #pragma unroll
         for (int k = 0; k < DC; ++k) q[k].c[s] = a[k];
     }
+}
+
+template <int DC, int S>
+__device__ __forceinline__ void cn_check(float *__restrict__ m, int deg, uint32_t sb, uint32_t al, float qmax2) {
+    if (!al) return;
+    FV<S> q[DC];
+#pragma unroll
+    for (int k = 0; k < DC; ++k) q[k] = (k < deg) ? ldv<S>(m + (size_t)k * LANES * S) : splat<S>(DUMMY_Q);
+    cn_lanes<DC, S>(q, sb, al, qmax2);
 #pragma unroll
     for (int k = 0; k < DC; ++k)
         if (k < deg) stv<S>(m + (size_t)k * LANES * S, q[k]);
@@ -245,6 +270,203 @@ __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 24) ? 4 : (DCT *
     if (last && lane < S) {
         const uint32_t v = atomicOr(&s_unsat[lane], 0u);
         if (v) atomicOr(reinterpret_cast<uint32_t *>(&ds.tile_unsat[t]) + lane, v);
+    }
+}
+
+// ------------------------------------------------------------------ check nodes, TMA-streamed
+//
+// The CN pass is a pure stream over the arena: for tile t the messages of checks
+// [c0, c0 + CPI) are ONE contiguous span of (row_ptr[c0 + CPI] - row_ptr[c0]) x
+// 128 S bytes (CSR slot order, frame-interleaved rows).  A persistent CTA walks
+// work items (tile, group of CPI checks); one producer lane streams each item's
+// span into a shared-memory ring with cp.async.bulk (TMA bulk copy, mbarrier
+// complete_tx), CPI consumer warps take one check each, read their DC lines
+// from shared memory, and store C2V straight to global memory.  Loads no longer
+// occupy registers, so the number of bytes in flight is set by the ring depth
+// instead of by occupancy.  Same arithmetic and stores as k_cn (cn_update), so
+// results are bit-identical.
+
+constexpr int CPI = 8;                 // checks per work item = consumer warps per CTA
+constexpr int CN_TMA_THREADS = (CPI + 1) * 32;
+constexpr int CN_TMA_MAX_STAGES = 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// one check of one item: DC lines from the stage, release the stage, update, store
+template <int DC, int S>
+__device__ __forceinline__ void cn_tma_item(const float *__restrict__ sm, float *__restrict__ m, int deg, uint32_t sb,
+                                            uint32_t al, float qmax2, uint64_t *empty_bar, int lane) {
+    constexpr int ROW = LANES * S;
+    FV<S> q[DC];
+    if (al) {
+#pragma unroll
+        for (int k = 0; k < DC; ++k) q[k] = (k < deg) ? ldv<S>(sm + (size_t)k * ROW) : splat<S>(DUMMY_Q);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_bar);
+    if (al) {
+        cn_lanes<DC, S>(q, sb, al, qmax2);
+#pragma unroll
+        for (int k = 0; k < DC; ++k)
+            if (k < deg) stv<S>(m + (size_t)k * ROW, q[k]);
+    }
+}
+
+template <int DCT, int S>
+__global__ void __launch_bounds__(CN_TMA_THREADS, 2) k_cn_tma(CodeDev cd, DecState ds, float qmax2, int groups,
+                                                           int nstage, int stage_bytes) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+    uint64_t *empty = full + CN_TMA_MAX_STAGES;
+    unsigned char *ring = smem + 2 * CN_TMA_MAX_STAGES * sizeof(uint64_t);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_items = ds.counts[0] * groups;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nstage; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], CPI);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    constexpr int ROW = LANES * S;  // floats per edge row of a tile
+    if (warp == CPI) {
+        // producer warp: the lanes look up 32 items' spans at once, then one lane issues
+        // the bulk copies in order (no dependent global load on the issue path)
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int base = blockIdx.x; base < n_items; base += 32 * gridDim.x) {
+            const int my = base + lane * gridDim.x;
+            int t = 0, e0 = 0, e1 = 0;
+            if (my < n_items) {
+                t = ds.active_list[my / groups];
+                const int c0 = (my % groups) * CPI;
+                e0 = cd.row_ptr[c0];
+                e1 = cd.row_ptr[min(c0 + CPI, cd.M)];
+            }
+            const int nb = min(32, (n_items - base + gridDim.x - 1) / gridDim.x);
+            for (int j = 0; j < nb; ++j) {
+                const int tj = __shfl_sync(FULL, t, j), e0j = __shfl_sync(FULL, e0, j),
+                          e1j = __shfl_sync(FULL, e1, j);
+                if (lane == 0) {
+                    mbar_wait(&empty[stage], phase ^ 1u);
+                    const uint32_t bytes = (uint32_t)(e1j - e0j) * ROW * 4u;
+                    mbar_arrive_tx(&full[stage], bytes);
+                    if (bytes)
+                        bulk_g2s(ring + (size_t)stage * stage_bytes, ds.msg + ((size_t)tj * cd.E + e0j) * ROW, bytes,
+                                 &full[stage]);
+                }
+                __syncwarp();
+                if (++stage == nstage) { stage = 0; phase ^= 1u; }
+            }
+        }
+        return;
+    }
+    // consumers: warp w owns check c0 + w of every item.  The per-item metadata is
+    // software-pipelined two items deep: A = (tile, row range) for item i + 2,
+    // B = (hard-decision words, syndrome word, active mask) for item i + 1, so the
+    // dependent gather chain row_ptr -> col_idx -> hb overlaps the compute of item i.
+    struct MetaA { int t, lo, deg, e0; bool valid; };
+    struct MetaB { MetaA a; uint4 h, stc, act; };
+    auto load_a = [&](int it) {
+        MetaA m{0, 0, 0, 0, false};
+        if (it < n_items) {
+            m.t = ds.active_list[it / groups];
+            const int c0 = (it % groups) * CPI, c = c0 + warp;
+            m.e0 = cd.row_ptr[c0];
+            if (c < cd.M) {
+                m.valid = true;
+                m.lo = cd.row_ptr[c];
+                m.deg = cd.row_ptr[c + 1] - m.lo;
+            }
+        }
+        return m;
+    };
+    auto load_b = [&](const MetaA &a, int it) {
+        MetaB m;
+        m.a = a;
+        m.h = make_uint4(0u, 0u, 0u, 0u);
+        m.stc = make_uint4(0u, 0u, 0u, 0u);
+        m.act = make_uint4(0u, 0u, 0u, 0u);
+        if (it < n_items) {
+            m.act = ds.tile_active[a.t];
+            if (a.valid) {
+                const int c = (it % groups) * CPI + warp;
+                m.stc = ds.st[(size_t)a.t * cd.M + c];
+                if (lane < a.deg) m.h = ds.hb[(size_t)a.t * cd.n + cd.col_idx[a.lo + lane]];
+            }
+        }
+        return m;
+    };
+    int stage = 0;
+    uint32_t phase = 0;
+    int pub_t = -1;
+    uint32_t pub = 0u;  // unsatisfied bits of tile pub_t already published by this warp (lane s < S)
+    const int G = gridDim.x;
+    MetaB cur = load_b(load_a(blockIdx.x), blockIdx.x);
+    MetaA nxt = load_a(blockIdx.x + G);
+    for (int it = blockIdx.x; it < n_items; it += G) {
+        const MetaB b_next = load_b(nxt, it + G);
+        const MetaA a_next = load_a(it + 2 * G);
+        const int t = cur.a.t, lo = cur.a.lo, deg = cur.a.deg;
+        const bool have = cur.a.valid;
+        mbar_wait(&full[stage], phase);
+        const uint32_t al = have ? lane_act<S>(cur.act, lane) : 0u;
+        {
+            const float *sm = reinterpret_cast<const float *>(ring + (size_t)stage * stage_bytes) +
+                              (size_t)(lo - cur.a.e0) * ROW + lane * S;
+            float *m = ds.msg + ((size_t)t * cd.E + lo) * ROW + lane * S;
+            const uint32_t sb = lane_act<S>(cur.stc, lane);
+            cn_tma_item<DCT, S>(sm, m, deg, sb, al, qmax2, &empty[stage], lane);
+        }
+        if (++stage == nstage) { stage = 0; phase ^= 1u; }
+        // parity of the check under decision k-1, masked by the active frames
+        uint4 par = cur.stc;
+        par.x ^= __reduce_xor_sync(FULL, cur.h.x);
+        if (S > 1) par.y ^= __reduce_xor_sync(FULL, cur.h.y);
+        if (S > 2) {
+            par.z ^= __reduce_xor_sync(FULL, cur.h.z);
+            par.w ^= __reduce_xor_sync(FULL, cur.h.w);
+        }
+        if (t != pub_t) { pub_t = t; pub = 0u; }
+        if (lane < S && have) {
+            const uint32_t v = cmpu(par, lane) & cmpu(cur.act, lane) & ~pub;
+            if (v) {
+                atomicOr(reinterpret_cast<uint32_t *>(&ds.tile_unsat[t]) + lane, v);
+                pub |= v;
+            }
+        }
+        cur = b_next;
+        nxt = a_next;
     }
 }
 
@@ -915,8 +1137,62 @@ static void launch_cn_s(const CodeDev &cd, const DecState &ds, dim3 grid, float 
     }
 }
 
+// TMA-streamed CN pass (k_cn_tma): ring of nstage stages of CPI x DCT rows per CTA,
+// persistent grid of (CTAs per SM) x SMs.  Opt-in (CVSR_CN_TMA=1): it measured
+// slower than k_cn; CVSR_CN_RING_KB sets the ring budget per CTA.
+static int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+
+template <int DCT, int S>
+static void launch_cn_tma_t(const CodeDev &cd, const DecState &ds, int grid_tiles, float q2, cudaStream_t s) {
+    static int ctas_per_sm = -1, nstage = 0, stage_bytes = 0, n_sm = 0;
+    if (ctas_per_sm < 0) {
+        stage_bytes = CPI * DCT * LANES * S * 4;
+        const int budget = env_int("CVSR_CN_RING_KB", 96) * 1024;
+        nstage = budget / stage_bytes;
+        nstage = nstage < 2 ? 2 : (nstage > CN_TMA_MAX_STAGES ? CN_TMA_MAX_STAGES : nstage);
+        const int smem = 128 + nstage * stage_bytes;
+        cudaFuncSetAttribute(k_cn_tma<DCT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_cn_tma<DCT, S>, CN_TMA_THREADS, smem);
+        if (ctas_per_sm < 1) ctas_per_sm = 1;
+    }
+    const int groups = (cd.M + CPI - 1) / CPI;
+    const long long items = (long long)groups * grid_tiles;
+    const int grid = (int)(items < (long long)ctas_per_sm * n_sm ? items : (long long)ctas_per_sm * n_sm);
+    k_cn_tma<DCT, S><<<grid, CN_TMA_THREADS, 128 + nstage * stage_bytes, s>>>(cd, ds, q2, groups, nstage,
+                                                                               stage_bytes);
+}
+
+template <int S>
+static bool launch_cn_tma_s(const CodeDev &cd, const DecState &ds, int grid_tiles, float q2, cudaStream_t s) {
+    switch (cd.max_dc) {
+        case 1: case 2: launch_cn_tma_t<2, S>(cd, ds, grid_tiles, q2, s); return true;
+        case 3: launch_cn_tma_t<3, S>(cd, ds, grid_tiles, q2, s); return true;
+        case 4: launch_cn_tma_t<4, S>(cd, ds, grid_tiles, q2, s); return true;
+        case 5: launch_cn_tma_t<5, S>(cd, ds, grid_tiles, q2, s); return true;
+        case 6: launch_cn_tma_t<6, S>(cd, ds, grid_tiles, q2, s); return true;
+        case 7: launch_cn_tma_t<7, S>(cd, ds, grid_tiles, q2, s); return true;
+        case 8: launch_cn_tma_t<8, S>(cd, ds, grid_tiles, q2, s); return true;
+        default: return false;
+    }
+}
+
 void launch_cn(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, int check_only, cudaStream_t s) {
     if (grid_tiles <= 0) return;
+    static const int use_tma = env_int("CVSR_CN_TMA", 0);
+    if (use_tma && !check_only) {
+        const float q2t = qmax * LOG2E;
+        bool done = false;
+        if (ds.subs == 4) done = launch_cn_tma_s<4>(cd, ds, grid_tiles, q2t, s);
+        else if (ds.subs == 2) done = launch_cn_tma_s<2>(cd, ds, grid_tiles, q2t, s);
+        else done = launch_cn_tma_s<1>(cd, ds, grid_tiles, q2t, s);
+        if (done) return;
+    }
     const int per_block = WARPS_PER_BLOCK * CPW;
     dim3 grid((cd.M + per_block - 1) / per_block, grid_tiles);
     const float q2 = qmax * LOG2E;

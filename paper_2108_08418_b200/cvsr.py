@@ -15,7 +15,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libcvsr.so")
+# CVSR_LIB: load another build of the same library (tools/build_variant.py A/B runs)
+LIB_PATH = os.environ.get("CVSR_LIB") or os.path.join(_PKG, "libcvsr.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
