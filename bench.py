@@ -304,7 +304,7 @@ def main():
     fer = 1.0 - ok_all / frames_all
 
     # beta (equation: beta) with the realised rates R_j = 1 - M_j/N_R
-    from oracle import analysis  # host-side analysis only (fp64 formulas), not the hot path
+    from paper_2108_08418_b200 import keyrate as analysis  # host-side fp64 formulas
     rates = [c.rate if c is not None else 0.0 for c in codes_l]
     pi_my, _ = analysis.entropies(cfg.gamma, m, cfg.delta)
     beta = analysis.beta(pi_my, m, rates, cfg.gamma)

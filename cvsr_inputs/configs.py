@@ -1,7 +1,7 @@
 """Workload configurations C1..C5 (BASELINE.json ``configs``; readings in SURVEY.md §8(d)).
 
 Numbers marked DERIVED come from SURVEY.md Appendix A and are re-derived by
-``oracle`` (tests/test_oracle_analysis.py) -- this module only stores them.
+``paper_2108_08418_b200.keyrate`` (tests/test_keyrate.py) -- this module only stores them.
 """
 from __future__ import annotations
 

@@ -13,12 +13,9 @@ Parity-pin status per function:
                                      sign symmetry, (3,6) threshold trend)
   reconcile                       -- pinned (composition: reduces to the pinned parts;
                                      noiseless limit; MC posterior of the LLR feed)
-  analysis.*                      -- pinned to the paper's printed/derived values
-                                     (gamma, I_AB, A, C_Finite, beta identities);
-                                     delta* and slice capacities: parity unpinned vs
-                                     paper (the paper prints no value)
+  verify.frame_hash               -- pinned (key = 1 word checksum, key = 2^32 shifted
+                                     integer, zero string, bit-flip detection)
 """
-from . import analysis  # noqa: F401
 from .oracle import (  # noqa: F401
     build, bp_decode, bp_trace, llr_biawgn, llr_slice, quantise, reconcile, slice_bits,
     syndrome, num_threads,

@@ -18,7 +18,7 @@ import torch  # noqa: E402
 
 from cvsr_inputs import configs  # noqa: E402
 from cvsr_inputs.awgn import torch_quadratures  # noqa: E402
-from oracle import analysis  # noqa: E402  (host-side beta formula only)
+from paper_2108_08418_b200 import keyrate as analysis  # noqa: E402  (host-side beta formula)
 from paper_2108_08418_b200.pipeline import SRPipeline  # noqa: E402
 
 
