@@ -249,6 +249,17 @@ cvsr_status cvsr_session_run(cvsr_session *s, const float *x, const float *y, cv
 cvsr_status cvsr_session_run_host(cvsr_session *s, const float *x_host, const float *y_host, uint8_t *label_host,
                                   uint8_t *frame_ok_host, int32_t *iters_host, cvsr_stats *stats_out);
 
+/* Streaming variant for a sequence of batches (the serving loop): batch b's
+ * inputs x_host[b], y_host[b] (pinned host, float[frames][n]) are copied in
+ * while batch b-1 is reconciled, and batch b's results (label_host[b]
+ * uint8[frames][n], may be NULL; frame_ok_host[b] uint8[frames]) are copied out
+ * while batch b+1 runs, using a second device buffer set allocated on the first
+ * call.  Results per batch equal cvsr_session_run_host's.  Synchronous: returns
+ * after the last result copy.  Per-batch statistics are not collected. */
+cvsr_status cvsr_session_run_host_stream(cvsr_session *s, int32_t n_batches, const float *const *x_host,
+                                         const float *const *y_host, uint8_t *const *label_host,
+                                         uint8_t *const *frame_ok_host);
+
 /* Hash verification inside the session step: key != 0 makes
  * every later run / run_host call end with cvsr_verify on the session's
  * labels, so frame_ok (device buffer and frame_ok_host) reports

@@ -25,6 +25,13 @@ struct cvsr_session {
     uint8_t *label_bob = nullptr, *label_alice = nullptr, *frame_ok = nullptr;
     int32_t *iters = nullptr;
     uint32_t *synd[8] = {};
+    // second input/output set + D2H stream of cvsr_session_run_host_stream (allocated on first use)
+    void *mem2 = nullptr;
+    float *x2 = nullptr, *y2 = nullptr;
+    uint8_t *label_alice2 = nullptr, *frame_ok2 = nullptr;
+    int32_t *iters2 = nullptr;
+    cudaStream_t copy_out = nullptr;
+    cudaEvent_t ev_done[2] = {}, ev_d2h[2] = {};
 };
 
 namespace {
@@ -107,7 +114,11 @@ cvsr_status cvsr_session_create(cvsr_ctx *ctx, int32_t m, const cvsr_code *const
 
 // Bob + Alice for frames [f0, f0 + nf) of the session's buffers
 static cvsr_status run_range(cvsr_session *s, const float *x, const float *y, int32_t f0, int32_t nf,
-                             cvsr_stats *stats_out) {
+                             cvsr_stats *stats_out, uint8_t *label_alice = nullptr, uint8_t *frame_ok = nullptr,
+                             int32_t *iters = nullptr) {
+    if (!label_alice) label_alice = s->label_alice;
+    if (!frame_ok) frame_ok = s->frame_ok;
+    if (!iters) iters = s->iters;
     const size_t off = (size_t)f0 * s->n;
     if (cvsr_status st = cvsr_quantise(s->ctx, &s->q, y + off, (int64_t)nf * s->n, s->label_bob + off)) return st;
     const uint32_t *sy[8];
@@ -120,12 +131,12 @@ static cvsr_status run_range(cvsr_session *s, const float *x, const float *y, in
         sy[j] = dst;
     }
     if (cvsr_status st = cvsr_reconcile(s->ctx, s->m, s->codes, s->order, &s->q, s->sigma_n, x + off, sy, nf, s->n,
-                                        &s->opts, s->label_alice + off, s->frame_ok + f0,
-                                        s->iters + (size_t)f0 * s->m, stats_out))
+                                        &s->opts, label_alice + off, frame_ok + f0, iters + (size_t)f0 * s->m,
+                                        stats_out))
         return st;
     if (!s->verify_key) return CVSR_OK;
-    return cvsr_verify(s->ctx, s->label_alice + off, s->label_bob + off, s->frame_ok + f0, nf, s->n, s->verify_key,
-                       s->frame_ok + f0, nullptr, nullptr);
+    return cvsr_verify(s->ctx, label_alice + off, s->label_bob + off, frame_ok + f0, nf, s->n, s->verify_key,
+                       frame_ok + f0, nullptr, nullptr);
 }
 
 cvsr_status cvsr_session_set_verify(cvsr_session *s, uint64_t key) {
@@ -195,6 +206,85 @@ cvsr_status cvsr_session_run_host(cvsr_session *s, const float *x_host, const fl
     return CVSR_OK;
 }
 
+// Batches back to back, double-buffered: batch b+1's inputs are copied in (copy
+// stream) while batch b is reconciled (context stream), and batch b's results are
+// copied out (copy_out stream) while batch b+1 runs.  Whole batches are decoded
+// (no chunking), so only the first batch's input copy and the last batch's
+// result copy are exposed.
+cvsr_status cvsr_session_run_host_stream(cvsr_session *s, int32_t n_batches, const float *const *x_host,
+                                         const float *const *y_host, uint8_t *const *label_host,
+                                         uint8_t *const *frame_ok_host) {
+    if (!s || n_batches < 0 || (n_batches > 0 && (!x_host || !y_host || !frame_ok_host)))
+        return cvsr_internal_fail(CVSR_EINVAL, "null session or buffer list");
+    for (int32_t b = 0; b < n_batches; ++b)
+        if (!x_host[b] || !y_host[b] || !frame_ok_host[b]) return cvsr_internal_fail(CVSR_EINVAL, "null batch buffer");
+    const size_t F = (size_t)s->frames, n = (size_t)s->n;
+    if (!s->mem2) {
+        const size_t bytes = 2 * al(F * n * 4) + al(F * n) + al(F) + al(F * s->m * 4);
+        if (cudaMalloc(&s->mem2, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            s->mem2 = nullptr;
+            return cvsr_internal_fail(CVSR_ENOMEM, "session stream buffers");
+        }
+        char *p = static_cast<char *>(s->mem2);
+        auto take = [&](size_t b) {
+            char *r = p;
+            p += al(b);
+            return r;
+        };
+        s->x2 = reinterpret_cast<float *>(take(F * n * 4));
+        s->y2 = reinterpret_cast<float *>(take(F * n * 4));
+        s->label_alice2 = reinterpret_cast<uint8_t *>(take(F * n));
+        s->frame_ok2 = reinterpret_cast<uint8_t *>(take(F));
+        s->iters2 = reinterpret_cast<int32_t *>(take(F * s->m * 4));
+        if (cudaStreamCreateWithFlags(&s->copy_out, cudaStreamNonBlocking) != cudaSuccess)
+            return cvsr_internal_fail(CVSR_ECUDA, "session copy-out stream");
+        for (int i = 0; i < 2; ++i) {
+            cudaEventCreateWithFlags(&s->ev_done[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&s->ev_d2h[i], cudaEventDisableTiming);
+        }
+    }
+    float *xs[2] = {s->x, s->x2}, *ys[2] = {s->y, s->y2};
+    uint8_t *labs[2] = {s->label_alice, s->label_alice2}, *oks[2] = {s->frame_ok, s->frame_ok2};
+    int32_t *its[2] = {s->iters, s->iters2};
+    cudaStream_t st = cvsr_internal_ctx_stream(s->ctx), cin = s->copy, cout = s->copy_out;
+    const char *emsg = "session stream: CUDA copy or synchronisation failed";
+    if (cudaStreamSynchronize(st) != cudaSuccess) return cvsr_internal_fail(CVSR_ECUDA, emsg);
+    auto h2d = [&](int32_t b) -> bool {
+        const int k = b & 1;
+        return cudaMemcpyAsync(xs[k], x_host[b], F * n * 4, cudaMemcpyHostToDevice, cin) == cudaSuccess &&
+               cudaMemcpyAsync(ys[k], y_host[b], F * n * 4, cudaMemcpyHostToDevice, cin) == cudaSuccess &&
+               cudaEventRecord(s->ev_in[k], cin) == cudaSuccess;
+    };
+    if (n_batches > 0 && !h2d(0)) return cvsr_internal_fail(CVSR_ECUDA, emsg);
+    for (int32_t b = 0; b < n_batches; ++b) {
+        const int k = b & 1;
+        if (b + 1 < n_batches) {
+            // set (b+1)&1 was last read by batch b-1's kernels
+            if (b >= 1 && cudaStreamWaitEvent(cin, s->ev_done[(b + 1) & 1], 0) != cudaSuccess)
+                return cvsr_internal_fail(CVSR_ECUDA, emsg);
+            if (!h2d(b + 1)) return cvsr_internal_fail(CVSR_ECUDA, emsg);
+        }
+        if (cudaStreamWaitEvent(st, s->ev_in[k], 0) != cudaSuccess) return cvsr_internal_fail(CVSR_ECUDA, emsg);
+        // set k's results of batch b-2 must have left the device
+        if (b >= 2 && cudaStreamWaitEvent(st, s->ev_d2h[k], 0) != cudaSuccess)
+            return cvsr_internal_fail(CVSR_ECUDA, emsg);
+        if (cvsr_status r = run_range(s, xs[k], ys[k], 0, s->frames, nullptr, labs[k], oks[k], its[k])) return r;
+        if (cudaEventRecord(s->ev_done[k], st) != cudaSuccess || cudaStreamWaitEvent(cout, s->ev_done[k], 0) != cudaSuccess)
+            return cvsr_internal_fail(CVSR_ECUDA, emsg);
+        if (label_host && label_host[b] &&
+            cudaMemcpyAsync(label_host[b], labs[k], F * n, cudaMemcpyDeviceToHost, cout) != cudaSuccess)
+            return cvsr_internal_fail(CVSR_ECUDA, emsg);
+        if (cudaMemcpyAsync(frame_ok_host[b], oks[k], F, cudaMemcpyDeviceToHost, cout) != cudaSuccess ||
+            cudaEventRecord(s->ev_d2h[k], cout) != cudaSuccess)
+            return cvsr_internal_fail(CVSR_ECUDA, emsg);
+    }
+    if (cudaStreamSynchronize(cin) != cudaSuccess || cudaStreamSynchronize(cout) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return cvsr_internal_fail(CVSR_ECUDA, emsg);
+    return CVSR_OK;
+}
+
 cvsr_status cvsr_session_buffers(const cvsr_session *s, uint8_t **label_bob, uint8_t **label_alice,
                                  uint8_t **frame_ok, int32_t **iters) {
     if (!s) return cvsr_internal_fail(CVSR_EINVAL, "null session");
@@ -212,10 +302,19 @@ void cvsr_session_destroy(cvsr_session *s) {
         cudaStreamSynchronize(s->copy);
         cudaStreamDestroy(s->copy);
     }
+    if (s->copy_out) {
+        cudaStreamSynchronize(s->copy_out);
+        cudaStreamDestroy(s->copy_out);
+    }
     for (int i = 0; i < 8; ++i) {
         if (s->ev_in[i]) cudaEventDestroy(s->ev_in[i]);
         if (s->ev_out[i]) cudaEventDestroy(s->ev_out[i]);
     }
+    for (int i = 0; i < 2; ++i) {
+        if (s->ev_done[i]) cudaEventDestroy(s->ev_done[i]);
+        if (s->ev_d2h[i]) cudaEventDestroy(s->ev_d2h[i]);
+    }
+    if (s->mem2) cudaFree(s->mem2);
     cudaFree(s->mem);
     delete s;
 }

@@ -83,6 +83,7 @@ _SIGS = {
     "cvsr_count_errors": ([_vp, _vp, _vp, _vp, _i32, _i32, _P(_i64)], _i32),
     "cvsr_frame_hash": ([_vp, _vp, _i32, _i32, ctypes.c_uint64, _vp], _i32),
     "cvsr_session_set_verify": ([_vp, ctypes.c_uint64], _i32),
+    "cvsr_session_run_host_stream": ([_vp, _i32, _vp, _vp, _vp, _vp], _i32),
     "cvsr_verify": ([_vp, _vp, _vp, _vp, _i32, _i32, ctypes.c_uint64, _vp, _vp, _vp], _i32),
     "cvsr_session_create": ([_vp, _i32, _P(_vp), _P(_i32), _P(cvsr_quantiser), _f32, _i32, _i32,
                              _P(cvsr_decode_opts), _P(_vp)], _i32),
@@ -254,6 +255,19 @@ def cvsr_reconcile(ctx: int, m: int, codes: Sequence[Optional[int]], order: Sequ
 
 def cvsr_frame_hash(ctx: int, label, frames: int, n: int, key: int, hash_out) -> None:
     _call("cvsr_frame_hash", ctx, _ptr(label), frames, n, key, _ptr(hash_out))
+
+
+def cvsr_session_run_host_stream(sess: int, x_hosts, y_hosts, label_hosts, frame_ok_hosts) -> None:
+    """Lists of host buffers, one per batch (torch CPU tensors, pinned, or numpy arrays);
+    label_hosts entries may be None."""
+    def hp(a):
+        if a is None:
+            return None
+        return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+    nb = len(x_hosts)
+    arr = lambda lst: (ctypes.c_void_p * max(1, nb))(*[hp(a) for a in lst])  # noqa: E731
+    _call("cvsr_session_run_host_stream", sess, nb, arr(x_hosts), arr(y_hosts), arr(label_hosts),
+          arr(frame_ok_hosts))
 
 
 def cvsr_session_set_verify(sess: int, key: int) -> None:

@@ -523,3 +523,35 @@ def test_reconcile_then_verify(cv, ctx):
         if h:
             cv.cvsr_code_free(h)
     pipe.close()
+
+
+def test_session_stream_matches_run_host(cv, ctx):
+    """cvsr_session_run_host_stream (double-buffered batches) returns, per batch, exactly what
+    cvsr_session_run_host returns for that batch alone (3 batches, hash check on)."""
+    cfg = configs.scaled(configs.C2, 4096, 40)
+    codes_l = cfg.build_codes()
+    hs = [load(cv, ctx, c) if c is not None else None for c in codes_l]
+    sess = cv.cvsr_session_create(ctx, cfg.m, hs, cfg.order, cv.make_quantiser(cfg.edges()), cfg.sigma_n, cfg.n,
+                                  cfg.frames, cv.decode_opts(cfg.max_iter, 40.0))
+    cv.cvsr_session_set_verify(sess, 987654321)
+    xs, ys, want_lab, want_ok = [], [], [], []
+    for b in range(3):
+        x, y = awgn.quadratures(cfg.frames, cfg.n, cfg.gamma, seed=100 + b)
+        x, y = np.ascontiguousarray(x), np.ascontiguousarray(y)
+        lab = np.empty((cfg.frames, cfg.n), np.uint8)
+        ok = np.empty(cfg.frames, np.uint8)
+        cv.cvsr_session_run_host(sess, x, y, lab, ok)
+        xs.append(x), ys.append(y), want_lab.append(lab), want_ok.append(ok)
+    labs = [np.full((cfg.frames, cfg.n), 255, np.uint8) for _ in range(3)]
+    oks = [np.full(cfg.frames, 255, np.uint8) for _ in range(3)]
+    cv.cvsr_session_run_host_stream(sess, xs, ys, labs, oks)
+    for b in range(3):
+        assert np.array_equal(labs[b], want_lab[b]) and np.array_equal(oks[b], want_ok[b])
+    # labels may be skipped; a second call reuses the buffer sets
+    oks2 = [np.zeros(cfg.frames, np.uint8) for _ in range(3)]
+    cv.cvsr_session_run_host_stream(sess, xs, ys, [None, None, None], oks2)
+    assert all(np.array_equal(a, b) for a, b in zip(oks2, want_ok))
+    cv.cvsr_session_destroy(sess)
+    for h in hs:
+        if h:
+            cv.cvsr_code_free(h)
