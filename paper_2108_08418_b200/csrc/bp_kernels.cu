@@ -1072,6 +1072,11 @@ __global__ void __launch_bounds__(1024) k_compact_plan(DecState src, DecState ds
 }
 
 // dst[t'][row][lane][s] = src[slot dst_src(t', s, lane)] for float rows (messages, LLRs)
+// A warp moves CR consecutive rows of destination tile t; the slot map of its lanes
+// (S source slots each) is loaded once and reused for every row.
+constexpr int CR_ROWS = 8;   // rows per warp, float rows
+constexpr int CB_ROWS = 32;  // rows per warp, bit rows
+
 template <int S>
 __global__ void __launch_bounds__(256) k_compact_rows(const float *__restrict__ src, float *__restrict__ dst,
                                                       int64_t rows, const int32_t *__restrict__ dst_src,
@@ -1079,19 +1084,27 @@ __global__ void __launch_bounds__(256) k_compact_rows(const float *__restrict__ 
     const int t = blockIdx.y;
     if (t >= counts[0]) return;
     const int lane = threadIdx.x & 31;
-    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (r >= rows) return;
-    FV<S> v;
+    const int64_t r0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * CR_ROWS;
+    if (r0 >= rows) return;
+    size_t base[S];  // source element offset of row 0 for each of this lane's S slots, or SIZE_MAX
 #pragma unroll
     for (int q = 0; q < S; ++q) {
         const int so = dst_src[t * LANES * S + q * LANES + lane];
-        v.c[q] = 0.0f;
+        base[q] = ~size_t(0);
         if (so >= 0) {
             const int st = so / (LANES * S), rem = so % (LANES * S);
-            v.c[q] = src[(((size_t)st * rows + r) * LANES + (rem % LANES)) * S + rem / LANES];
+            base[q] = ((size_t)st * rows * LANES + (rem % LANES)) * S + rem / LANES;
         }
     }
-    stv<S>(dst + (((size_t)t * rows + r) * LANES + lane) * S, v);
+    const int nr = (int)(rows - r0 < CR_ROWS ? rows - r0 : CR_ROWS);
+#pragma unroll 4
+    for (int i = 0; i < nr; ++i) {
+        const int64_t r = r0 + i;
+        FV<S> v;
+#pragma unroll
+        for (int q = 0; q < S; ++q) v.c[q] = base[q] != ~size_t(0) ? src[base[q] + (size_t)r * LANES * S] : 0.0f;
+        stv<S>(dst + (((size_t)t * rows + r) * LANES + lane) * S, v);
+    }
 }
 
 // dst[t'][row] bit (s, lane) = src bit of slot dst_src(t', s, lane) for uint4 bit rows (st, hb)
@@ -1101,19 +1114,25 @@ __global__ void __launch_bounds__(256) k_compact_bits(const uint4 *__restrict__ 
     const int t = blockIdx.y;
     if (t >= counts[0]) return;
     const int lane = threadIdx.x & 31;
-    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (r >= rows) return;
-    uint32_t w[SUBS] = {0u, 0u, 0u, 0u};
+    const int64_t r0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * CB_ROWS;
+    if (r0 >= rows) return;
+    int st_[SUBS], word[SUBS], bit[SUBS];
     for (int q = 0; q < subs; ++q) {
         const int so = dst_src[t * LANES * subs + q * LANES + lane];
-        uint32_t b = 0u;
-        if (so >= 0) {
-            const int st = so / (LANES * subs), rem = so % (LANES * subs);
-            b = (cmpu(src[(size_t)st * rows + r], rem / LANES) >> (rem % LANES)) & 1u;
-        }
-        w[q] = __ballot_sync(FULL, b);
+        st_[q] = so >= 0 ? so / (LANES * subs) : -1;
+        word[q] = so >= 0 ? (so % (LANES * subs)) / LANES : 0;
+        bit[q] = so >= 0 ? so % LANES : 0;
     }
-    if (lane == 0) dst[(size_t)t * rows + r] = make_uint4(w[0], w[1], w[2], w[3]);
+    const int nr = (int)(rows - r0 < CB_ROWS ? rows - r0 : CB_ROWS);
+    for (int i = 0; i < nr; ++i) {
+        const int64_t r = r0 + i;
+        uint32_t w[SUBS] = {0u, 0u, 0u, 0u};
+        for (int q = 0; q < subs; ++q) {
+            const uint32_t b = st_[q] >= 0 ? (cmpu(src[(size_t)st_[q] * rows + r], word[q]) >> bit[q]) & 1u : 0u;
+            w[q] = __ballot_sync(FULL, b);
+        }
+        if (lane == 0) dst[(size_t)t * rows + r] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
 }
 
 // ---------------------------------------------------------------- launchers
@@ -1344,8 +1363,9 @@ void launch_init_tiles(const DecState &ds, const uint8_t *alive, cudaStream_t s)
 int launch_compact(const CodeDev &cd, const DecState &src, const DecState &dst, int32_t *dst_src, int max_tiles,
                    int32_t *host_counts, cudaStream_t s) {
     k_compact_plan<<<1, 1024, 0, s>>>(src, dst, dst_src, host_counts);
-    const dim3 gE((unsigned)((cd.E + 7) / 8), max_tiles), gN((unsigned)((cd.n + 7) / 8), max_tiles),
-        gM((unsigned)((cd.M + 7) / 8), max_tiles);
+    const int64_t fr = 8 * CR_ROWS, br = 8 * CB_ROWS;  // rows per block
+    const dim3 gE((unsigned)((cd.E + fr - 1) / fr), max_tiles), gN((unsigned)((cd.n + fr - 1) / fr), max_tiles),
+        gNb((unsigned)((cd.n + br - 1) / br), max_tiles), gM((unsigned)((cd.M + br - 1) / br), max_tiles);
     if (src.subs == 4) {
         k_compact_rows<4><<<gE, 256, 0, s>>>(src.msg, dst.msg, cd.E, dst_src, dst.counts);
         k_compact_rows<4><<<gN, 256, 0, s>>>(src.L, dst.L, cd.n, dst_src, dst.counts);
@@ -1357,7 +1377,7 @@ int launch_compact(const CodeDev &cd, const DecState &src, const DecState &dst, 
         k_compact_rows<1><<<gN, 256, 0, s>>>(src.L, dst.L, cd.n, dst_src, dst.counts);
     }
     k_compact_bits<<<gM, 256, 0, s>>>(src.st, dst.st, cd.M, src.subs, dst_src, dst.counts);
-    k_compact_bits<<<gN, 256, 0, s>>>(src.hb, dst.hb, cd.n, src.subs, dst_src, dst.counts);
+    k_compact_bits<<<gNb, 256, 0, s>>>(src.hb, dst.hb, cd.n, src.subs, dst_src, dst.counts);
     return 6;
 }
 
