@@ -46,18 +46,35 @@ __global__ void k_quantise(QEdges q, int m, const float *__restrict__ y, int64_t
     }
 }
 
-// S_j packed: warp per (frame, 32-var word)
-__global__ void __launch_bounds__(BLOCK) k_slice_bits(const uint8_t *__restrict__ label, int32_t n, int32_t j,
-                                                       uint32_t *__restrict__ bits) {
-    const int f = blockIdx.y;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// bit j of each byte of x, as a nibble (byte 0 -> bit 0): the four bits land in
+// bits 28..31 of the product without carries (movemask by multiplication)
+__device__ __forceinline__ uint32_t byte_bits(uint32_t x, int j) {
+    return (((x >> j) & 0x01010101u) * 0x10204080u) >> 28;
+}
+
+// S_j packed: thread per (frame, 32-var word); 32 label bytes in, one word out
+__global__ void __launch_bounds__(BLOCK) k_slice_bits(const uint8_t *__restrict__ label, int32_t F, int32_t n,
+                                                       int32_t j, uint32_t *__restrict__ bits) {
     const int Wn = words_of(n);
-    const int w = blockIdx.x * WARPS_PER_BLOCK + warp;
-    if (w >= Wn) return;
-    const int v = w * 32 + lane;
-    const uint32_t b = (v < n) ? (label[(size_t)f * n + v] >> j) & 1u : 0u;
-    const uint32_t word = __ballot_sync(FULLB, b);
-    if (lane == 0) bits[(size_t)f * Wn + w] = word;
+    const int64_t total = (int64_t)F * Wn;
+    const bool vec = (n & 31) == 0 && (reinterpret_cast<uintptr_t>(label) & 15) == 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = i / Wn;
+        const int w = (int)(i - f * Wn);
+        const uint8_t *lab = label + (size_t)f * n + (size_t)w * 32;
+        uint32_t word = 0u;
+        if (vec) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4 *>(lab));
+            const uint4 b = __ldg(reinterpret_cast<const uint4 *>(lab) + 1);
+            const uint32_t x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int k = 0; k < 8; ++k) word |= byte_bits(x[k], j) << (4 * k);
+        } else {
+            const int cnt = min(32, n - w * 32);
+            for (int k = 0; k < cnt; ++k) word |= (uint32_t)((lab[k] >> j) & 1u) << k;
+        }
+        bits[i] = word;
+    }
 }
 
 // K2: s_j[c] = XOR_{v in row c} bit_j(label[v]); warp per (frame, 32-check word), lane = check
@@ -103,6 +120,43 @@ __global__ void __launch_bounds__(BLOCK) k_syndrome_bits(CodeDev cd, const uint3
     if (lane == 0) synd[(size_t)f * Wm + w] = word;
 }
 
+// Same, FB frames per block: their packed rows are staged in shared memory and each
+// check's column indices are read once for all FB frames (the code structure is the
+// same for every frame, so per-frame re-reads of col_idx were the dominant traffic).
+template <int FB>
+__global__ void __launch_bounds__(BLOCK) k_syndrome_bits_smem(CodeDev cd, const uint32_t *__restrict__ bits,
+                                                               int32_t F, uint32_t *__restrict__ synd) {
+    extern __shared__ uint32_t srow[];  // [FB][Wn]
+    const int Wm = words_of(cd.M), Wn = words_of(cd.n);
+    const int f0 = blockIdx.x * FB;
+    const int nf = min(FB, F - f0);
+    for (int i = threadIdx.x; i < FB * Wn; i += blockDim.x) {
+        const int k = i / Wn;
+        srow[i] = k < nf ? bits[(size_t)(f0 + k) * Wn + (i - k * Wn)] : 0u;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (int w = threadIdx.x >> 5; w < Wm; w += WARPS_PER_BLOCK) {
+        const int c = w * 32 + lane;
+        uint32_t par[FB];
+#pragma unroll
+        for (int k = 0; k < FB; ++k) par[k] = 0u;
+        if (c < cd.M) {
+            const int beg = cd.row_ptr[c], end = cd.row_ptr[c + 1];
+            for (int e = beg; e < end; ++e) {
+                const int v = cd.col_idx[e];
+#pragma unroll
+                for (int k = 0; k < FB; ++k) par[k] ^= srow[k * Wn + (v >> 5)] >> (v & 31);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < FB; ++k) {
+            const uint32_t word = __ballot_sync(FULLB, par[k] & 1u);
+            if (lane == 0 && k < nf) synd[(size_t)(f0 + k) * Wm + w] = word;
+        }
+    }
+}
+
 // simulation check: counts {ok frames, ok frames with any label mismatch, mismatching bytes}
 __global__ void k_count_errors(const uint8_t *__restrict__ a, const uint8_t *__restrict__ b,
                                const uint8_t *__restrict__ ok, int32_t n, unsigned long long *counts) {
@@ -146,17 +200,37 @@ struct BitPtrs {
     const uint32_t *p[8];
 };
 
-__global__ void k_assemble(BitPtrs bits, int32_t m, const uint8_t *__restrict__ attempt, int32_t n,
-                           uint8_t *__restrict__ label_out) {
-    const int f = blockIdx.y;
-    const int v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
+// bit k of w spread to byte k of the result for k = 0..3 (inverse of byte_bits)
+__device__ __forceinline__ uint32_t spread_nibble(uint32_t nib) {
+    return (nib * 0x00204081u) & 0x01010101u;
+}
+
+// thread per (frame, 32-symbol word): m packed words in, 32 label bytes out
+__global__ void __launch_bounds__(256) k_assemble(BitPtrs bits, int32_t m, const uint8_t *__restrict__ attempt,
+                                                  int32_t F, int32_t n, uint8_t *__restrict__ label_out) {
     const int Wn = words_of(n);
-    const uint32_t am = attempt[f];
-    uint32_t lab = 0u;
-    for (int j = 0; j < m; ++j)
-        if ((am >> j) & 1u) lab |= ((bits.p[j][(size_t)f * Wn + (v >> 5)] >> (v & 31)) & 1u) << j;
-    label_out[(size_t)f * n + v] = (uint8_t)lab;
+    const int64_t total = (int64_t)F * Wn;
+    const bool vec = (n & 31) == 0 && (reinterpret_cast<uintptr_t>(label_out) & 15) == 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = i / Wn;
+        const int w = (int)(i - f * Wn);
+        const uint32_t am = attempt[f];
+        uint32_t out[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        for (int j = 0; j < m; ++j) {
+            if (!((am >> j) & 1u)) continue;
+            const uint32_t word = bits.p[j][i];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) out[k] |= spread_nibble((word >> (4 * k)) & 0xFu) << j;
+        }
+        uint8_t *dst = label_out + (size_t)f * n + (size_t)w * 32;
+        if (vec) {
+            reinterpret_cast<uint4 *>(dst)[0] = make_uint4(out[0], out[1], out[2], out[3]);
+            reinterpret_cast<uint4 *>(dst)[1] = make_uint4(out[4], out[5], out[6], out[7]);
+        } else {
+            const int cnt = min(32, n - w * 32);
+            for (int k = 0; k < cnt; ++k) dst[k] = (uint8_t)(out[k >> 2] >> (8 * (k & 3)));
+        }
+    }
 }
 
 __global__ void k_fill_i32(int32_t *p, int64_t count, int32_t v) {
@@ -199,8 +273,7 @@ void launch_quantise(const float *edges_host, int m, const float *y, int64_t cou
 }
 
 void launch_slice_bits(const uint8_t *label, int32_t F, int32_t n, int32_t j, uint32_t *bits, cudaStream_t s) {
-    dim3 grid((words_of(n) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, F);
-    k_slice_bits<<<grid, BLOCK, 0, s>>>(label, n, j, bits);
+    k_slice_bits<<<grid_for((int64_t)F * words_of(n), BLOCK), BLOCK, 0, s>>>(label, F, n, j, bits);
 }
 
 void launch_syndrome(const CodeDev &cd, const uint8_t *label, int32_t F, int32_t j, uint32_t *synd, cudaStream_t s) {
@@ -209,8 +282,21 @@ void launch_syndrome(const CodeDev &cd, const uint8_t *label, int32_t F, int32_t
 }
 
 void launch_syndrome_bits(const CodeDev &cd, const uint32_t *bits, int32_t F, uint32_t *synd, cudaStream_t s) {
-    dim3 grid((words_of(cd.M) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, F);
-    k_syndrome_bits<<<grid, BLOCK, 0, s>>>(cd, bits, synd);
+    // stage FB frames' rows in shared memory when they fit (<= 96 KB per block) and the
+    // batch still fills the GPU with blocks; otherwise the per-frame kernel
+    const size_t row = (size_t)words_of(cd.n) * 4;
+    auto smem_launch = [&](auto kern, int fb) {
+        const size_t bytes = row * fb;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        kern<<<(F + fb - 1) / fb, BLOCK, bytes, s>>>(cd, bits, F, synd);
+    };
+    if (row * 8 <= 96 * 1024 && F >= 8 * 148) smem_launch(k_syndrome_bits_smem<8>, 8);
+    else if (row * 4 <= 96 * 1024 && F >= 4 * 148) smem_launch(k_syndrome_bits_smem<4>, 4);
+    else if (row * 2 <= 96 * 1024 && F >= 2 * 148) smem_launch(k_syndrome_bits_smem<2>, 2);
+    else {
+        dim3 grid((words_of(cd.M) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, F);
+        k_syndrome_bits<<<grid, BLOCK, 0, s>>>(cd, bits, synd);
+    }
 }
 
 void launch_count_errors(const uint8_t *a, const uint8_t *b, const uint8_t *ok, int32_t F, int32_t n,
@@ -227,8 +313,7 @@ void launch_assemble(const uint32_t *const *bits, int32_t m, const uint8_t *atte
                      uint8_t *label_out, cudaStream_t s) {
     BitPtrs bp;
     for (int j = 0; j < 8; ++j) bp.p[j] = (j < m) ? bits[j] : nullptr;
-    dim3 grid((n + 255) / 256, F);
-    k_assemble<<<grid, 256, 0, s>>>(bp, m, attempt, n, label_out);
+    k_assemble<<<grid_for((int64_t)F * words_of(n), 256), 256, 0, s>>>(bp, m, attempt, F, n, label_out);
 }
 
 void launch_fill_i32(int32_t *p, int64_t count, int32_t v, cudaStream_t s) {

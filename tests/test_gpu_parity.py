@@ -105,11 +105,13 @@ CODES = {
 }
 
 
-@pytest.mark.parametrize("name", list(CODES))
-def test_slice_bits_and_syndrome_bitexact(cv, ctx, name):
+@pytest.mark.parametrize("name,F", [(k, 37) for k in CODES] + [("c1_36", 300), ("c1_36", 600), ("c1_36", 1200),
+                                                                  ("irreg_ragged", 1201)])
+def test_slice_bits_and_syndrome_bitexact(cv, ctx, name, F):
+    """Bit-exact vs the oracle; F = 300 / 600 / 1200 take the shared-memory syndrome kernel with
+    2 / 4 / 8 frames per block (1201: a ragged last block), n = 4100 the unaligned pack path."""
     code = CODES[name]()
     rng = np.random.default_rng(17)
-    F = 37
     lab = rng.integers(0, 256, (F, code.n), dtype=np.uint8)
     h = load(cv, ctx, code)
     ld = dev(lab)
