@@ -15,6 +15,8 @@ Parity-pin status per function:
                                      noiseless limit; MC posterior of the LLR feed)
   verify.frame_hash               -- pinned (key = 1 word checksum, key = 2^32 shifted
                                      integer, zero string, bit-flip detection)
+  pa.toeplitz_hash                -- pinned (numpy convolution window, unit / all-ones
+                                     seeds, linearity, 2-universality statistics)
 """
 from .oracle import (  # noqa: F401
     build, bp_decode, bp_trace, llr_biawgn, llr_slice, quantise, reconcile, slice_bits,

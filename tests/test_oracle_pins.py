@@ -369,3 +369,50 @@ def test_hash_zero_and_collision_bound():
         assert verify.frame_hash(lab, key)[0] != verify.frame_hash(other, key)[0]
     with pytest.raises(ValueError):
         verify.frame_hash(lab, 0)
+
+
+# ----------------------------------------------------------------- Toeplitz privacy amplification (R-8)
+def test_pa_equals_numpy_convolution_window():
+    """y_i = (t * x)[n_in - 1 + i] mod 2: the window of numpy's integer convolution."""
+    from oracle import pa
+    rng = np.random.default_rng(21)
+    for n_in, n_out in ((1, 1), (7, 3), (64, 64), (100, 37), (513, 200)):
+        t = rng.integers(0, 2, n_in + n_out - 1, dtype=np.uint8)
+        x = rng.integers(0, 2, n_in, dtype=np.uint8)
+        conv = np.convolve(t.astype(np.int64), x.astype(np.int64))
+        assert np.array_equal(pa.toeplitz_hash(t, x, n_out), (conv[n_in - 1: n_in - 1 + n_out] & 1).astype(np.uint8))
+
+
+def test_pa_special_seeds_and_linearity():
+    """Unit seed at n_in - 1 + s is a shift (y_i = x_{i-s}); the all-ones seed gives the parity of x
+    in every output; y is linear in x and in t."""
+    from oracle import pa
+    rng = np.random.default_rng(22)
+    n_in, n_out = 50, 20
+    x = rng.integers(0, 2, n_in, dtype=np.uint8)
+    for s in (0, 3, 19):
+        t = np.zeros(n_in + n_out - 1, np.uint8)
+        t[n_in - 1 + s] = 1
+        want = np.array([x[i - s] if 0 <= i - s < n_in else 0 for i in range(n_out)], np.uint8)
+        assert np.array_equal(pa.toeplitz_hash(t, x, n_out), want)
+    assert np.all(pa.toeplitz_hash(np.ones(n_in + n_out - 1, np.uint8), x, n_out) == x.sum() % 2)
+    t1, t2 = (rng.integers(0, 2, n_in + n_out - 1, dtype=np.uint8) for _ in range(2))
+    x2 = rng.integers(0, 2, n_in, dtype=np.uint8)
+    assert np.array_equal(pa.toeplitz_hash(t1, x ^ x2, n_out), pa.toeplitz_hash(t1, x, n_out) ^ pa.toeplitz_hash(t1, x2, n_out))
+    assert np.array_equal(pa.toeplitz_hash(t1 ^ t2, x, n_out), pa.toeplitz_hash(t1, x, n_out) ^ pa.toeplitz_hash(t2, x, n_out))
+    w = pa.pack_bits(x)
+    assert np.array_equal(pa.unpack_bits(w, n_in), x) and w.dtype == np.dtype("<u4")
+
+
+def test_pa_two_universal():
+    """2-universality: for a fixed x != 0 and a uniform seed, P(T x = 0) = 2^-n_out."""
+    from oracle import pa
+    from scipy import stats as st
+    rng = np.random.default_rng(23)
+    n_in, n_out, trials = 40, 3, 4000
+    x = rng.integers(0, 2, n_in, dtype=np.uint8)
+    x[5] = 1
+    zeros = sum(not pa.toeplitz_hash(rng.integers(0, 2, n_in + n_out - 1, dtype=np.uint8), x, n_out).any()
+                for _ in range(trials))
+    ci = st.binomtest(zeros, trials).proportion_ci(0.999)
+    assert ci.low <= 1 / 8 <= ci.high
