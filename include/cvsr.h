@@ -221,6 +221,27 @@ cvsr_status cvsr_verify(cvsr_ctx *ctx, const uint8_t *label_alice, const uint8_t
                         int32_t frames, int32_t n, uint64_t key, uint8_t *verified_out, uint64_t *hash_alice_out,
                         uint64_t *hash_bob_out);
 
+/* ------------------------------------------------------------ privacy amplification
+ * Toeplitz hashing (Step 6: "apply a 2-universal hashing function on
+ * their reconciled string"; reading R-8 of DESIGN.md): the n_in + n_out - 1 seed
+ * bits t define T in {0,1}^{n_out x n_in}, T[i][j] = t[i - j + n_in - 1], and
+ * y = T x over GF(2).  Computed exactly as the window [n_in - 1, n_in + n_out - 2]
+ * of the integer convolution t * x by a number-theoretic transform modulo
+ * 15 * 2^27 + 1 of size N = 2^ceil(log2(n_in + n_out - 1)).
+ * Bit strings are packed LSB first: bit i at bit (i % 32) of uint32 word i / 32.
+ * Limits: 1 <= n_out <= n_in, n_in + n_out - 1 <= 2^27.  The plan owns 16 N bytes
+ * of device memory (twiddles, the seed's transform, one work array) on the
+ * context's device; one plan serves one stream at a time. */
+typedef struct cvsr_pa_plan cvsr_pa_plan;
+cvsr_status cvsr_pa_plan_create(cvsr_ctx *ctx, int64_t n_in, int64_t n_out, const uint32_t *seed_bits_host,
+                                cvsr_pa_plan **out);
+cvsr_status cvsr_pa_plan_info(const cvsr_pa_plan *p, int64_t *n_in, int64_t *n_out, int64_t *ntt_size);
+/* x_bits: device uint32[blocks][ceil(n_in/32)]; y_bits: device uint32[blocks][ceil(n_out/32)]
+ * (bits past n_out in the last word are 0).  Every block is hashed with the plan's seed. */
+cvsr_status cvsr_pa_hash(cvsr_ctx *ctx, const cvsr_pa_plan *p, int32_t blocks, const uint32_t *x_bits,
+                         uint32_t *y_bits);
+void cvsr_pa_plan_free(cvsr_pa_plan *p);
+
 /* Simulation-only check against Bob's labels (both uint8[frames][n]):
  * counts_out HOST int64[3] = {frames ok, ok frames whose labels differ from
  * Bob's (undetected errors), differing label bytes over ok frames}.  Syncs. */

@@ -387,6 +387,8 @@ cvsr_status check_quantiser(const cvsr_quantiser *q) {
 // internal accessors for session.cu (not part of the ABI)
 cudaStream_t cvsr_internal_ctx_stream(cvsr_ctx *ctx) { return ctx->stream; }
 cvsr_status cvsr_internal_fail(cvsr_status st, const char *msg) { return fail(st, "%s", msg); }
+cvsr_status cvsr_internal_launched(cvsr_ctx *ctx, int n) { return check_launch(ctx, n); }
+int cvsr_internal_ctx_device(cvsr_ctx *ctx) { return ctx->device; }
 
 // =================================================================== ABI
 

@@ -84,6 +84,10 @@ _SIGS = {
     "cvsr_frame_hash": ([_vp, _vp, _i32, _i32, ctypes.c_uint64, _vp], _i32),
     "cvsr_session_set_verify": ([_vp, ctypes.c_uint64], _i32),
     "cvsr_session_run_host_stream": ([_vp, _i32, _vp, _vp, _vp, _vp], _i32),
+    "cvsr_pa_plan_create": ([_vp, _i64, _i64, _vp, _P(_vp)], _i32),
+    "cvsr_pa_plan_info": ([_vp, _P(_i64), _P(_i64), _P(_i64)], _i32),
+    "cvsr_pa_hash": ([_vp, _vp, _i32, _vp, _vp], _i32),
+    "cvsr_pa_plan_free": ([_vp], None),
     "cvsr_verify": ([_vp, _vp, _vp, _vp, _i32, _i32, ctypes.c_uint64, _vp, _vp, _vp], _i32),
     "cvsr_session_create": ([_vp, _i32, _P(_vp), _P(_i32), _P(cvsr_quantiser), _f32, _i32, _i32,
                              _P(cvsr_decode_opts), _P(_vp)], _i32),
@@ -268,6 +272,31 @@ def cvsr_session_run_host_stream(sess: int, x_hosts, y_hosts, label_hosts, frame
     arr = lambda lst: (ctypes.c_void_p * max(1, nb))(*[hp(a) for a in lst])  # noqa: E731
     _call("cvsr_session_run_host_stream", sess, nb, arr(x_hosts), arr(y_hosts), arr(label_hosts),
           arr(frame_ok_hosts))
+
+
+def cvsr_pa_plan_create(ctx: int, n_in: int, n_out: int, seed_bits) -> int:
+    """seed_bits: host uint32 words (numpy), n_in + n_out - 1 bits LSB first."""
+    import numpy as np
+    seed = np.ascontiguousarray(seed_bits, dtype=np.uint32)
+    if seed.size * 32 < n_in + n_out - 1:
+        raise ValueError("seed too short")
+    out = ctypes.c_void_p()
+    _call("cvsr_pa_plan_create", ctx, n_in, n_out, seed.ctypes.data, ctypes.byref(out))
+    return out.value
+
+
+def cvsr_pa_plan_info(plan: int):
+    a, b, c = _i64(), _i64(), _i64()
+    _call("cvsr_pa_plan_info", plan, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
+    return a.value, b.value, c.value
+
+
+def cvsr_pa_hash(ctx: int, plan: int, blocks: int, x_bits, y_bits) -> None:
+    _call("cvsr_pa_hash", ctx, plan, blocks, _ptr(x_bits), _ptr(y_bits))
+
+
+def cvsr_pa_plan_free(plan: int) -> None:
+    _lib.cvsr_pa_plan_free(plan)
 
 
 def cvsr_session_set_verify(sess: int, key: int) -> None:

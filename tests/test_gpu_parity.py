@@ -557,3 +557,42 @@ def test_session_stream_matches_run_host(cv, ctx):
     for h in hs:
         if h:
             cv.cvsr_code_free(h)
+
+
+# ----------------------------------------------------------------- Toeplitz privacy amplification (R-8)
+@pytest.mark.parametrize("n_in,n_out,blocks,sample", [(1, 1, 2, None), (5, 3, 3, None), (100, 37, 2, None),
+                                                      (4096, 1000, 2, None), (5000, 4999, 1, None),
+                                                      (20000, 7000, 3, None), (1 << 16, 1 << 15, 2, 300),
+                                                      ((1 << 20) + 3, 777_777, 1, 64)])
+def test_pa_toeplitz_bitexact(cv, ctx, n_in, n_out, blocks, sample):
+    """cvsr_pa_hash equals the oracle's row-by-row Toeplitz product bit for bit (all rows, or
+    `sample` random rows at the larger sizes); sizes cover N = 2 .. 2^21 (shared-memory-only
+    transforms and 1-4-stage global passes) and ragged bit counts."""
+    from oracle import pa
+    rng = np.random.default_rng(n_in + n_out)
+    t = rng.integers(0, 2, n_in + n_out - 1, dtype=np.uint8)
+    plan = cv.cvsr_pa_plan_create(ctx, n_in, n_out, pa.pack_bits(t))
+    assert cv.cvsr_pa_plan_info(plan)[:2] == (n_in, n_out)
+    xs = [rng.integers(0, 2, n_in, dtype=np.uint8) for _ in range(blocks)]
+    xd = dev(np.stack([pa.pack_bits(x) for x in xs]))
+    wo = (n_out + 31) // 32
+    yd = torch.empty((blocks, wo), dtype=torch.int32, device="cuda")
+    cv.cvsr_pa_hash(ctx, plan, blocks, xd, yd)
+    yh = host_u32(yd)
+    for b in range(blocks):
+        got = pa.unpack_bits(yh[b], n_out)
+        if sample is None:
+            assert np.array_equal(got, pa.toeplitz_hash(t, xs[b], n_out))
+            assert (n_out % 32 == 0) or (yh[b][-1] >> (n_out % 32)) == 0
+        else:
+            rows = np.sort(rng.choice(n_out, size=sample, replace=False))
+            rows = np.unique(np.concatenate([rows, [0, n_out - 1]]))
+            assert np.array_equal(got[rows], pa.toeplitz_hash(t, xs[b], n_out, rows=rows))
+    cv.cvsr_pa_plan_free(plan)
+
+
+def test_pa_errors(cv, ctx):
+    with pytest.raises(cv.CvsrError):
+        cv.cvsr_pa_plan_create(ctx, 10, 11, np.zeros(1, np.uint32))     # n_out > n_in
+    with pytest.raises(cv.CvsrError):
+        cv.cvsr_pa_plan_create(ctx, 1 << 27, 2, np.zeros((1 << 22) + 1, np.uint32))  # > 2^27
