@@ -44,6 +44,12 @@ __host__ __device__ __forceinline__ uint32_t mont_mul(uint32_t a, uint32_t b) {
     const uint32_t u = (uint32_t)((t + (uint64_t)m * P) >> 32);
     return u >= P ? u - P : u;
 }
+// a w mod P for a fixed w with wq = floor(w 2^32 / P) (Shoup): 3 32-bit multiplies, no 64-bit product
+__device__ __forceinline__ uint32_t mul_shoup(uint32_t a, uint32_t w, uint32_t wq) {
+    const uint32_t q = __umulhi(a, wq);
+    const uint32_t r = a * w - q * P;
+    return r >= P ? r - P : r;
+}
 __device__ __forceinline__ uint32_t addp(uint32_t a, uint32_t b) {
     const uint32_t r = a + b;
     return r >= P ? r - P : r;
@@ -63,15 +69,21 @@ __host__ __device__ inline uint32_t powmod(uint32_t b, uint64_t e) {
 __host__ __device__ inline uint32_t to_mont(uint32_t a) { return (uint32_t)(((uint64_t)a << 32) % P); }
 
 // twiddles: T[h - 1 + j] = w_2h^(+-j) in Montgomery form, h = 1, 2, ..., N/2, j < h
-__global__ void k_twiddles(uint32_t *__restrict__ tw, uint32_t *__restrict__ twi, int64_t N) {
+__global__ void k_twiddles(uint32_t *__restrict__ tw, uint32_t *__restrict__ twi, uint2 *__restrict__ sh,
+                           uint2 *__restrict__ shi, int64_t N) {
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < N - 1;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int lg = 63 - __clzll((unsigned long long)(idx + 1));  // h = 2^lg <= idx + 1 < 2h
         const int64_t h = 1LL << lg, j = idx - (h - 1);
         const uint64_t step = (uint64_t)(P - 1) / (uint64_t)(2 * h);  // w_2h = G^step
         const uint64_t e = (step * (uint64_t)j) % (P - 1);
-        tw[idx] = to_mont(powmod(G, e));
-        twi[idx] = to_mont(powmod(G, (P - 1 - e) % (P - 1)));
+        const uint32_t w = powmod(G, e), wi = powmod(G, (P - 1 - e) % (P - 1));
+        tw[idx] = to_mont(w);
+        twi[idx] = to_mont(wi);
+        if (idx < (1 << MID_LOG)) {  // the shared-memory stages use Shoup pairs (w, floor(w 2^32 / P))
+            sh[idx] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / P));
+            shi[idx] = make_uint2(wi, (uint32_t)(((uint64_t)wi << 32) / P));
+        }
     }
 }
 
@@ -142,8 +154,8 @@ __global__ void __launch_bounds__(256) k_dit_pass(uint32_t *__restrict__ a, cons
 // the lowest lb stages of the forward DIF of a block of B = 2^lb contiguous values, then
 // (tm != null) the pointwise product with the seed transform and the lowest lb stages of
 // the inverse DIT, in shared memory
-__global__ void __launch_bounds__(512) k_ntt_mid(uint32_t *__restrict__ a, const uint32_t *__restrict__ tw,
-                                                 const uint32_t *__restrict__ twi, const uint32_t *__restrict__ tm,
+__global__ void __launch_bounds__(512) k_ntt_mid(uint32_t *__restrict__ a, const uint2 *__restrict__ tw,
+                                                 const uint2 *__restrict__ twi, const uint32_t *__restrict__ tm,
                                                  int lb) {
     __shared__ uint32_t s[1 << MID_LOG];
     const int B = 1 << lb;
@@ -155,8 +167,9 @@ __global__ void __launch_bounds__(512) k_ntt_mid(uint32_t *__restrict__ a, const
         for (int b = threadIdx.x; b < B / 2; b += blockDim.x) {
             const int j = b & (h - 1), i = ((b >> st) << (st + 1)) + j;
             const uint32_t x = s[i], y = s[i + h];
+            const uint2 w = __ldg(tw + h - 1 + j);
             s[i] = addp(x, y);
-            s[i + h] = mont_mul(subp(x, y), __ldg(tw + h - 1 + j));
+            s[i + h] = mul_shoup(subp(x, y), w.x, w.y);
         }
         __syncthreads();
     }
@@ -168,7 +181,8 @@ __global__ void __launch_bounds__(512) k_ntt_mid(uint32_t *__restrict__ a, const
             const int h = 1 << st;
             for (int b = threadIdx.x; b < B / 2; b += blockDim.x) {
                 const int j = b & (h - 1), i = ((b >> st) << (st + 1)) + j;
-                const uint32_t x = s[i], y = mont_mul(s[i + h], __ldg(twi + h - 1 + j));
+                const uint2 w = __ldg(twi + h - 1 + j);
+                const uint32_t x = s[i], y = mul_shoup(s[i + h], w.x, w.y);
                 s[i] = addp(x, y);
                 s[i + h] = subp(x, y);
             }
@@ -176,6 +190,77 @@ __global__ void __launch_bounds__(512) k_ntt_mid(uint32_t *__restrict__ a, const
         }
     }
     for (int i = threadIdx.x; i < B; i += blockDim.x) blk[i] = s[i];
+}
+
+// Specialisation for full 4096-value blocks (lb = MID_LOG = 12): 512 threads own 8 values
+// each; the 12 stages per direction run as 4 radix-8 steps entirely in registers
+// (compile-time indices, 12 butterflies per thread and step, one barrier per step).
+// Shared memory is padded by one word per 32 (conflict-free except 2-way in one step).
+__device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
+
+template <int S0, bool FWD>
+__device__ __forceinline__ void mid8(uint32_t *s, const uint2 *__restrict__ tab, int g) {
+    constexpr int d = 1 << S0;
+    const int off = g & (d - 1), base = ((g >> S0) << (S0 + 3)) + off;
+    uint32_t v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = s[pad32(base + q * d)];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int sh = FWD ? 2 - k : k;
+        const int h = d << sh;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (q & (1 << sh)) continue;
+            const uint2 w = __ldg(tab + h - 1 + off + (q & ((1 << sh) - 1)) * d);
+            const uint32_t x = v[q];
+            if (FWD) {
+                const uint32_t y = v[q + (1 << sh)];
+                v[q] = addp(x, y);
+                v[q + (1 << sh)] = mul_shoup(subp(x, y), w.x, w.y);
+            } else {
+                const uint32_t y = mul_shoup(v[q + (1 << sh)], w.x, w.y);
+                v[q] = addp(x, y);
+                v[q + (1 << sh)] = subp(x, y);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[pad32(base + q * d)] = v[q];
+}
+
+__global__ void __launch_bounds__(512) k_ntt_mid12(uint32_t *__restrict__ a, const uint2 *__restrict__ tw,
+                                                   const uint2 *__restrict__ twi, const uint32_t *__restrict__ tm) {
+    __shared__ uint32_t s[4096 + 128];
+    uint32_t *blk = a + (int64_t)blockIdx.x * 4096;
+    const int g = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s[pad32(g + 512 * k)] = blk[g + 512 * k];
+    __syncthreads();
+    mid8<9, true>(s, tw, g);
+    __syncthreads();
+    mid8<6, true>(s, tw, g);
+    __syncthreads();
+    mid8<3, true>(s, tw, g);
+    __syncthreads();
+    mid8<0, true>(s, tw, g);
+    __syncthreads();
+    if (tm) {
+        const uint32_t *tb = tm + (int64_t)blockIdx.x * 4096;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s[pad32(g + 512 * k)] = mont_mul(s[pad32(g + 512 * k)], __ldg(tb + g + 512 * k));
+        __syncthreads();
+        mid8<0, false>(s, twi, g);
+        __syncthreads();
+        mid8<3, false>(s, twi, g);
+        __syncthreads();
+        mid8<6, false>(s, twi, g);
+        __syncthreads();
+        mid8<9, false>(s, twi, g);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) blk[g + 512 * k] = s[pad32(g + 512 * k)];
 }
 
 __global__ void k_to_mont(uint32_t *__restrict__ a, int64_t N) {
@@ -219,7 +304,8 @@ static void launch_radix(K k1, K k2, K k3, K k4, int rb, uint32_t *a, const uint
 // forward DIF of a (natural in, bit-reversed out) when tm == null; with tm: forward,
 // pointwise product with tm (Montgomery form, bit-reversed) and inverse DIT (natural out,
 // scaled by N).  Returns the number of kernel launches.
-static int ntt_run(uint32_t *a, const uint32_t *tw, const uint32_t *twi, const uint32_t *tm, int lg, cudaStream_t st) {
+static int ntt_run(uint32_t *a, const uint32_t *tw, const uint32_t *twi, const uint2 *sh, const uint2 *shi,
+                   const uint32_t *tm, int lg, cudaStream_t st) {
     const int64_t N = 1LL << lg;
     const int lb = lg < MID_LOG ? lg : MID_LOG;
     int launches = 0;
@@ -229,7 +315,8 @@ static int ntt_run(uint32_t *a, const uint32_t *tw, const uint32_t *twi, const u
         ++launches;
         s_hi -= rb;
     }
-    k_ntt_mid<<<(unsigned)(N >> lb), 512, 0, st>>>(a, tw, twi, tm, lb);
+    if (lb == MID_LOG) k_ntt_mid12<<<(unsigned)(N >> lb), 512, 0, st>>>(a, sh, shi, tm);
+    else k_ntt_mid<<<(unsigned)(N >> lb), 512, 0, st>>>(a, sh, shi, tm, lb);
     ++launches;
     if (!tm) return launches;
     for (int s_lo = lb; s_lo < lg;) {  // global DIT passes, lowest remaining stages first
@@ -252,6 +339,7 @@ struct cvsr_pa_plan {
     int64_t n_in = 0, n_out = 0, N = 0;
     uint32_t *mem = nullptr;
     uint32_t *tw = nullptr, *twi = nullptr, *tm = nullptr, *work = nullptr;
+    uint2 *sh = nullptr, *shi = nullptr;  // Shoup pairs of the first 2^MID_LOG twiddles
 };
 
 cudaStream_t cvsr_internal_ctx_stream(cvsr_ctx *ctx);
@@ -277,7 +365,7 @@ cvsr_status cvsr_pa_plan_create(cvsr_ctx *ctx, int64_t n_in, int64_t n_out, cons
     p->n_out = n_out;
     p->N = 1LL << lg;
     const int64_t N = p->N;
-    if (cudaMalloc(&p->mem, (size_t)N * 4 * 4) != cudaSuccess) {
+    if (cudaMalloc(&p->mem, (size_t)N * 4 * 4 + 2 * (size_t)(1 << MID_LOG) * 8) != cudaSuccess) {
         cudaGetLastError();
         delete p;
         return cvsr_internal_fail(CVSR_ENOMEM, "pa: plan buffers");
@@ -286,6 +374,8 @@ cvsr_status cvsr_pa_plan_create(cvsr_ctx *ctx, int64_t n_in, int64_t n_out, cons
     p->twi = p->mem + N;
     p->tm = p->mem + 2 * N;
     p->work = p->mem + 3 * N;
+    p->sh = reinterpret_cast<uint2 *>(p->mem + 4 * N);
+    p->shi = p->sh + (1 << MID_LOG);
     cudaStream_t st = cvsr_internal_ctx_stream(ctx);
     const int64_t sw = (need + 31) / 32;
     uint32_t *seed_dev = nullptr;
@@ -297,10 +387,10 @@ cvsr_status cvsr_pa_plan_create(cvsr_ctx *ctx, int64_t n_in, int64_t n_out, cons
         return cvsr_internal_fail(CVSR_ECUDA, "pa: seed upload");
     }
     int launches = 0;
-    k_twiddles<<<grid_for(N - 1, 256), 256, 0, st>>>(p->tw, p->twi, N);
+    k_twiddles<<<grid_for(N - 1, 256), 256, 0, st>>>(p->tw, p->twi, p->sh, p->shi, N);
     ++launches;
     k_unpack<<<grid_for(N, 256), 256, 0, st>>>(seed_dev, need, p->tm, N);
-    launches += 1 + ntt_run(p->tm, p->tw, p->twi, nullptr, lg, st);
+    launches += 1 + ntt_run(p->tm, p->tw, p->twi, p->sh, p->shi, nullptr, lg, st);
     k_to_mont<<<grid_for(N, 256), 256, 0, st>>>(p->tm, N);
     ++launches;
     cudaFreeAsync(seed_dev, st);
@@ -334,7 +424,7 @@ cvsr_status cvsr_pa_hash(cvsr_ctx *ctx, const cvsr_pa_plan *p, int32_t blocks, c
     int launches = 0;
     for (int32_t b = 0; b < blocks; ++b) {
         k_unpack<<<grid_for(p->N, 256), 256, 0, st>>>(x_bits + b * wi, p->n_in, p->work, p->N);
-        launches += 1 + ntt_run(p->work, p->tw, p->twi, p->tm, p->lg, st);
+        launches += 1 + ntt_run(p->work, p->tw, p->twi, p->sh, p->shi, p->tm, p->lg, st);
         k_pack_window<<<grid_for(wo * 32, 256), 256, 0, st>>>(p->work, p->n_in, p->n_out, ninv, y_bits + b * wo);
         ++launches;
     }
