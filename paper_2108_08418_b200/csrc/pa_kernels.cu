@@ -93,10 +93,17 @@ __global__ void k_unpack(const uint32_t *__restrict__ bits, int64_t nbits, uint3
         a[i] = i < nbits ? (__ldg(bits + (i >> 5)) >> (i & 31)) & 1u : 0u;
 }
 
-// forward DIF stages s_hi .. s_hi - RB + 1 (half-size >= 2^MID_LOG), one thread per group
+// Twiddles of a radix-2^RB pass from ONE table load per thread: for the pass's top
+// stage (half-size H = d 2^(RB-1)) b = w_2H^off; stage sh (half-size h = d 2^sh) needs
+// w_2h^(off + q' d) = b^(2^(RB-1-sh)) * w_(2^(sh+1))^q', the second factor from the
+// tiny head of the table (index 2^sh - 1 + q').
+
+// forward DIF stages s_hi .. s_hi - RB + 1 (half-size >= 2^MID_LOG), one thread per group;
+// xbits != null: the input is the packed bit string (first pass), values 0/1
 template <int RB>
 __global__ void __launch_bounds__(256) k_dif_pass(uint32_t *__restrict__ a, const uint32_t *__restrict__ tw,
-                                                  int s_hi, int64_t N) {
+                                                  int s_hi, int64_t N, const uint32_t *__restrict__ xbits,
+                                                  int64_t nbits) {
     constexpr int Q = 1 << RB;
     const int S0 = s_hi - RB + 1;
     const int64_t d = 1LL << S0, groups = N >> RB;
@@ -104,28 +111,33 @@ __global__ void __launch_bounds__(256) k_dif_pass(uint32_t *__restrict__ a, cons
         const int64_t off = g & (d - 1), base = ((g >> S0) << (S0 + RB)) + off;
         uint32_t v[Q];
 #pragma unroll
-        for (int q = 0; q < Q; ++q) v[q] = a[base + q * d];
+        for (int q = 0; q < Q; ++q) {
+            const int64_t i = base + q * d;
+            v[q] = xbits ? (i < nbits ? (__ldg(xbits + (i >> 5)) >> (i & 31)) & 1u : 0u) : a[i];
+        }
+        uint32_t b = __ldg(tw + (d << (RB - 1)) - 1 + off);  // w_2H^off
 #pragma unroll
         for (int sh = RB - 1; sh >= 0; --sh) {
-            const int64_t h = d << sh;
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
                 if (q & (1 << sh)) continue;
-                const uint32_t w = __ldg(tw + h - 1 + off + (int64_t)(q & ((1 << sh) - 1)) * d);
+                const int qq = q & ((1 << sh) - 1);
+                const uint32_t w = qq ? mont_mul(b, __ldg(tw + (1 << sh) - 1 + qq)) : b;
                 const uint32_t x = v[q], y = v[q + (1 << sh)];
                 v[q] = addp(x, y);
                 v[q + (1 << sh)] = mont_mul(subp(x, y), w);
             }
+            b = mont_mul(b, b);
         }
 #pragma unroll
         for (int q = 0; q < Q; ++q) a[base + q * d] = v[q];
     }
 }
 
-// inverse DIT stages s_lo .. s_lo + RB - 1
+// inverse DIT stages s_lo .. s_lo + RB - 1 (inverse twiddle table, same derivation)
 template <int RB>
 __global__ void __launch_bounds__(256) k_dit_pass(uint32_t *__restrict__ a, const uint32_t *__restrict__ twi,
-                                                  int s_lo, int64_t N) {
+                                                  int s_lo, int64_t N, const uint32_t *__restrict__, int64_t) {
     constexpr int Q = 1 << RB;
     const int S0 = s_lo;
     const int64_t d = 1LL << S0, groups = N >> RB;
@@ -134,13 +146,17 @@ __global__ void __launch_bounds__(256) k_dit_pass(uint32_t *__restrict__ a, cons
         uint32_t v[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) v[q] = a[base + q * d];
+        uint32_t bs[RB];  // bs[sh] = w_2h^-off for stage sh
+        bs[RB - 1] = __ldg(twi + (d << (RB - 1)) - 1 + off);
+#pragma unroll
+        for (int sh = RB - 2; sh >= 0; --sh) bs[sh] = mont_mul(bs[sh + 1], bs[sh + 1]);
 #pragma unroll
         for (int sh = 0; sh < RB; ++sh) {
-            const int64_t h = d << sh;
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
                 if (q & (1 << sh)) continue;
-                const uint32_t w = __ldg(twi + h - 1 + off + (int64_t)(q & ((1 << sh) - 1)) * d);
+                const int qq = q & ((1 << sh) - 1);
+                const uint32_t w = qq ? mont_mul(bs[sh], __ldg(twi + (1 << sh) - 1 + qq)) : bs[sh];
                 const uint32_t x = v[q], y = mont_mul(v[q + (1 << sh)], w);
                 v[q] = addp(x, y);
                 v[q + (1 << sh)] = subp(x, y);
@@ -291,27 +307,35 @@ static int grid_for(int64_t work, int block) {
 
 template <typename K>
 static void launch_radix(K k1, K k2, K k3, K k4, int rb, uint32_t *a, const uint32_t *tw, int s, int64_t N,
-                         cudaStream_t st) {
+                         const uint32_t *xbits, int64_t nbits, cudaStream_t st) {
     const int g = grid_for(N >> rb, 256);
     switch (rb) {
-        case 1: k1<<<g, 256, 0, st>>>(a, tw, s, N); break;
-        case 2: k2<<<g, 256, 0, st>>>(a, tw, s, N); break;
-        case 3: k3<<<g, 256, 0, st>>>(a, tw, s, N); break;
-        default: k4<<<g, 256, 0, st>>>(a, tw, s, N); break;
+        case 1: k1<<<g, 256, 0, st>>>(a, tw, s, N, xbits, nbits); break;
+        case 2: k2<<<g, 256, 0, st>>>(a, tw, s, N, xbits, nbits); break;
+        case 3: k3<<<g, 256, 0, st>>>(a, tw, s, N, xbits, nbits); break;
+        default: k4<<<g, 256, 0, st>>>(a, tw, s, N, xbits, nbits); break;
     }
 }
 
 // forward DIF of a (natural in, bit-reversed out) when tm == null; with tm: forward,
 // pointwise product with tm (Montgomery form, bit-reversed) and inverse DIT (natural out,
-// scaled by N).  Returns the number of kernel launches.
+// scaled by N).  The input is the packed bit string xbits of nbits bits, unpacked on the
+// fly by the first pass.  Returns the number of kernel launches.
 static int ntt_run(uint32_t *a, const uint32_t *tw, const uint32_t *twi, const uint2 *sh, const uint2 *shi,
-                   const uint32_t *tm, int lg, cudaStream_t st) {
+                   const uint32_t *tm, int lg, const uint32_t *xbits, int64_t nbits, cudaStream_t st) {
     const int64_t N = 1LL << lg;
     const int lb = lg < MID_LOG ? lg : MID_LOG;
     int launches = 0;
+    if (lg == lb) {  // no global pass to fuse the unpacking into
+        k_unpack<<<grid_for(N, 256), 256, 0, st>>>(xbits, nbits, a, N);
+        ++launches;
+        xbits = nullptr;
+    }
     for (int s_hi = lg - 1; s_hi >= lb;) {  // global DIF passes, highest stages first
         const int rb = (s_hi - lb + 1) >= 4 ? 4 : (s_hi - lb + 1);
-        launch_radix(k_dif_pass<1>, k_dif_pass<2>, k_dif_pass<3>, k_dif_pass<4>, rb, a, tw, s_hi, N, st);
+        launch_radix(k_dif_pass<1>, k_dif_pass<2>, k_dif_pass<3>, k_dif_pass<4>, rb, a, tw, s_hi, N, xbits, nbits,
+                     st);
+        xbits = nullptr;
         ++launches;
         s_hi -= rb;
     }
@@ -321,7 +345,8 @@ static int ntt_run(uint32_t *a, const uint32_t *tw, const uint32_t *twi, const u
     if (!tm) return launches;
     for (int s_lo = lb; s_lo < lg;) {  // global DIT passes, lowest remaining stages first
         const int rb = (lg - s_lo) >= 4 ? 4 : (lg - s_lo);
-        launch_radix(k_dit_pass<1>, k_dit_pass<2>, k_dit_pass<3>, k_dit_pass<4>, rb, a, twi, s_lo, N, st);
+        launch_radix(k_dit_pass<1>, k_dit_pass<2>, k_dit_pass<3>, k_dit_pass<4>, rb, a, twi, s_lo, N, nullptr, 0,
+                     st);
         ++launches;
         s_lo += rb;
     }
@@ -389,8 +414,7 @@ cvsr_status cvsr_pa_plan_create(cvsr_ctx *ctx, int64_t n_in, int64_t n_out, cons
     int launches = 0;
     k_twiddles<<<grid_for(N - 1, 256), 256, 0, st>>>(p->tw, p->twi, p->sh, p->shi, N);
     ++launches;
-    k_unpack<<<grid_for(N, 256), 256, 0, st>>>(seed_dev, need, p->tm, N);
-    launches += 1 + ntt_run(p->tm, p->tw, p->twi, p->sh, p->shi, nullptr, lg, st);
+    launches += ntt_run(p->tm, p->tw, p->twi, p->sh, p->shi, nullptr, lg, seed_dev, need, st);
     k_to_mont<<<grid_for(N, 256), 256, 0, st>>>(p->tm, N);
     ++launches;
     cudaFreeAsync(seed_dev, st);
@@ -423,8 +447,7 @@ cvsr_status cvsr_pa_hash(cvsr_ctx *ctx, const cvsr_pa_plan *p, int32_t blocks, c
     const uint32_t ninv = to_mont(powmod((uint32_t)(p->N % P), P - 2));
     int launches = 0;
     for (int32_t b = 0; b < blocks; ++b) {
-        k_unpack<<<grid_for(p->N, 256), 256, 0, st>>>(x_bits + b * wi, p->n_in, p->work, p->N);
-        launches += 1 + ntt_run(p->work, p->tw, p->twi, p->sh, p->shi, p->tm, p->lg, st);
+        launches += ntt_run(p->work, p->tw, p->twi, p->sh, p->shi, p->tm, p->lg, x_bits + b * wi, p->n_in, st);
         k_pack_window<<<grid_for(wo * 32, 256), 256, 0, st>>>(p->work, p->n_in, p->n_out, ninv, y_bits + b * wo);
         ++launches;
     }

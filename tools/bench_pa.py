@@ -44,8 +44,11 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / K / blocks
         lg = N.bit_length() - 1
-        passes = 2 * (-(-max(lg - 12, 0) // 4)) + 1 + 2  # global DIF + DIT passes, mid, unpack + pack
-        traffic = passes * 2 * 4 * N + 4 * N  # read + write of N uint32 per pass, + seed transform read
+        P = -(-max(lg - 12, 0) // 4)  # global radix-16 passes per direction
+        # design bytes: first DIF pass reads the packed bits and writes N words; the other 2P - 1
+        # global passes read + write N words; the shared-memory kernel reads data + seed transform
+        # and writes data; the pack reads the n_out-word window and writes n_out bits
+        traffic = n_in / 8 + 4 * N + (2 * P - 1) * 8 * N + 12 * N + 4 * n_out + n_out / 8
         print(json.dumps({"workload": "toeplitz_pa", "n_in": n_in, "n_out": n_out, "ntt_size": N, "blocks": blocks,
                           "ms_per_block": ms, "input_bits_per_s": n_in / (ms * 1e-3),
                           "output_bits_per_s": n_out / (ms * 1e-3),
