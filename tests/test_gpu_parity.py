@@ -596,3 +596,34 @@ def test_pa_errors(cv, ctx):
         cv.cvsr_pa_plan_create(ctx, 10, 11, np.zeros(1, np.uint32))     # n_out > n_in
     with pytest.raises(cv.CvsrError):
         cv.cvsr_pa_plan_create(ctx, 1 << 27, 2, np.zeros((1 << 22) + 1, np.uint32))  # > 2^27
+
+
+def test_sharded_reconcile_equals_single_batch(cv, ctx):
+    """what rank r of k computes for its frame range (inputs from the
+    shard-invariant generator the bench uses, `first_frame = r F`) equals the same frames of one
+    k F-frame run -- labels, flags, iteration counts and hashes -- for k = 2 and 4."""
+    from cvsr_inputs.awgn import torch_quadratures
+    from paper_2108_08418_b200 import dist as cdist
+    from paper_2108_08418_b200.pipeline import SRPipeline
+    cfg = configs.scaled(configs.C2, 4096, 64)
+    codes_l = cfg.build_codes()
+    dev0 = torch.device("cuda:0")
+    F = cfg.frames
+
+    def run(frames, first):
+        x, y = torch_quadratures(frames, cfg.n, cfg.gamma, dev0, first_frame=first)
+        p = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, cfg.n, frames, dev0, max_iter=cfg.max_iter)
+        p.step(x, y, key=12345)
+        torch.cuda.synchronize()
+        out = (p.label_alice.cpu().numpy(), p.verified.cpu().numpy(), p.iters.cpu().numpy(), p.hash_alice.cpu().numpy())
+        p.close()
+        return out
+
+    for k in (2, 4):
+        full = run(k * F, 0)
+        for r in range(k):
+            first, nloc = cdist.shard(F, r)
+            assert nloc == F and first == r * F
+            part = run(F, first)
+            for a, b in zip(part, full):
+                assert np.array_equal(a, b[r * F:(r + 1) * F])
