@@ -95,6 +95,25 @@ def test_ga_threshold_regular_36():
     assert abs(s - 0.8747) < 2e-3 and s < 0.8809
 
 
+def test_ga_threshold_irregular_rate_half():
+    """Textbook value with lambda_2 > 0: the rate-1/2 ensemble lambda = 0.30013 x + 0.28395 x^2 +
+    0.41592 x^7, rho = 0.22919 x^5 + 0.77081 x^6 has the exact-DE BI-AWGN threshold sigma* =
+    0.9158 (Richardson, Shokrollahi, Urbanke 2001); the GA lands within 1.5 %."""
+    s = A.ga_threshold_sigma({2: 0.30013, 3: 0.28395, 8: 0.41592}, {6: 0.22919, 7: 0.77081}, iters=1000)
+    assert abs(s / 0.9158 - 1) < 0.015
+
+
+def test_biawgn_capacity_limits():
+    """BI-AWGN capacity: -> 1 for sigma -> 0, ~ 1/(2 sigma^2 ln 2) for large sigma, 0.5 at the
+    Shannon limit sigma = 0.9787 of rate 1/2; the inverse round-trips."""
+    assert abs(A.biawgn_capacity(0.2) - 1.0) < 1e-5
+    assert abs(A.biawgn_capacity(0.9787) - 0.5) < 2e-4
+    s = 20.0
+    assert abs(A.biawgn_capacity(s) / (1 / (2 * s * s * np.log(2))) - 1) < 0.01
+    assert abs(A.biawgn_sigma_for_capacity(0.3414) - 1.277) < 2e-3
+    assert abs(A.biawgn_capacity(A.biawgn_sigma_for_capacity(0.1)) - 0.1) < 1e-9
+
+
 def test_ga_iterations_monotone():
     """eq:rob2: D_j decreases as the channel improves and is 'never' above the threshold."""
     lam, rho = {3: 1.0}, {6: 1.0}
