@@ -47,6 +47,9 @@ def rho_for(lam: dict, rate: float):
     return rho
 
 
+_SIGMA = {}
+
+
 def evaluate(lam: dict, rate: float, cap: float, n: int, max_iter: int = 200):
     rho = rho_for(lam, rate)
     if rho is None:
@@ -55,7 +58,9 @@ def evaluate(lam: dict, rate: float, cap: float, n: int, max_iter: int = 200):
     frac2 = (lam.get(2, 0.0) / 2.0) * e_per_n            # degree-2 variables per symbol
     if frac2 >= (1.0 - rate):
         return None
-    sigma = K.biawgn_sigma_for_capacity(cap)
+    if cap not in _SIGMA:
+        _SIGMA[cap] = K.biawgn_sigma_for_capacity(cap)
+    sigma = _SIGMA[cap]
     d = K.ga_iterations(2.0 / sigma ** 2, lam, rho, 1.0 / n, max_iter)
     if d > max_iter:
         return None
@@ -69,7 +74,9 @@ def main():
     ap.add_argument("--n", type=int, default=65536)
     ap.add_argument("--iters", type=int, default=60)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--degrees", default=",".join(map(str, DEGREES)))
     args = ap.parse_args()
+    degrees = tuple(int(d) for d in args.degrees.split(","))
     ref = evaluate({2: 0.30013, 3: 0.28395, 8: 0.41592}, args.rate, args.cap, args.n)
     print(json.dumps({"reference": ref}), flush=True)
 
@@ -78,7 +85,7 @@ def main():
         if w.sum() <= 0:
             return None
         w = w / w.sum()
-        return {a: float(x) for a, x in zip(DEGREES, w) if x > 1e-4}
+        return {a: float(x) for a, x in zip(degrees, w) if x > 1e-4}
 
     def f(w):
         lam = lam_of(w)
@@ -87,7 +94,7 @@ def main():
         r = evaluate(lam, args.rate, args.cap, args.n)
         return 1e9 if r is None else r["cost"]
 
-    res = optimize.differential_evolution(f, [(0.0, 1.0)] * len(DEGREES), seed=args.seed, maxiter=args.iters,
+    res = optimize.differential_evolution(f, [(0.0, 1.0)] * len(degrees), seed=args.seed, maxiter=args.iters,
                                           popsize=12, tol=1e-4, polish=False)
     best = evaluate(lam_of(res.x), args.rate, args.cap, args.n)
     print(json.dumps({"best": best}), flush=True)
