@@ -296,6 +296,43 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
     int launched = launch_vn(cd, ds, ds.tiles, qmax, true, nullptr, s);  // decision 0 -> hbuf[0]
     prof_end(ctx);
     int bound = ds.tiles;
+    // Host look-ahead check (counts of iteration k - LOOKAHEAD + 1 are upper bounds of the
+    // current ones) and frame compaction.  Returns false when every frame has stopped.  In the
+    // per-pass path it runs between the status/retire of iteration k and VN_k, so the hard
+    // decisions need not be moved (VN_k rewrites them for every active frame).
+    auto check_and_compact = [&](int k, bool move_hb) -> bool {
+        if (k < LOOKAHEAD) return true;
+        if (cudaEventSynchronize(ctx->ring[(k - LOOKAHEAD + 1) % RING]) != cudaSuccess) return true;
+        const int32_t na = hc[0];
+        const int32_t lanes = hc[2];
+        if (lanes == 0) return false;
+        bound = std::min(bound, std::max(na, 1));
+        // compaction: the active frames fill at most compact_frac of the active tiles
+        if (ca && k < max_iter && na >= 2 && (double)lanes <= compact_frac() * (double)na * T) {
+            DecState dst = ds;
+            if (arena == 0) {
+                dst.msg = ca->msg;
+                dst.L = ca->L;
+                dst.hb = ca->hb;
+                dst.st = ca->st;
+            } else {
+                dst.msg = ds0.msg;
+                dst.L = ds0.L;
+                dst.hb = ds0.hb;
+                dst.st = ds0.st;
+            }
+            dst.slot_frame = ca->slot_frame[n_compact & 1];
+            prof_begin(ctx, KC_CTRL);
+            launched += launch_compact(cd, ds, dst, ca->dst_src, std::max(1, (lanes + T - 1) / T),
+                                       ctx->host_counts_dev, move_hb, s);
+            prof_end(ctx);
+            ds = dst;
+            arena ^= 1;
+            ++n_compact;
+            bound = std::max(1, (lanes + T - 1) / T);
+        }
+        return true;
+    };
     for (int k = 1; k <= max_iter + 1; ++k) {
         const int final_pass = (k == max_iter + 1);
         if (fused && !final_pass) {
@@ -311,55 +348,28 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
             launch_retire(dsc, cd.n, bound, bits_out, s);
             prof_end(ctx);
             launched += 3;
-        } else {
-            if (fused) ds.hb = hbuf[(k - 1) & 1];  // (per-pass path: ds.hb follows compaction)
-            prof_begin(ctx, KC_CN);
-            launch_cn(cd, ds, bound, qmax, final_pass, s);
-            prof_end(ctx);
-            prof_begin(ctx, KC_CTRL);
-            launch_status(ds, k, max_iter, final_pass, ctx->host_counts_dev, s);
-            launch_retire(ds, cd.n, bound, bits_out, s);
-            prof_end(ctx);
-            launched += 3;
-            if (!final_pass) {
-                prof_begin(ctx, KC_VN);
-                launched += launch_vn(cd, ds, bound, qmax, false, nullptr, s);
-                prof_end(ctx);
-            }
+            CK(cudaEventRecord(ctx->ring[k % RING], s));
+            if (!check_and_compact(k, true)) break;
+            continue;
         }
+        if (fused) ds.hb = hbuf[(k - 1) & 1];  // (per-pass path: ds.hb follows compaction)
+        prof_begin(ctx, KC_CN);
+        launch_cn(cd, ds, bound, qmax, final_pass, s);
+        prof_end(ctx);
+        prof_begin(ctx, KC_CTRL);
+        launch_status(ds, k, max_iter, final_pass, ctx->host_counts_dev, s);
+        launch_retire(ds, cd.n, bound, bits_out, s);
+        prof_end(ctx);
+        launched += 3;
+        if (final_pass) {
+            CK(cudaEventRecord(ctx->ring[k % RING], s));
+            break;
+        }
+        if (!check_and_compact(k, fused)) break;
+        prof_begin(ctx, KC_VN);
+        launched += launch_vn(cd, ds, bound, qmax, false, nullptr, s);
+        prof_end(ctx);
         CK(cudaEventRecord(ctx->ring[k % RING], s));
-        if (k >= LOOKAHEAD && !final_pass) {
-            CK(cudaEventSynchronize(ctx->ring[(k - LOOKAHEAD + 1) % RING]));
-            const int32_t na = hc[0];
-            const int32_t lanes = hc[2];
-            if (lanes == 0) break;
-            bound = std::min(bound, std::max(na, 1));
-            // compaction: the active frames fill at most half of the active tiles (counts of
-            // iteration k - LOOKAHEAD + 1 are upper bounds of the current ones)
-            if (ca && k < max_iter && na >= 2 && (double)lanes <= compact_frac() * (double)na * T) {
-                DecState dst = ds;
-                if (arena == 0) {
-                    dst.msg = ca->msg;
-                    dst.L = ca->L;
-                    dst.hb = ca->hb;
-                    dst.st = ca->st;
-                } else {
-                    dst.msg = ds0.msg;
-                    dst.L = ds0.L;
-                    dst.hb = ds0.hb;
-                    dst.st = ds0.st;
-                }
-                dst.slot_frame = ca->slot_frame[n_compact & 1];
-                prof_begin(ctx, KC_CTRL);
-                launched += launch_compact(cd, ds, dst, ca->dst_src, std::max(1, (lanes + T - 1) / T),
-                                           ctx->host_counts_dev, s);
-                prof_end(ctx);
-                ds = dst;
-                arena ^= 1;
-                ++n_compact;
-                bound = std::max(1, (lanes + T - 1) / T);
-            }
-        }
     }
     return check_launch(ctx, launched);
 }

@@ -40,7 +40,10 @@
 namespace cvsr {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int CPW = 4;  // checks per warp
+#ifndef CVSR_CPW
+#define CVSR_CPW 4
+#endif
+constexpr int CPW = CVSR_CPW;  // checks per warp
 
 __device__ __forceinline__ float ex2f(float x) {
     float y;
@@ -1075,7 +1078,6 @@ __global__ void __launch_bounds__(1024) k_compact_plan(DecState src, DecState ds
 // A warp moves CR consecutive rows of destination tile t; the slot map of its lanes
 // (S source slots each) is loaded once and reused for every row.
 constexpr int CR_ROWS = 8;   // rows per warp, float rows
-constexpr int CB_ROWS = 32;  // rows per warp, bit rows
 
 template <int S>
 __global__ void __launch_bounds__(256) k_compact_rows(const float *__restrict__ src, float *__restrict__ dst,
@@ -1107,31 +1109,33 @@ __global__ void __launch_bounds__(256) k_compact_rows(const float *__restrict__ 
     }
 }
 
-// dst[t'][row] bit (s, lane) = src bit of slot dst_src(t', s, lane) for uint4 bit rows (st, hb)
+// dst[t'][row] bit (s, lane) = src bit of slot dst_src(t', s, lane) for uint4 bit rows (st, hb).
+// Thread per row (coalesced uint4 loads and stores); the tile's slot map sits in shared
+// memory and the source word is re-loaded only when the source tile changes.
 __global__ void __launch_bounds__(256) k_compact_bits(const uint4 *__restrict__ src, uint4 *__restrict__ dst,
                                                       int64_t rows, int subs, const int32_t *__restrict__ dst_src,
                                                       const int32_t *__restrict__ counts) {
     const int t = blockIdx.y;
     if (t >= counts[0]) return;
-    const int lane = threadIdx.x & 31;
-    const int64_t r0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * CB_ROWS;
-    if (r0 >= rows) return;
-    int st_[SUBS], word[SUBS], bit[SUBS];
-    for (int q = 0; q < subs; ++q) {
-        const int so = dst_src[t * LANES * subs + q * LANES + lane];
-        st_[q] = so >= 0 ? so / (LANES * subs) : -1;
-        word[q] = so >= 0 ? (so % (LANES * subs)) / LANES : 0;
-        bit[q] = so >= 0 ? so % LANES : 0;
-    }
-    const int nr = (int)(rows - r0 < CB_ROWS ? rows - r0 : CB_ROWS);
-    for (int i = 0; i < nr; ++i) {
-        const int64_t r = r0 + i;
+    __shared__ int smap[LANES * SUBS];
+    const int slots = LANES * subs;
+    for (int i = threadIdx.x; i < slots; i += blockDim.x) smap[i] = dst_src[t * slots + i];
+    __syncthreads();
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
         uint32_t w[SUBS] = {0u, 0u, 0u, 0u};
-        for (int q = 0; q < subs; ++q) {
-            const uint32_t b = st_[q] >= 0 ? (cmpu(src[(size_t)st_[q] * rows + r], word[q]) >> bit[q]) & 1u : 0u;
-            w[q] = __ballot_sync(FULL, b);
+        int cur_t = -1;
+        uint4 cur = make_uint4(0u, 0u, 0u, 0u);
+        for (int i = 0; i < slots; ++i) {
+            const int so = smap[i];
+            if (so < 0) continue;
+            const int st = so / slots, rem = so - st * slots;
+            if (st != cur_t) {
+                cur = src[(size_t)st * rows + r];
+                cur_t = st;
+            }
+            w[i / LANES] |= ((cmpu(cur, rem / LANES) >> (rem % LANES)) & 1u) << (i % LANES);
         }
-        if (lane == 0) dst[(size_t)t * rows + r] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[(size_t)t * rows + r] = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
@@ -1361,11 +1365,11 @@ void launch_init_tiles(const DecState &ds, const uint8_t *alive, cudaStream_t s)
 
 // move the active frames of `src` densely into `dst` (state after a VN pass); returns launches
 int launch_compact(const CodeDev &cd, const DecState &src, const DecState &dst, int32_t *dst_src, int max_tiles,
-                   int32_t *host_counts, cudaStream_t s) {
+                   int32_t *host_counts, bool move_hb, cudaStream_t s) {
     k_compact_plan<<<1, 1024, 0, s>>>(src, dst, dst_src, host_counts);
-    const int64_t fr = 8 * CR_ROWS, br = 8 * CB_ROWS;  // rows per block
+    const int64_t fr = 8 * CR_ROWS;  // float rows per block
     const dim3 gE((unsigned)((cd.E + fr - 1) / fr), max_tiles), gN((unsigned)((cd.n + fr - 1) / fr), max_tiles),
-        gNb((unsigned)((cd.n + br - 1) / br), max_tiles), gM((unsigned)((cd.M + br - 1) / br), max_tiles);
+        gNb((unsigned)((cd.n + 255) / 256), max_tiles), gM((unsigned)((cd.M + 255) / 256), max_tiles);
     if (src.subs == 4) {
         k_compact_rows<4><<<gE, 256, 0, s>>>(src.msg, dst.msg, cd.E, dst_src, dst.counts);
         k_compact_rows<4><<<gN, 256, 0, s>>>(src.L, dst.L, cd.n, dst_src, dst.counts);
@@ -1377,6 +1381,7 @@ int launch_compact(const CodeDev &cd, const DecState &src, const DecState &dst, 
         k_compact_rows<1><<<gN, 256, 0, s>>>(src.L, dst.L, cd.n, dst_src, dst.counts);
     }
     k_compact_bits<<<gM, 256, 0, s>>>(src.st, dst.st, cd.M, src.subs, dst_src, dst.counts);
+    if (!move_hb) return 5;
     k_compact_bits<<<gNb, 256, 0, s>>>(src.hb, dst.hb, cd.n, src.subs, dst_src, dst.counts);
     return 6;
 }

@@ -23,7 +23,7 @@ void launch_synd_transpose(const uint32_t *synd, int32_t F, int32_t M, int subs,
 void launch_init_tiles(const DecState &ds, const uint8_t *alive, cudaStream_t s);
 void launch_set_counts(const DecState &ds, int32_t n_active, cudaStream_t s);
 int launch_compact(const CodeDev &cd, const DecState &src, const DecState &dst, int32_t *dst_src, int max_tiles,
-                   int32_t *host_counts, cudaStream_t s);
+                   int32_t *host_counts, bool move_hb, cudaStream_t s);
 
 // bob_kernels.cu
 void launch_quantise(const float *edges_host, int m, const float *y, int64_t count, uint8_t *label, cudaStream_t s);

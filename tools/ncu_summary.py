@@ -37,9 +37,10 @@ def full(rep, out_md, traffic_json=None, edge_frames=None):
         dur = float(g("gpu__time_duration.sum", "0") or 0)
         rd = float(g("dram__bytes_read.sum", "0") or 0)
         wr = float(g("dram__bytes_write.sum", "0") or 0)
-        units = rows[1][ix["dram__bytes_read.sum"]] if "dram__bytes_read.sum" in ix else ""
-        scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(units, 1.0)
-        rd_mb, wr_mb = rd * scale, wr * scale
+        def to_mb(col, v):
+            unit = rows[1][ix[col]] if col in ix else ""
+            return v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(unit, 1.0)
+        rd_mb, wr_mb = to_mb("dram__bytes_read.sum", rd), to_mb("dram__bytes_write.sum", wr)
         dur_unit = rows[1][ix["gpu__time_duration.sum"]]
         dur_us = dur * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(dur_unit, 1.0)
         gbs = (rd_mb + wr_mb) * 1e6 / (dur_us * 1e-6) / 1e9 if dur_us else 0
