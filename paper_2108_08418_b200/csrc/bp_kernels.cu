@@ -140,6 +140,14 @@ __device__ __forceinline__ void cn_lanes(FV<S> (&q)[DC], uint32_t sb, uint32_t a
 template <int DC, int S>
 __device__ __forceinline__ void cn_check(float *__restrict__ m, int deg, uint32_t sb, uint32_t al, float qmax2) {
     if (!al) return;
+    if constexpr (DC >= 5) {
+        // degree-2 checks in a code with a large maximum degree (the type-A checks of the
+        // MET-style codes, 96 % of their checks): a 2-edge body instead of DC - 2 dummy edges
+        if (deg <= 2) {
+            cn_check<2, S>(m, deg, sb, al, qmax2);
+            return;
+        }
+    }
     FV<S> q[DC];
 #pragma unroll
     for (int k = 0; k < DC; ++k) q[k] = (k < deg) ? ldv<S>(m + (size_t)k * LANES * S) : splat<S>(DUMMY_Q);
