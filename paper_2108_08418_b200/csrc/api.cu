@@ -717,6 +717,8 @@ static void fill_llr_params(LlrParams &p, const cvsr_quantiser *q, int j, uint32
     p.m = q->m;
     p.j = j;
     p.known_mask = mask;
+    for (int jj = 0; jj < q->m; ++jj)
+        if ((mask >> jj) & 1u) p.kj[p.nk++] = jj;
     p.sigma_n = sigma_n;
     p.inv_sigma = 1.0f / sigma_n;
     p.llr_max = llr_max;

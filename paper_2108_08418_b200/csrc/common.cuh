@@ -91,6 +91,8 @@ struct LlrParams {
     float inv_sigma;
     float llr_max;
     const uint32_t *known_bits[8];  // packed [F][Wn] per known slice (nullptr if unknown)
+    int32_t nk;                     // number of known slices
+    int32_t kj[8];                  // their indices, ascending (bit t of a table combo = slice kj[t])
     const float *table;             // [2^|K|][LLR_NTAB] unclamped L on the x grid (nullptr: exact only)
     float edges[255];
 };

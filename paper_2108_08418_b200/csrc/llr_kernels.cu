@@ -145,10 +145,27 @@ __global__ void k_llr_slice(LlrParams p, const float *__restrict__ x, const uint
     }
 }
 
+// L(x) from the table for the known-bit pattern with table index `combo` (bit t =
+// slice kj[t]); exact evaluation off the grid
+__device__ __forceinline__ float llr_eval_combo(const LlrParams &p, const float *se, uint32_t combo, float x) {
+    const float u = (x + LLR_XMAX) * (1.0f / LLR_H);
+    if (p.table && u >= 0.0f && u < 4095.0f) {
+        const int i = (int)u;
+        const float t = u - (float)i;
+        const float *f = p.table + (size_t)combo * LLR_NTAB + i;  // f[0] = grid point i-1
+        const float tm1 = t - 1.0f, tm2 = t - 2.0f, tp1 = t + 1.0f;
+        const float L = (-t * tm1 * tm2 * (1.0f / 6.0f)) * f[0] + (tp1 * tm1 * tm2 * 0.5f) * f[1] +
+                        (-tp1 * t * tm2 * 0.5f) * f[2] + (tp1 * t * tm1 * (1.0f / 6.0f)) * f[3];
+        return llr_clamp(L, p.llr_max);
+    }
+    return llr_cond(se, p.m, p.j, p.known_mask, kappa_of(p.known_mask, (int)combo), x, p.inv_sigma, p.llr_max);
+}
+
 // decoder feed: conditional LLR written straight into the interleaved arena
 // L[t][v][lane][S] (fused transpose, log2 units); known bits read from the
-// packed slices.
-template <int S>
+// packed slices.  NK = number of known slices (compile time: the table index is
+// assembled with NK unrolled bit extractions, no per-symbol mask walking).
+template <int S, int NK>
 __global__ void __launch_bounds__(256) k_llr_interleaved(LlrParams p, const float *__restrict__ x, int32_t F,
                                                          int32_t n, float *__restrict__ L) {
     __shared__ float se[256];
@@ -159,29 +176,29 @@ __global__ void __launch_bounds__(256) k_llr_interleaved(LlrParams p, const floa
     const int v0 = blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int Wn = words_of(n);
+    const int v = v0 + tx;
+    const uint32_t *kb[NK > 0 ? NK : 1];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) kb[k] = p.known_bits[p.kj[k]] + (v0 >> 5);
     for (int fl = ty; fl < LANES * S; fl += 8) {
         const int f = t * LANES * S + fl;
-        const int v = v0 + tx;
         float val = 0.0f;
         if (f < F && v < n) {
-            uint32_t kappa = 0u;
-            if (p.known_mask) {
-                for (int jj = 0; jj < p.m; ++jj)
-                    if ((p.known_mask >> jj) & 1u)
-                        kappa |= ((p.known_bits[jj][(size_t)f * Wn + (v >> 5)] >> (v & 31)) & 1u) << jj;
-            }
-            val = llr_eval(p, se, kappa, x[(size_t)f * n + v]);
+            uint32_t combo = 0u;
+#pragma unroll
+            for (int k = 0; k < NK; ++k) combo |= ((__ldg(kb[k] + (size_t)f * Wn) >> tx) & 1u) << k;
+            val = llr_eval_combo(p, se, combo, x[(size_t)f * n + v]);
         }
         sm[fl][tx] = val * LOG2E;  // arena: log2 units
     }
     __syncthreads();
     for (int vl = ty; vl < 32; vl += 8) {
-        const int v = v0 + vl;
-        if (v < n) {
+        const int vv = v0 + vl;
+        if (vv < n) {
             FV<S> o;
 #pragma unroll
             for (int s = 0; s < S; ++s) o.c[s] = sm[s * LANES + tx][vl];
-            stv<S>(L + (((size_t)t * n + v) * LANES + tx) * S, o);
+            stv<S>(L + (((size_t)t * n + vv) * LANES + tx) * S, o);
         }
     }
 }
@@ -217,12 +234,27 @@ void launch_llr_biawgn(const float *y, int64_t count, float sigma2, float llr_ma
     k_llr_biawgn<<<grid_for(count, 256), 256, 0, s>>>(y, count, sigma2, llr_max, out);
 }
 
+template <int S>
+static void launch_llr_il_s(const LlrParams &p, const float *x, int32_t F, int32_t n, dim3 grid, float *L,
+                            cudaStream_t s) {
+    switch (p.nk) {
+        case 0: k_llr_interleaved<S, 0><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
+        case 1: k_llr_interleaved<S, 1><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
+        case 2: k_llr_interleaved<S, 2><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
+        case 3: k_llr_interleaved<S, 3><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
+        case 4: k_llr_interleaved<S, 4><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
+        case 5: k_llr_interleaved<S, 5><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
+        case 6: k_llr_interleaved<S, 6><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
+        default: k_llr_interleaved<S, 7><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
+    }
+}
+
 void launch_llr_interleaved(const LlrParams &p, const float *x, int32_t F, int32_t n, int tiles, int subs, float *L,
                             cudaStream_t s) {
     dim3 grid((n + 31) / 32, tiles);
-    if (subs == 4) k_llr_interleaved<4><<<grid, 256, 0, s>>>(p, x, F, n, L);
-    else if (subs == 2) k_llr_interleaved<2><<<grid, 256, 0, s>>>(p, x, F, n, L);
-    else k_llr_interleaved<1><<<grid, 256, 0, s>>>(p, x, F, n, L);
+    if (subs == 4) launch_llr_il_s<4>(p, x, F, n, grid, L, s);
+    else if (subs == 2) launch_llr_il_s<2>(p, x, F, n, grid, L, s);
+    else launch_llr_il_s<1>(p, x, F, n, grid, L, s);
 }
 
 }  // namespace cvsr
