@@ -502,6 +502,8 @@ __device__ __forceinline__ void vn_finish(const DecState &ds, const CodeDev &cd,
 template <int DV, int VPW_, bool FIRST, int S>
 __device__ __forceinline__ void vn_chunk(const CodeDev &cd, const DecState &ds, int cls, int t, const uint4 &act,
                                          int chunk, float qmax2, float *post_dbg) {
+    // the warp's variables and slot indices are fetched with one load per lane
+    static_assert(VPW_ <= LANES && VPW_ * DV <= LANES, "VPW x DV slot indices must fit one warp load");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int w0 = (chunk * WARPS_PER_BLOCK + warp) * VPW_;
     const int cnt = cd.vc_cnt[cls];
