@@ -77,7 +77,7 @@ C1 = dict(name="C1", n=1024, dv=3, dc=6, frames=100, ebn0_db=1.5, max_iter=100)
 # S3 0.307 -> FER 1.0, 0.257 -> 0.  See DESIGN.md "Rate calibration".
 # The coded slices use lambda(x) = 0.3 x + 0.7 x^2 (R-3b): at C2's calibrated
 # rates (0.79 / 0.75 of slice capacity) it needs 23 % fewer edges than the rate-1/2
-# lambda for 1-2 more iterations; FER 0 and no undetected frame in 12288 B200 frames.
+# lambda for 1-2 more iterations; FER 0 and no undetected frame in 40960 B200 frames.
 LAMBDA_C2 = ((2, 0.3), (3, 0.7))
 C2 = SRConfig(
     name="C2", m=4, gamma=1.0, delta=0.44905, n=1 << 16, frames=2048,
