@@ -70,6 +70,7 @@ struct Carve {
 struct cvsr_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t cap_stream = nullptr;   // capture-only stream for CUDA graphs (created on first use)
     void *scratch = nullptr;
     size_t scratch_cap = 0;
     int32_t *host_counts = nullptr;      // mapped pinned: [n_act, n_ret, lanes, epoch]
@@ -182,6 +183,17 @@ int pick_subs(int32_t frames, int64_t E) {
 int tiles_for(int32_t frames, int subs) { return (frames + LANES * subs - 1) / (LANES * subs); }
 
 // frame compaction (second arena) on/off: CVSR_COMPACT=0 disables
+// CUDA-graph replay of the iteration loop for small batches (launch-bound): CVSR_GRAPH=0 disables
+bool graph_enabled() {
+    static const int v = [] {
+        const char *e = getenv("CVSR_GRAPH");
+        return (e && *e) ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+constexpr int GRAPH_ITERS = 8;      // iterations per captured graph
+constexpr int GRAPH_MAX_TILES = 2;  // batches of at most this many tiles take the graph path
+
 bool compact_enabled() {
     static int v = -1;
     if (v < 0) {
@@ -292,6 +304,7 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
     // compaction arenas: index 0 = ds0's buffers, 1 = ca's; slot_frame alternates between ca's two maps
     int arena = 0, n_compact = 0;
     const int T = ds0.tile_frames;
+    CK(cudaMemsetAsync(ds0.counts + 3, 0, sizeof(int32_t), s));  // device iteration counter (k_status)
     prof_begin(ctx, KC_INIT);
     int launched = launch_vn(cd, ds, ds.tiles, qmax, true, nullptr, s);  // decision 0 -> hbuf[0]
     prof_end(ctx);
@@ -333,7 +346,53 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
         }
         return true;
     };
-    for (int k = 1; k <= max_iter + 1; ++k) {
+    int k = 1;
+    // Small batches are launch-bound: capture GRAPH_ITERS plain iterations (CN, status with the
+    // device iteration counter, retire, VN; grids sized for all tiles, kernels exit on the
+    // device counts) once and replay the graph, checking the mapped counters one graph behind.
+    const bool use_graph = graph_enabled() && !fused && !ca && !ctx->profiling && ds.tiles <= GRAPH_MAX_TILES &&
+                           max_iter >= 2 * GRAPH_ITERS;
+    if (use_graph) {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        // captured on a private stream (the context stream may be the legacy default stream,
+        // which cannot capture); the graph is launched on the context stream
+        if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+        cudaStream_t cs = ctx->cap_stream;
+        CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < GRAPH_ITERS; ++i) {
+            launch_cn(cd, ds, ds.tiles, qmax, 0, cs);
+            launch_status(ds, -1, max_iter, 0, ctx->host_counts_dev, cs);
+            launch_retire(ds, cd.n, ds.tiles, bits_out, cs);
+            launch_vn(cd, ds, ds.tiles, qmax, false, nullptr, cs);
+        }
+        const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        if (ce != cudaSuccess) return fail(CVSR_ECUDA, "graph capture: %s", cudaGetErrorString(ce));
+        if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+            cudaGraphDestroy(graph);
+            return fail(CVSR_ECUDA, "graph instantiate: %s", cudaGetErrorString(cudaGetLastError()));
+        }
+        bool done = false;
+        int chunk = 0;
+        while (k + GRAPH_ITERS - 1 <= max_iter) {
+            CK(cudaGraphLaunch(exec, s));
+            CK(cudaEventRecord(ctx->ring[chunk % RING], s));
+            launched += GRAPH_ITERS * (3 + cd.n_vclass);
+            k += GRAPH_ITERS;
+            if (++chunk >= 2) {
+                CK(cudaEventSynchronize(ctx->ring[(chunk - 2) % RING]));
+                if (hc[2] == 0) {
+                    done = true;
+                    break;
+                }
+            }
+        }
+        CK(cudaStreamSynchronize(s));  // the graph objects may be freed once the replays finished
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+        if (done || hc[2] == 0) return check_launch(ctx, launched);
+    }
+    for (; k <= max_iter + 1; ++k) {
         const int final_pass = (k == max_iter + 1);
         if (fused && !final_pass) {
             // CN_k (tests decision k-1 in hbuf[(k-1)&1]) + per-tile status + VN_k (writes hbuf[k&1])
@@ -483,6 +542,7 @@ void cvsr_ctx_destroy(cvsr_ctx *ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     else cudaDeviceSynchronize();
     if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->host_counts) cudaFreeHost(ctx->host_counts);
     for (int i = 0; i < RING; ++i)
         if (ctx->ring[i]) cudaEventDestroy(ctx->ring[i]);

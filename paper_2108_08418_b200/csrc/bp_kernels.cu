@@ -658,10 +658,13 @@ __device__ __forceinline__ void mark_frames(const DecState &ds, int t, int s, ui
 
 // Convergence bookkeeping after CN pass k (which tested decision k-1).
 // Single block; loops over tiles.  final_pass: k = max_iter + 1.
-__global__ void __launch_bounds__(1024) k_status(DecState ds, int k, int max_iter, int final_pass,
+// k < 0: the iteration number is the device counter counts[3] + 1 (CUDA-graph replays,
+// where launch arguments are frozen); every call stores its iteration in counts[3].
+__global__ void __launch_bounds__(1024) k_status(DecState ds, int k_arg, int max_iter, int final_pass,
                                                  int32_t *host_counts) {
     __shared__ int s_warp[33];
     __shared__ int s_lanes;
+    const int k = k_arg >= 0 ? k_arg : ds.counts[3] + 1;
     if (threadIdx.x == 0) s_lanes = 0;
     __syncthreads();
     int n_act = 0, n_ret = 0;
@@ -707,6 +710,7 @@ __global__ void __launch_bounds__(1024) k_status(DecState ds, int k, int max_ite
         ds.counts[0] = n_act;
         ds.counts[1] = n_ret;
         ds.counts[2] = s_lanes;
+        ds.counts[3] = k;
         if (host_counts) {
             volatile int32_t *h = host_counts;
             h[0] = n_act;

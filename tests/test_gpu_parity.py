@@ -627,3 +627,44 @@ def test_sharded_reconcile_equals_single_batch(cv, ctx):
             part = run(F, first)
             for a, b in zip(part, full):
                 assert np.array_equal(a, b[r * F:(r + 1) * F])
+
+
+def test_graph_replay_matches_launch_loop():
+    """Small batches replay the iteration loop as a CUDA graph (CVSR_GRAPH, default on): decoded
+    bits, flags and iteration counts equal the plain launch loop's (CVSR_GRAPH=0) exactly."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prog = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+from cvsr_inputs import awgn, codes
+from paper_2108_08418_b200 import cvsr as cv
+code = codes.regular(1024, 3, 6, seed=1)
+sigma = awgn.biawgn_sigma(0.5, 1.5)
+u, y = awgn.biawgn(100, 1024, sigma, seed=77)
+ctx = cv.cvsr_ctx_create(0, torch.cuda.current_stream())
+h = cv.cvsr_code_load(ctx, code.n, code.m_checks, code.row_ptr, code.col_idx)
+lab = torch.from_numpy(u).cuda()
+synd = torch.empty((100, 16), dtype=torch.int32, device="cuda")
+cv.cvsr_syndrome(ctx, h, lab, 100, 0, synd)
+yd = torch.from_numpy(y).cuda(); llr = torch.empty_like(yd)
+cv.cvsr_llr_biawgn(ctx, yd, y.size, sigma ** 2, 40.0, llr)
+bits = torch.empty((100, 32), dtype=torch.int32, device="cuda")
+conv = torch.empty(100, dtype=torch.uint8, device="cuda"); it = torch.empty(100, dtype=torch.int32, device="cuda")
+cv.cvsr_decode(ctx, h, llr, synd, 100, cv.decode_opts(100, 40.0), bits, conv, it)
+torch.cuda.synchronize()
+np.savez(sys.argv[1], bits=bits.cpu().numpy(), conv=conv.cpu().numpy(), it=it.cpu().numpy())
+'''
+    outs = []
+    for g in ("1", "0"):
+        path = os.path.join(root, "gpurun_out", f"graph_{g}.npz") if os.path.isdir(os.path.join(root, "gpurun_out")) \
+            else f"/tmp/graph_{g}.npz"
+        res = subprocess.run([sys.executable, "-c", prog, path], cwd=root, env=dict(os.environ, CVSR_GRAPH=g),
+                             capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(np.load(path))
+    for k in ("bits", "conv", "it"):
+        assert np.array_equal(outs[0][k], outs[1][k]), k
+    assert outs[0]["conv"].sum() >= 50
