@@ -18,6 +18,12 @@
  *    on the context stream and return; outputs are valid after the stream
  *    (or cvsr_ctx_sync) completes.  Entry points that fill a host struct
  *    (cvsr_reconcile with stats_out != NULL, cvsr_count_errors) synchronise.
+ *    cvsr_decode and cvsr_reconcile drive the BP iterations from the host:
+ *    they keep the stream LOOKAHEAD (3) iterations ahead of a mapped
+ *    progress counter and therefore return when the last iteration has been
+ *    enqueued (at most a few iterations before the stream drains); batches of
+ *    at most two tiles replay 8-iteration CUDA graphs instead (CVSR_GRAPH=0
+ *    disables).
  *  - Errors.  The return status is the only error channel.  Argument and
  *    shape validation happens before any launch, so on a validation error
  *    nothing is written.  Asynchronous CUDA faults are sticky and reported
