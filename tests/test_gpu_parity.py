@@ -561,13 +561,15 @@ def test_session_stream_matches_run_host(cv, ctx):
 
 # ----------------------------------------------------------------- Toeplitz privacy amplification (R-8)
 @pytest.mark.parametrize("n_in,n_out,blocks,sample", [(1, 1, 2, None), (5, 3, 3, None), (100, 37, 2, None),
+                                                      (2048, 2048, 2, None), (4097, 4096, 1, None),
                                                       (4096, 1000, 2, None), (5000, 4999, 1, None),
                                                       (20000, 7000, 3, None), (1 << 16, 1 << 15, 2, 300),
                                                       ((1 << 20) + 3, 777_777, 1, 64)])
 def test_pa_toeplitz_bitexact(cv, ctx, n_in, n_out, blocks, sample):
     """cvsr_pa_hash equals the oracle's row-by-row Toeplitz product bit for bit (all rows, or
     `sample` random rows at the larger sizes); sizes cover N = 2 .. 2^21 (shared-memory-only
-    transforms and 1-4-stage global passes) and ragged bit counts."""
+    transforms and 1-4-stage global passes), n_in = n_out, N exactly 4096 (shared-memory
+    kernel only) and n_in + n_out - 1 = 2^13 exactly, and ragged bit counts."""
     from oracle import pa
     rng = np.random.default_rng(n_in + n_out)
     t = rng.integers(0, 2, n_in + n_out - 1, dtype=np.uint8)
