@@ -245,7 +245,9 @@ def main():
     clk, launches, t_ms = timed()
     # a timed region that saw a hardware/thermal slowdown is rejected and measured once more
     # (every rank agrees, so the barriers stay matched)
-    bad = int(bool({"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(clk["reasons"])))
+    bad = int(bool({"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(clk["reasons"])) or
+              (bool(clk.get("sm_mhz")) and bool(clk.get("sm_max_mhz")) and not clk["reasons"] and
+               clk["sm_mhz"] < 0.75 * clk["sm_max_mhz"]))  # clocks pinned low with no reason
     if distributed:
         flag = torch.tensor([bad], device=device)
         dist.all_reduce(flag, op=dist.ReduceOp.MAX)
