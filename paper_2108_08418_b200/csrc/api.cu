@@ -191,6 +191,22 @@ bool graph_enabled() {
     }();
     return v != 0;
 }
+// one-CTA-per-frame shared-memory decoder for small codes: CVSR_SMEM=0 disables,
+// CVSR_SMEM_KB sets the largest per-frame footprint that takes it (default 80 KB)
+bool smem_enabled() {
+    static const int v = [] {
+        const char *e = getenv("CVSR_SMEM");
+        return (e && *e) ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+size_t smem_limit() {
+    static const size_t v = [] {
+        const char *e = getenv("CVSR_SMEM_KB");
+        return (size_t)((e && *e) ? atoi(e) : 80) * 1024;
+    }();
+    return v;
+}
 constexpr int GRAPH_ITERS = 8;      // iterations per captured graph
 constexpr int GRAPH_MAX_TILES = 2;  // batches of at most this many tiles take the graph path
 
@@ -304,6 +320,9 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
     // compaction arenas: index 0 = ds0's buffers, 1 = ca's; slot_frame alternates between ca's two maps
     int arena = 0, n_compact = 0;
     const int T = ds0.tile_frames;
+    if (smem_enabled() && !fused && decode_smem_bytes(cd) <= smem_limit() &&
+        launch_decode_smem(cd, ds0, max_iter, qmax, bits_out, s))
+        return check_launch(ctx, 1);
     CK(cudaMemsetAsync(ds0.counts + 3, 0, sizeof(int32_t), s));  // device iteration counter (k_status)
     prof_begin(ctx, KC_INIT);
     int launched = launch_vn(cd, ds, ds.tiles, qmax, true, nullptr, s);  // decision 0 -> hbuf[0]

@@ -1153,6 +1153,150 @@ __global__ void __launch_bounds__(256) k_compact_bits(const uint4 *__restrict__ 
     }
 }
 
+// ---------------------------------------------------------------- shared-memory decoder
+//
+// Small codes (all E messages and n LLRs of a frame fit in shared memory): one CTA
+// decodes one frame for all its iterations, so no message crosses HBM after the
+// LLRs are read (the on-chip decoder for small N_R).  The
+// arithmetic is that of the interleaved kernels, in the same order (cn_update on
+// the same dummy-padded edge lists, variable sums in CSC slot order, the same
+// clamps), so results are bit-identical to the interleaved path; the iteration
+// bookkeeping follows k_status (a frame whose decision k-1 satisfies H x = s at
+// pass k stops with D = k-1; after max_iter it fails with D = max_iter).
+
+__device__ __forceinline__ uint32_t sbit(const uint32_t *w, int i) { return (w[i >> 5] >> (i & 31)) & 1u; }
+
+template <int DCT>
+__global__ void __launch_bounds__(512) k_decode_smem(CodeDev cd, DecState ds, int max_iter, float qmax2,
+                                                     uint32_t *__restrict__ bits_out) {
+    extern __shared__ float smem_f[];
+    const int f = blockIdx.x;
+    const int T = ds.tile_frames, S = ds.subs;
+    const int t = f / T, r = f % T, sub = r / LANES, l = r % LANES;
+    if (!((cmpu(ds.tile_active[t], sub) >> l) & 1u)) return;  // frame stopped in an earlier slice
+    const int n = cd.n, M = cd.M, E = cd.E;
+    const int Wn = words_of(n), Wm = words_of(M);
+    float *msg = smem_f;
+    float *L = msg + E;
+    uint32_t *hb = reinterpret_cast<uint32_t *>(L + n);
+    uint32_t *sy = hb + Wn;
+    __shared__ int s_unsat;
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+    for (int v = tid; v < n; v += nthr) L[v] = ds.L[(((size_t)t * n + v) * LANES + l) * S + sub];
+    for (int w = tid; w < Wm; w += nthr) {
+        uint32_t word = 0u;
+        const int c1 = min(M, 32 * w + 32);
+        for (int c = 32 * w; c < c1; ++c) word |= ((cmpu(ds.st[(size_t)t * M + c], sub) >> l) & 1u) << (c & 31);
+        sy[w] = word;
+    }
+    __syncthreads();
+    // first VN pass: q = clamp(L), decision 0
+    for (int v0 = warp * LANES; v0 < n; v0 += nwarps * LANES) {
+        const int v = v0 + lane;
+        float lv = 0.0f;
+        if (v < n) {
+            lv = L[v];
+            const float q = clampf(lv, qmax2);
+            for (int p = cd.col_ptr[v]; p < cd.col_ptr[v + 1]; ++p) msg[cd.csc_slot[p]] = q;
+        }
+        const uint32_t word = __ballot_sync(FULL, v < n && lv < 0.0f);
+        if (lane == 0) hb[v0 >> 5] = word;
+    }
+    __syncthreads();
+    int it = max_iter;
+    uint8_t cv = 0;
+    for (int k = 1; k <= max_iter + 1; ++k) {
+        // syndrome test of decision k-1
+        if (tid == 0) s_unsat = 0;
+        __syncthreads();
+        for (int c = tid; c < M; c += nthr) {
+            uint32_t par = sbit(sy, c);
+            for (int e = cd.row_ptr[c]; e < cd.row_ptr[c + 1]; ++e) par ^= sbit(hb, cd.col_idx[e]);
+            if (par) s_unsat = 1;
+        }
+        __syncthreads();
+        if (!s_unsat) {
+            it = k - 1;
+            cv = 1;
+            break;
+        }
+        if (k == max_iter + 1) break;
+        // CN pass k
+        for (int c = tid; c < M; c += nthr) {
+            const int e0 = cd.row_ptr[c], deg = cd.row_ptr[c + 1] - e0;
+            const uint32_t sb = sbit(sy, c);
+            if (DCT >= 5 && deg <= 2) {  // same special case as cn_check
+                float q[2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) q[i] = i < deg ? msg[e0 + i] : DUMMY_Q;
+                cn_update<2>(q, sb, qmax2);
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    if (i < deg) msg[e0 + i] = q[i];
+            } else {
+                float q[DCT];
+#pragma unroll
+                for (int i = 0; i < DCT; ++i) q[i] = i < deg ? msg[e0 + i] : DUMMY_Q;
+                cn_update<DCT>(q, sb, qmax2);
+#pragma unroll
+                for (int i = 0; i < DCT; ++i)
+                    if (i < deg) msg[e0 + i] = q[i];
+            }
+        }
+        __syncthreads();
+        // VN pass k: posterior in CSC slot order, extrinsic V2C, decision k
+        for (int v0 = warp * LANES; v0 < n; v0 += nwarps * LANES) {
+            const int v = v0 + lane;
+            float post = 0.0f;
+            if (v < n) {
+                const int p0 = cd.col_ptr[v], p1 = cd.col_ptr[v + 1];
+                post = L[v];
+                for (int p = p0; p < p1; ++p) post += msg[cd.csc_slot[p]];
+                for (int p = p0; p < p1; ++p) {
+                    const int e = cd.csc_slot[p];
+                    msg[e] = clampf(post - msg[e], qmax2);
+                }
+            }
+            const uint32_t word = __ballot_sync(FULL, v < n && post < 0.0f);
+            if (lane == 0) hb[v0 >> 5] = word;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        ds.iters[f] = it;
+        ds.conv[f] = cv;
+    }
+    for (int w = tid; w < Wn; w += nthr) bits_out[(size_t)f * Wn + w] = hb[w];
+}
+
+size_t decode_smem_bytes(const CodeDev &cd) {
+    return (size_t)(cd.E + cd.n) * 4 + (size_t)(words_of(cd.n) + words_of(cd.M)) * 4;
+}
+
+// returns false when the code is not eligible (max check degree > 12)
+bool launch_decode_smem(const CodeDev &cd, const DecState &ds, int max_iter, float qmax, uint32_t *bits_out,
+                        cudaStream_t s) {
+    const size_t bytes = decode_smem_bytes(cd);
+    const float q2 = qmax * LOG2E;
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        kern<<<ds.frames, 512, bytes, s>>>(cd, ds, max_iter, q2, bits_out);
+    };
+    switch (cd.max_dc) {
+        case 1: case 2: go(k_decode_smem<2>); return true;
+        case 3: go(k_decode_smem<3>); return true;
+        case 4: go(k_decode_smem<4>); return true;
+        case 5: go(k_decode_smem<5>); return true;
+        case 6: go(k_decode_smem<6>); return true;
+        case 7: go(k_decode_smem<7>); return true;
+        case 8: go(k_decode_smem<8>); return true;
+        case 9: go(k_decode_smem<9>); return true;
+        case 10: go(k_decode_smem<10>); return true;
+        case 11: case 12: go(k_decode_smem<12>); return true;
+        default: return false;
+    }
+}
+
 // ---------------------------------------------------------------- launchers
 
 // qmax is in natural LLR units; the arena works in log2 units.  The kernel body

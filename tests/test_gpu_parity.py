@@ -631,9 +631,10 @@ def test_sharded_reconcile_equals_single_batch(cv, ctx):
                 assert np.array_equal(a, b[r * F:(r + 1) * F])
 
 
-def test_graph_replay_matches_launch_loop():
-    """Small batches replay the iteration loop as a CUDA graph (CVSR_GRAPH, default on): decoded
-    bits, flags and iteration counts equal the plain launch loop's (CVSR_GRAPH=0) exactly."""
+def test_graph_replay_and_smem_decoder_match_launch_loop():
+    """Three implementations of the same iterations give identical decoded bits, flags and
+    iteration counts on C1: the plain launch loop (CVSR_SMEM=0 CVSR_GRAPH=0), its CUDA-graph
+    replay (CVSR_GRAPH=1) and the one-CTA-per-frame shared-memory decoder (CVSR_SMEM=1)."""
     import os
     import subprocess
     import sys
@@ -659,14 +660,56 @@ cv.cvsr_decode(ctx, h, llr, synd, 100, cv.decode_opts(100, 40.0), bits, conv, it
 torch.cuda.synchronize()
 np.savez(sys.argv[1], bits=bits.cpu().numpy(), conv=conv.cpu().numpy(), it=it.cpu().numpy())
 '''
-    outs = []
-    for g in ("1", "0"):
-        path = os.path.join(root, "gpurun_out", f"graph_{g}.npz") if os.path.isdir(os.path.join(root, "gpurun_out")) \
-            else f"/tmp/graph_{g}.npz"
-        res = subprocess.run([sys.executable, "-c", prog, path], cwd=root, env=dict(os.environ, CVSR_GRAPH=g),
+    def run(env, tag):
+        path = os.path.join(root, "gpurun_out", f"dec_{tag}.npz") if os.path.isdir(os.path.join(root, "gpurun_out")) \
+            else f"/tmp/dec_{tag}.npz"
+        res = subprocess.run([sys.executable, "-c", prog, path], cwd=root, env=dict(os.environ, **env),
                              capture_output=True, text=True, timeout=600)
         assert res.returncode == 0, res.stderr[-2000:]
-        outs.append(np.load(path))
-    for k in ("bits", "conv", "it"):
-        assert np.array_equal(outs[0][k], outs[1][k]), k
+        return np.load(path)
+
+    # graph replay vs plain launches (interleaved path), and the shared-memory decoder vs both
+    outs = [run({"CVSR_SMEM": "0", "CVSR_GRAPH": "1"}, "graph"), run({"CVSR_SMEM": "0", "CVSR_GRAPH": "0"}, "loop"),
+            run({"CVSR_SMEM": "1"}, "smem")]
+    for o in outs[1:]:
+        for k in ("bits", "conv", "it"):
+            assert np.array_equal(outs[0][k], o[k]), k
     assert outs[0]["conv"].sum() >= 50
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_smem_decoder_reconcile_matches_interleaved(name):
+    """Whole reconciles (several slices, frames that stop after a failed slice, MET codes with
+    degree-2 checks) give identical labels, flags and iteration counts with the shared-memory
+    decoder (n = 4096 fits it) and with the interleaved kernels (CVSR_SMEM=0)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prog = r'''
+import sys, dataclasses, numpy as np, torch
+sys.path.insert(0, ".")
+from cvsr_inputs import awgn, configs
+from paper_2108_08418_b200.pipeline import SRPipeline
+cfg = configs.scaled(configs.CONFIGS[sys.argv[2]], 4096, 200)
+if sys.argv[2] == "C4":
+    cfg = dataclasses.replace(cfg, gamma=1.9)   # harsher than the calibrated SNR: some frames fail
+codes_l = cfg.build_codes()
+x, y = awgn.quadratures(cfg.frames, cfg.n, cfg.gamma, seed=31)
+p = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, cfg.n, cfg.frames, torch.device("cuda:0"),
+               max_iter=cfg.max_iter)
+p.step(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+torch.cuda.synchronize()
+np.savez(sys.argv[1], lab=p.label_alice.cpu().numpy(), ok=p.frame_ok.cpu().numpy(), it=p.iters.cpu().numpy())
+'''
+    outs = []
+    for flag in ("1", "0"):
+        path = os.path.join(root, "gpurun_out", f"rec_{name}_{flag}.npz") \
+            if os.path.isdir(os.path.join(root, "gpurun_out")) else f"/tmp/rec_{name}_{flag}.npz"
+        res = subprocess.run([sys.executable, "-c", prog, path, name], cwd=root,
+                             env=dict(os.environ, CVSR_SMEM=flag), capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(np.load(path))
+    for k in ("lab", "ok", "it"):
+        assert np.array_equal(outs[0][k], outs[1][k]), k
+    assert outs[0]["ok"].sum() >= 1
