@@ -192,7 +192,8 @@ bool graph_enabled() {
     return v != 0;
 }
 // one-CTA-per-frame shared-memory decoder for small codes: CVSR_SMEM=0 disables,
-// CVSR_SMEM_KB sets the largest per-frame footprint that takes it (default 80 KB)
+// CVSR_SMEM_KB sets the largest per-frame footprint that takes it (default 40 KB: measured
+// crossover)
 bool smem_enabled() {
     static const int v = [] {
         const char *e = getenv("CVSR_SMEM");
@@ -203,7 +204,7 @@ bool smem_enabled() {
 size_t smem_limit() {
     static const size_t v = [] {
         const char *e = getenv("CVSR_SMEM_KB");
-        return (size_t)((e && *e) ? atoi(e) : 80) * 1024;
+        return (size_t)((e && *e) ? atoi(e) : 40) * 1024;
     }();
     return v;
 }
