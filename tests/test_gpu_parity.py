@@ -681,7 +681,8 @@ np.savez(sys.argv[1], bits=bits.cpu().numpy(), conv=conv.cpu().numpy(), it=it.cp
 def test_smem_decoder_reconcile_matches_interleaved(name):
     """Whole reconciles (several slices, frames that stop after a failed slice, MET codes with
     degree-2 checks) give identical labels, flags and iteration counts with the shared-memory
-    decoder (n = 4096 fits it) and with the interleaved kernels (CVSR_SMEM=0)."""
+    decoder (n = 2048 fits its 40 KB limit; the launch count shows it was taken) and with the
+    interleaved kernels (CVSR_SMEM=0)."""
     import os
     import subprocess
     import sys
@@ -691,7 +692,7 @@ import sys, dataclasses, numpy as np, torch
 sys.path.insert(0, ".")
 from cvsr_inputs import awgn, configs
 from paper_2108_08418_b200.pipeline import SRPipeline
-cfg = configs.scaled(configs.CONFIGS[sys.argv[2]], 4096, 200)
+cfg = configs.scaled(configs.CONFIGS[sys.argv[2]], 2048, 200)
 if sys.argv[2] == "C4":
     cfg = dataclasses.replace(cfg, gamma=1.9)   # harsher than the calibrated SNR: some frames fail
 codes_l = cfg.build_codes()
@@ -700,7 +701,8 @@ p = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, cfg.n, cfg.f
                max_iter=cfg.max_iter)
 p.step(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
 torch.cuda.synchronize()
-np.savez(sys.argv[1], lab=p.label_alice.cpu().numpy(), ok=p.frame_ok.cpu().numpy(), it=p.iters.cpu().numpy())
+np.savez(sys.argv[1], lab=p.label_alice.cpu().numpy(), ok=p.frame_ok.cpu().numpy(), it=p.iters.cpu().numpy(),
+         launches=np.array([p.launches()]))
 '''
     outs = []
     for flag in ("1", "0"):
@@ -713,3 +715,4 @@ np.savez(sys.argv[1], lab=p.label_alice.cpu().numpy(), ok=p.frame_ok.cpu().numpy
     for k in ("lab", "ok", "it"):
         assert np.array_equal(outs[0][k], outs[1][k]), k
     assert outs[0]["ok"].sum() >= 1
+    assert outs[0]["launches"][0] < outs[1]["launches"][0] // 2   # the on-chip decoder was used
