@@ -527,10 +527,12 @@ def test_reconcile_then_verify(cv, ctx):
     pipe.close()
 
 
-def test_session_stream_matches_run_host(cv, ctx):
+@pytest.mark.parametrize("n,frames", [(4096, 40), (2048, 520)])
+def test_session_stream_matches_run_host(cv, ctx, n, frames):
     """cvsr_session_run_host_stream (double-buffered batches) returns, per batch, exactly what
-    cvsr_session_run_host returns for that batch alone (3 batches, hash check on)."""
-    cfg = configs.scaled(configs.C2, 4096, 40)
+    cvsr_session_run_host (which chunks batches of >= 512 frames) returns for that batch alone
+    (3 batches, hash check on)."""
+    cfg = configs.scaled(configs.C2, n, frames)
     codes_l = cfg.build_codes()
     hs = [load(cv, ctx, c) if c is not None else None for c in codes_l]
     sess = cv.cvsr_session_create(ctx, cfg.m, hs, cfg.order, cv.make_quantiser(cfg.edges()), cfg.sigma_n, cfg.n,
