@@ -34,6 +34,14 @@
  *    and may be shared by contexts on the same device.
  *  - Determinism.  Results are bit-identical for any batch size, frame order
  *    and GPU count: no floating-point atomics on any path.
+ *  - Environment switches (read once per process; defaults in brackets):
+ *    CVSR_SMEM [1] / CVSR_SMEM_KB [40]: one-CTA-per-frame on-chip decoder for
+ *    codes whose messages + LLRs fit in that many KB; CVSR_GRAPH [1]: CUDA
+ *    graph replay of the iteration loop for single-tile batches;
+ *    CVSR_COMPACT [1] / CVSR_COMPACT_FRAC [0.65]: frame compaction;
+ *    CVSR_SUBS [auto]: frames per lane (1, 2, 4); CVSR_FUSED [0] and
+ *    CVSR_CN_TMA [0]: experimental schedulers.  All paths give
+ *    bit-identical results.
  *  - Layouts.  "frame-major" arrays are [frames][n] row-major.  Packed bit
  *    vectors put bit i at bit (i mod 32) of 32-bit word floor(i/32); a
  *    vector of B bits occupies ceil(B/32) words per frame; padding bits are
