@@ -40,8 +40,9 @@
  *    graph replay of the iteration loop for single-tile batches;
  *    CVSR_COMPACT [1] / CVSR_COMPACT_FRAC [0.65]: frame compaction;
  *    CVSR_SUBS [auto]: frames per lane (1, 2, 4); CVSR_FUSED [0] and
- *    CVSR_CN_TMA [0]: experimental schedulers.  The SMEM, GRAPH
- *    and COMPACT paths are tested bit-identical to the default path.
+ *    CVSR_CN_TMA [0]: experimental schedulers.  The SMEM, GRAPH,
+ *    COMPACT, SUBS and FUSED variants are tested bit-identical to the default
+ *    path.
  *  - Layouts.  "frame-major" arrays are [frames][n] row-major.  Packed bit
  *    vectors put bit i at bit (i mod 32) of 32-bit word floor(i/32); a
  *    vector of B bits occupies ceil(B/32) words per frame; padding bits are

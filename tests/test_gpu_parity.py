@@ -718,3 +718,39 @@ np.savez(sys.argv[1], lab=p.label_alice.cpu().numpy(), ok=p.frame_ok.cpu().numpy
         assert np.array_equal(outs[0][k], outs[1][k]), k
     assert outs[0]["ok"].sum() >= 1
     assert outs[0]["launches"][0] < outs[1]["launches"][0] // 2   # the on-chip decoder was used
+
+
+def test_tile_width_and_fused_scheduler_bit_identical():
+    """The frames-per-lane choice (CVSR_SUBS = 1, 2, 4) and the experimental fused scheduler
+    (CVSR_FUSED=1) change only the schedule: a multi-tile C2-structure reconcile gives identical
+    labels, flags and iteration counts."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prog = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from cvsr_inputs import awgn, configs
+from paper_2108_08418_b200.pipeline import SRPipeline
+cfg = configs.scaled(configs.C2, 8192, 300)
+codes_l = cfg.build_codes()
+x, y = awgn.quadratures(cfg.frames, cfg.n, cfg.gamma, seed=12)
+p = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, cfg.n, cfg.frames, torch.device("cuda:0"),
+               max_iter=cfg.max_iter)
+p.step(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+torch.cuda.synchronize()
+np.savez(sys.argv[1], lab=p.label_alice.cpu().numpy(), ok=p.frame_ok.cpu().numpy(), it=p.iters.cpu().numpy())
+'''
+    outs = []
+    for tag, env in (("s4", {"CVSR_SUBS": "4"}), ("s2", {"CVSR_SUBS": "2"}), ("s1", {"CVSR_SUBS": "1"}),
+                     ("fused", {"CVSR_FUSED": "1"})):
+        path = os.path.join(root, "gpurun_out", f"sub_{tag}.npz") if os.path.isdir(os.path.join(root, "gpurun_out")) \
+            else f"/tmp/sub_{tag}.npz"
+        res = subprocess.run([sys.executable, "-c", prog, path], cwd=root, env=dict(os.environ, **env),
+                             capture_output=True, text=True, timeout=900)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(np.load(path))
+    for o in outs[1:]:
+        for k in ("lab", "ok", "it"):
+            assert np.array_equal(outs[0][k], o[k]), k
