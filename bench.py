@@ -338,6 +338,19 @@ def main():
     ms_step = tmax[0] / args.steps
     value = bits_step / (ms_step * 1e-3)
     fer = 1.0 - ok_all / frames_all
+    # Clopper-Pearson 95 % interval of the FER (SURVEY §5 metrics)
+    from scipy import stats as _st
+    fails = int(round(frames_all - ok_all))
+    fer_ci = [float(_st.beta.ppf(0.025, fails, frames_all - fails + 1)) if fails > 0 else 0.0,
+              float(_st.beta.ppf(0.975, fails + 1, frames_all - fails)) if fails < frames_all else 1.0]
+    # per-slice iteration distribution of the attempted frames (rank 0's batch)
+    iter_pct = {}
+    for j in range(m):
+        d = it_h[:, j]
+        d = d[d >= 0]
+        if codes_l[j] is not None and d.size:
+            iter_pct[str(j)] = {q: int(np.percentile(d, p)) for q, p in (("p50", 50), ("p90", 90), ("p99", 99))}
+            iter_pct[str(j)]["max"] = int(d.max())
 
     # beta (equation: beta) with the realised rates R_j = 1 - M_j/N_R
     from paper_2108_08418_b200 import keyrate as analysis  # host-side fp64 formulas
@@ -414,7 +427,8 @@ def main():
                                f"codes {[('disclosed' if c is None else f'R={c.rate:.3f}') for c in codes_l]}",
                    "frames_per_gpu": F, "symbols_per_gpu": F * n, "max_iter": cfg.max_iter,
                    "l2": "inputs and message arena > L2 (no flush needed)", "parallelism": f"frames sharded x{world}"},
-        "fer": fer, "beta": beta, "undetected_frames": int(undet),
+        "fer": fer, "fer_ci95": fer_ci, "beta": beta, "undetected_frames": int(undet),
+        "iters_percentiles_rank0": iter_pct,
         "mean_iters": [float(iters_sum[j] / max(frames_all, 1)) for j in range(m)],
         "group_waste_rank0": waste,
         "symbols_per_s": frames_all * n / (ms_step * 1e-3),
