@@ -251,7 +251,16 @@ __device__ __forceinline__ uint4 cn_group(const CodeDev &cd, const DecState &ds,
 }
 
 template <int DCT, int S>  // DCT = max check degree (templated body) or 0 = generic
-__global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 24) ? 4 : (DCT * S <= 32 ? 3 : 2))
+#ifndef CVSR_CN_MINB16
+#define CVSR_CN_MINB16 5
+#endif
+#ifndef CVSR_CN_MINB20
+#define CVSR_CN_MINB20 5
+#endif
+__global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 16) ? CVSR_CN_MINB16
+                                         : (DCT > 0 && DCT * S <= 20) ? CVSR_CN_MINB20
+                                         : (DCT > 0 && DCT * S <= 24) ? 4
+                                                                      : (DCT * S <= 32 ? 3 : 2))
     k_cn(CodeDev cd, DecState ds, float qmax2, int check_only) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
