@@ -255,7 +255,7 @@ template <int DCT, int S>  // DCT = max check degree (templated body) or 0 = gen
 #define CVSR_CN_MINB16 5
 #endif
 #ifndef CVSR_CN_MINB20
-#define CVSR_CN_MINB20 5
+#define CVSR_CN_MINB20 4
 #endif
 __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 16) ? CVSR_CN_MINB16
                                          : (DCT > 0 && DCT * S <= 20) ? CVSR_CN_MINB20
