@@ -577,7 +577,10 @@ __device__ __forceinline__ void vn_chunk(const CodeDev &cd, const DecState &ds, 
 }
 
 template <int DV, int VPW_, bool FIRST, int S>
-__global__ void __launch_bounds__(BLOCK, 3) k_vn_cls(CodeDev cd, DecState ds, int cls, float qmax2,
+#ifndef CVSR_VN_MINB
+#define CVSR_VN_MINB 3
+#endif
+__global__ void __launch_bounds__(BLOCK, CVSR_VN_MINB) k_vn_cls(CodeDev cd, DecState ds, int cls, float qmax2,
                                                      float *post_dbg) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
