@@ -34,5 +34,8 @@ def lib() -> ctypes.CDLL:
             L.ldpc_configuration_model.restype = ctypes.c_int
             L.ldpc_permutation.argtypes = [ctypes.c_int32, ctypes.c_uint64, i32p]
             L.ldpc_permutation.restype = ctypes.c_int
+            L.ldpc_peg.argtypes = [ctypes.c_int32, ctypes.c_int32, i32p, i32p, ctypes.c_uint64, ctypes.c_int32,
+                                   i32p, i32p]
+            L.ldpc_peg.restype = ctypes.c_int
             _lib = L
     return _lib

@@ -96,6 +96,24 @@ def from_degrees(var_deg: np.ndarray, chk_deg: np.ndarray, seed: int, name: str 
     return Code(n, M, row_ptr, col_idx, name)
 
 
+def peg_from_degrees(var_deg: np.ndarray, chk_deg: np.ndarray, seed: int, depth: int = 4, name: str = "") -> Code:
+    """Progressive-edge-growth construction (host C, `ldpc_peg`): no cycle shorter than
+    2 (depth + 2) is closed where the degree targets allow it."""
+    var_deg = np.ascontiguousarray(var_deg, dtype=np.int32)
+    chk_deg = np.ascontiguousarray(chk_deg, dtype=np.int32)
+    n, M = len(var_deg), len(chk_deg)
+    E = int(var_deg.sum())
+    if E != int(chk_deg.sum()):
+        raise ValueError("variable and check degree sums differ")
+    row_ptr = np.zeros(M + 1, dtype=np.int32)
+    col_idx = np.zeros(E, dtype=np.int32)
+    rc = _native.lib().ldpc_peg(n, M, _i32p(var_deg), _i32p(chk_deg), seed & 0xFFFFFFFFFFFFFFFF, depth,
+                                _i32p(row_ptr), _i32p(col_idx))
+    if rc != 0:
+        raise RuntimeError(f"ldpc_peg failed ({rc})")
+    return Code(n, M, row_ptr, col_idx, name)
+
+
 def permutation(n: int, seed: int) -> np.ndarray:
     p = np.zeros(n, dtype=np.int32)
     if _native.lib().ldpc_permutation(n, seed & 0xFFFFFFFFFFFFFFFF, _i32p(p)) != 0:
@@ -132,7 +150,8 @@ def regular(n: int, dv: int, dc: int, seed: int = 1) -> Code:
 
 
 def irregular_rate(n: int, rate: float, seed: int = 1,
-                   lam: Dict[int, float] = LAMBDA_IRREGULAR, chain_degree2: bool = True) -> Code:
+                   lam: Dict[int, float] = LAMBDA_IRREGULAR, chain_degree2: bool = True,
+                   construction: str = "config", peg_depth: int = 4) -> Code:
     """Irregular code of realised rate 1 - M/n, M = round((1-rate) n).
 
     chain_degree2 (default): the degree-2 variables form a single path through
@@ -157,6 +176,8 @@ def irregular_rate(n: int, rate: float, seed: int = 1,
     chk_deg = _two_degree_checks(int(var_deg.sum()), M)
     chk_deg = chk_deg[permutation(M, seed ^ 0xC4EC)]
     name = f"irregular R={1 - M / n:.4f} n={n}"
+    if construction == "peg":
+        return peg_from_degrees(var_deg, chk_deg, seed, peg_depth, name=name + " (PEG)")
     d2 = np.nonzero(var_deg == 2)[0].astype(np.int32)
     if not chain_degree2 or len(d2) == 0 or len(d2) >= M:
         return from_degrees(var_deg, chk_deg, seed, name=name)

@@ -24,6 +24,7 @@ class SliceSpec:
     rate: float = 0.0    # target rate (realised rate is 1 - M/n)
     met: Optional[Tuple[float, float, int, int]] = None  # (alpha, beta, dv_core, dc_core)
     lam: Optional[Tuple[Tuple[int, float], ...]] = None  # irregular: edge-perspective lambda (default LAMBDA_IRREGULAR)
+    construction: str = "config"  # irregular: "config" (configuration model + degree-2 staircase) or "peg"
 
 
 @dataclasses.dataclass(frozen=True)
@@ -54,6 +55,8 @@ class SRConfig:
                 continue
             if s.kind == "irregular":
                 kw = {"lam": dict(s.lam)} if s.lam else {}
+                if s.construction != "config":
+                    kw["construction"] = s.construction
                 out[s.j] = _codes.irregular_rate(self.n, s.rate, seed=seed + 17 * s.j, **kw)
             elif s.kind == "met":
                 a, b, dv, dc = s.met

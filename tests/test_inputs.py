@@ -61,3 +61,30 @@ def test_configs_build():
     cs = c2.build_codes()
     assert cs[0] is None and cs[1] is None and cs[2] is not None
     assert len(c2.edges()) == 15 and np.array_equal(c2.edges(), edge_table(4, 0.44905))
+
+
+def test_peg_construction_girth_and_degrees():
+    """PEG (host C, NEXT-2): variable degrees exact, check degrees on the two target values,
+    no duplicate edge, and no 4-cycle (two checks sharing two variables) -- the configuration
+    model with the same degrees has some."""
+    from collections import Counter
+
+    def four_cycles(c):
+        rp, ci = np.asarray(c.row_ptr), np.asarray(c.col_idx)
+        pairs = Counter()
+        for r in range(c.m_checks):
+            vs = ci[rp[r]:rp[r + 1]]
+            assert len(set(vs.tolist())) == len(vs)
+            for i in range(len(vs)):
+                for j in range(i + 1, len(vs)):
+                    pairs[(int(vs[i]), int(vs[j]))] += 1
+        return sum(v * (v - 1) // 2 for v in pairs.values())
+
+    peg = codes.irregular_rate(4096, 0.356, seed=3, lam={2: 0.3, 3: 0.7}, construction="peg")
+    cfg = codes.irregular_rate(4096, 0.356, seed=3, lam={2: 0.3, 3: 0.7})
+    dv = np.bincount(np.asarray(peg.col_idx), minlength=peg.n)
+    assert sorted(Counter(dv.tolist()).items()) == sorted(Counter(
+        np.bincount(np.asarray(cfg.col_idx), minlength=cfg.n).tolist()).items())
+    dc = np.diff(np.asarray(peg.row_ptr))
+    assert set(dc.tolist()) <= {4, 5} and peg.n_edges == cfg.n_edges
+    assert four_cycles(peg) == 0 and four_cycles(cfg) > 0
