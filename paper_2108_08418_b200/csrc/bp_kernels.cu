@@ -1113,7 +1113,10 @@ __global__ void __launch_bounds__(1024) k_compact_plan(DecState src, DecState ds
 // dst[t'][row][lane][s] = src[slot dst_src(t', s, lane)] for float rows (messages, LLRs)
 // A warp moves CR consecutive rows of destination tile t; the slot map of its lanes
 // (S source slots each) is loaded once and reused for every row.
-constexpr int CR_ROWS = 8;   // rows per warp, float rows
+#ifndef CVSR_CR_ROWS
+#define CVSR_CR_ROWS 8
+#endif
+constexpr int CR_ROWS = CVSR_CR_ROWS;  // rows per warp, float rows
 
 template <int S>
 __global__ void __launch_bounds__(256) k_compact_rows(const float *__restrict__ src, float *__restrict__ dst,
