@@ -11,6 +11,9 @@ Parity-pin status per function:
   bp_decode, bp_trace             -- pinned (tree exactness vs brute-force marginals,
                                      Hamming ML statistics, SPC/repetition closed forms,
                                      sign symmetry, (3,6) threshold trend)
+  layers, bp_decode_layered       -- pinned (colouring validity + greedy minimality by brute
+                                     force, tree exactness, repetition-chain sum, one-layer
+                                     = flooding, Hamming ML statistics)
   reconcile                       -- pinned (composition: reduces to the pinned parts;
                                      noiseless limit; MC posterior of the LLR feed)
   verify.frame_hash               -- pinned (key = 1 word checksum, key = 2^32 shifted
@@ -19,6 +22,6 @@ Parity-pin status per function:
                                      seeds, linearity, 2-universality statistics)
 """
 from .oracle import (  # noqa: F401
-    build, bp_decode, bp_trace, llr_biawgn, llr_slice, quantise, reconcile, slice_bits,
+    build, bp_decode, bp_decode_layered, bp_trace, layers, llr_biawgn, llr_slice, quantise, reconcile, slice_bits,
     syndrome, num_threads,
 )

@@ -356,6 +356,127 @@ int orc_bp_trace(int32_t n, int32_t n_checks, const int32_t *row_ptr, const int3
 }
 
 /* ------------------------------------------------------------------------
+ * O5'  Row-layered schedule (reading R-9; PAPER.md:189 names BP
+ * without fixing its schedule).  Same stopping rule, clamps and check rule
+ * as O5; only the order of the message updates differs.
+ *   Layers: greedy colouring of the checks in index order -- check c takes
+ *     the smallest colour not taken by a check c' < c sharing a variable with
+ *     it.  Checks of one layer share no variable.
+ *   Init: r_e = 0, post_v = L_v, xhat_v = [L_v < 0]; test H xhat = s (D = 0).
+ *   Iteration k: for layer l = 0, 1, ...: for every check c of layer l:
+ *       q_e = post_v - r_e                       (e = (c, v))
+ *       r_e <- (1 - 2 s_c) BOXPLUS_{e' != e} clamp(q_e', +-Q_MAX)
+ *       post_v <- q_e + r_e
+ *     then xhat_v = [post_v < 0]; test H xhat = s (D = k).
+ * ---------------------------------------------------------------------- */
+int orc_layers(int32_t n, int32_t n_checks, const int32_t *row_ptr, const int32_t *col_idx, int32_t *colour_out) {
+    if (n <= 0 || n_checks <= 0 || !row_ptr || !col_idx || !colour_out) return ORC_EINVAL;
+    orc_graph g;
+    if (graph_init(&g, n, n_checks, row_ptr, col_idx) != ORC_OK) { graph_free(&g); return ORC_EINVAL; }
+    /* the checks sharing a variable with c are the checks of the CSC columns of c's variables */
+    int32_t *chk_of_edge = (int32_t *)malloc(sizeof(int32_t) * (size_t)(row_ptr[n_checks] + 1));
+    for (int32_t c = 0; c < n_checks; ++c)
+        for (int32_t e = row_ptr[c]; e < row_ptr[c + 1]; ++e) chk_of_edge[e] = c;
+    int32_t max_colour = 0;
+    for (int32_t c = 0; c < n_checks; ++c) {
+        int32_t k = 0;
+        for (;;) { /* smallest k not taken by an earlier neighbouring check */
+            int taken = 0;
+            for (int32_t e = row_ptr[c]; e < row_ptr[c + 1] && !taken; ++e) {
+                const int32_t v = col_idx[e];
+                for (int32_t p = g.col_ptr[v]; p < g.col_ptr[v + 1]; ++p) {
+                    const int32_t c2 = chk_of_edge[g.col_edge[p]];
+                    if (c2 < c && colour_out[c2] == k) { taken = 1; break; }
+                }
+            }
+            if (!taken) break;
+            ++k;
+        }
+        colour_out[c] = k;
+        if (k > max_colour) max_colour = k;
+    }
+    free(chk_of_edge);
+    graph_free(&g);
+    return max_colour + 1;
+}
+
+static void layered_iteration(const orc_graph *g, const int32_t *colour, int32_t n_layers, const uint32_t *s,
+                              double q_max, double *r, double *post, double *q, uint8_t *xhat) {
+    for (int32_t l = 0; l < n_layers; ++l) {
+        for (int32_t c = 0; c < g->M; ++c) {
+            if (colour[c] != l) continue;
+            const int32_t beg = g->row_ptr[c], end = g->row_ptr[c + 1];
+            const double sign_c = get_bit(s, c) ? -1.0 : 1.0;
+            for (int32_t e = beg; e < end; ++e) q[e] = post[g->col_idx[e]] - r[e];
+            for (int32_t e = beg; e < end; ++e) {
+                int have = 0;
+                double acc = 0.0;
+                for (int32_t e2 = beg; e2 < end; ++e2) {
+                    if (e2 == e) continue;
+                    const double qc = clampd(q[e2], q_max);
+                    acc = have ? boxplus(acc, qc) : qc;
+                    have = 1;
+                }
+                r[e] = sign_c * (have ? acc : q_max);
+            }
+            for (int32_t e = beg; e < end; ++e) post[g->col_idx[e]] = q[e] + r[e];
+        }
+    }
+    for (int32_t v = 0; v < g->n; ++v) xhat[v] = post[v] < 0.0 ? 1 : 0;
+}
+
+/* stop_early = 1: decode (O3 stopping rule); 0: exactly max_iter iterations (trace).
+ * post_out (nullable): posteriors [frames][n] when the frame stops. */
+int orc_bp_layered(int32_t n, int32_t n_checks, const int32_t *row_ptr, const int32_t *col_idx,
+                   const double *llr, const uint32_t *synd, int32_t frames, int32_t max_iter, double q_max,
+                   int stop_early, uint32_t *bits_out, uint8_t *converged_out, int32_t *iters_out,
+                   double *post_out) {
+    if (n <= 0 || n_checks <= 0 || !row_ptr || !col_idx || !llr || !synd || max_iter < 0) return ORC_EINVAL;
+    int32_t *colour = (int32_t *)malloc(sizeof(int32_t) * (size_t)n_checks);
+    if (!colour) return ORC_EINVAL;
+    const int32_t n_layers = orc_layers(n, n_checks, row_ptr, col_idx, colour);
+    orc_graph g;
+    if (n_layers <= 0 || graph_init(&g, n, n_checks, row_ptr, col_idx) != ORC_OK) {
+        free(colour);
+        return ORC_EINVAL;
+    }
+    const int64_t E = row_ptr[n_checks];
+    const int32_t Wn = words_of(n), Wm = words_of(n_checks);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t f = 0; f < frames; ++f) {
+        const double *L = llr + (int64_t)f * n;
+        const uint32_t *s = synd + (int64_t)f * Wm;
+        double *r = (double *)calloc((size_t)(E + 1), sizeof(double));
+        double *q = (double *)malloc(sizeof(double) * (size_t)(E + 1));
+        double *post = (double *)malloc(sizeof(double) * (size_t)n);
+        uint8_t *xhat = (uint8_t *)malloc((size_t)n);
+        for (int32_t v = 0; v < n; ++v) {
+            post[v] = L[v];
+            xhat[v] = L[v] < 0.0 ? 1 : 0;
+        }
+        int conv = syndrome_ok(&g, xhat, s);
+        int32_t D = 0;
+        for (int32_t k = 1; k <= max_iter && !(stop_early && conv); ++k) {
+            layered_iteration(&g, colour, n_layers, s, q_max, r, post, q, xhat);
+            D = k;
+            conv = syndrome_ok(&g, xhat, s);
+        }
+        if (bits_out) {
+            uint32_t *w = bits_out + (int64_t)f * Wn;
+            memset(w, 0, sizeof(uint32_t) * (size_t)Wn);
+            for (int32_t v = 0; v < n; ++v) set_bit(w, v, xhat[v]);
+        }
+        if (converged_out) converged_out[f] = (uint8_t)conv;
+        if (iters_out) iters_out[f] = D;
+        if (post_out) memcpy(post_out + (int64_t)f * n, post, sizeof(double) * (size_t)n);
+        free(r); free(q); free(post); free(xhat);
+    }
+    graph_free(&g);
+    free(colour);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------
  * O6  Multi-stage slice driver (PAPER.md:114 steps 4-6, Fig. 3), per frame:
  *   K = {}; for j in order:
  *     disclosed slice (codes[j] == NULL): Alice's l_j := Bob's l_j (bits passed in

@@ -56,12 +56,16 @@ def _load():
                                         ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _u32p, _u8p, _i32p]
             L.orc_bp_trace.argtypes = [ctypes.c_int32, ctypes.c_int32, _i32p, _i32p, _f64p, _u32p,
                                        ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _f64p, _f64p]
+            L.orc_layers.argtypes = [ctypes.c_int32, ctypes.c_int32, _i32p, _i32p, _i32p]
+            L.orc_bp_layered.argtypes = [ctypes.c_int32, ctypes.c_int32, _i32p, _i32p, _f64p, _u32p,
+                                         ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_int,
+                                         _u32p, _u8p, _i32p, _f64p]
             L.orc_reconcile.argtypes = [ctypes.c_int32, ctypes.c_int32, _i32p, ctypes.POINTER(_i32p),
                                         ctypes.POINTER(_i32p), _i32p, _f32p, ctypes.c_double, _f32p,
                                         ctypes.POINTER(_u32p), ctypes.c_int32, ctypes.c_int32,
                                         ctypes.c_double, ctypes.c_double, _u8p, _u8p, _i32p]
             for name in ("orc_quantise", "orc_slice_bits", "orc_syndrome", "orc_llr_slice",
-                         "orc_llr_biawgn", "orc_bp_decode", "orc_bp_trace", "orc_reconcile"):
+                         "orc_llr_biawgn", "orc_bp_decode", "orc_bp_trace", "orc_reconcile", "orc_layers", "orc_bp_layered"):
                 getattr(L, name).restype = ctypes.c_int
             _lib = L
     return _lib
@@ -147,6 +151,33 @@ def bp_decode(code, llr: np.ndarray, synd: np.ndarray, max_iter: int = 100, q_ma
                                _p(llr, _f64p), _p(synd, _u32p), F, max_iter, float(q_max),
                                _p(bits, _u32p), _p(conv, _u8p), _p(iters, _i32p)), "bp_decode")
     return bits, conv, iters
+
+
+def layers(code) -> np.ndarray:
+    """Greedy check colouring of the row-layered schedule (reading R-9): int32[M] layer per check."""
+    out = np.empty(code.m_checks, np.int32)
+    rc = _load().orc_layers(code.n, code.m_checks, _p(code.row_ptr, _i32p), _p(code.col_idx, _i32p),
+                            _p(out, _i32p))
+    if rc <= 0:
+        raise RuntimeError(f"oracle layers failed ({rc})")
+    return out
+
+
+def bp_decode_layered(code, llr: np.ndarray, synd: np.ndarray, max_iter: int = 100, q_max: float = 40.0,
+                      stop_early: bool = True):
+    """Row-layered sum-product (reading R-9).  -> (bits, converged, iters, post float64[F][n])."""
+    llr = np.ascontiguousarray(llr, np.float64).reshape(-1, code.n)
+    F = llr.shape[0]
+    synd = np.ascontiguousarray(synd, np.uint32).reshape(F, words(code.m_checks))
+    bits = np.empty((F, words(code.n)), np.uint32)
+    conv = np.empty(F, np.uint8)
+    iters = np.empty(F, np.int32)
+    post = np.empty((F, code.n), np.float64)
+    _chk(_load().orc_bp_layered(code.n, code.m_checks, _p(code.row_ptr, _i32p), _p(code.col_idx, _i32p),
+                                _p(llr, _f64p), _p(synd, _u32p), F, max_iter, float(q_max), int(stop_early),
+                                _p(bits, _u32p), _p(conv, _u8p), _p(iters, _i32p), _p(post, _f64p)),
+         "bp_layered")
+    return bits, conv, iters, post
 
 
 def bp_trace(code, llr: np.ndarray, synd: np.ndarray, k_iters: int, q_max: float = 40.0):

@@ -416,3 +416,113 @@ def test_pa_two_universal():
                 for _ in range(trials))
     ci = st.binomtest(zeros, trials).proportion_ci(0.999)
     assert ci.low <= 1 / 8 <= ci.high
+
+
+# ----------------------------------------------------------------- row-layered BP (O5', reading R-9)
+
+def test_layers_valid_and_greedy():
+    """Checks of one layer share no variable; each check's layer is the smallest one not used
+    by an earlier neighbouring check (brute force over pairs of rows)."""
+    for code in (codes.regular(240, 3, 6, seed=5), codes.irregular_rate(300, 0.4, seed=2)):
+        col = oracle.layers(code)
+        H = code.dense().astype(bool)
+        share = (H.astype(np.int64) @ H.T.astype(np.int64)) > 0
+        M = code.m_checks
+        for c in range(M):
+            nb = [c2 for c2 in range(M) if c2 != c and share[c, c2]]
+            assert all(col[c2] != col[c] for c2 in nb)
+            earlier = {int(col[c2]) for c2 in nb if c2 < c}
+            assert col[c] == min(set(range(M + 1)) - earlier)
+
+
+def test_layered_tree_exact_marginals():
+    """Cycle-free Tanner graphs: the layered schedule also reaches the exact MAP marginals."""
+    rng = np.random.default_rng(21)
+    worst = 0.0
+    for trial in range(60):
+        H = _brute.random_tree_code(rng, int(rng.integers(2, 6)), 4)
+        if H.shape[1] > 16:
+            continue
+        code = codes.from_dense(H)
+        L = rng.normal(0, 3, H.shape[1])
+        u = rng.integers(0, 2, H.shape[1], dtype=np.uint8)
+        s = (H.astype(np.int64) @ u) % 2
+        K = 2 * H.shape[0] + 2
+        _, _, _, post = oracle.bp_decode_layered(code, L[None, :], _brute.pack_bits(s[None, :]), K,
+                                                 stop_early=False)
+        ref = _brute.exact_marginal_llr(H, s, L)
+        worst = max(worst, np.max(np.abs(post[0] - ref) / (np.abs(ref) + 1)))
+    assert worst < 1e-12
+
+
+def test_layered_repetition_chain_one_sweep():
+    """Repetition chain H[i] = e_i + e_{i+1}: layers alternate even/odd checks.  With L = 0
+    except L_0, one layered iteration carries L_0 (signed by the syndrome) along the chain
+    only as far as the two-layer sweep reaches: variables 0..2 get it, so does every
+    variable after enough iterations (posterior = signed sum, as in flooding)."""
+    n = 9
+    H = np.zeros((n - 1, n), np.uint8)
+    for i in range(n - 1):
+        H[i, i] = H[i, i + 1] = 1
+    code = codes.from_dense(H)
+    col = oracle.layers(code)
+    assert list(col) == [i % 2 for i in range(n - 1)]
+    rng = np.random.default_rng(9)
+    L = rng.normal(0, 1.5, n)
+    u = rng.integers(0, 2, n, dtype=np.uint8)
+    s = (H.astype(np.int64) @ u) % 2
+    _, _, _, post = oracle.bp_decode_layered(code, L[None, :], _brute.pack_bits(s[None, :]), n + 1,
+                                             stop_early=False)
+    sign = 1 - 2 * (u ^ u[0]).astype(np.int64)
+    for v in range(n):
+        assert abs(post[0, v] - np.sum(L * sign * sign[v])) < 1e-10
+
+
+def test_layered_disjoint_checks_equal_flooding():
+    """When no two checks share a variable there is one layer and the layered schedule is the
+    flooding schedule: identical decisions, D and posteriors."""
+    rng = np.random.default_rng(5)
+    H = np.zeros((6, 30), np.uint8)
+    perm = rng.permutation(30)
+    for c in range(6):
+        H[c, perm[5 * c:5 * c + 5]] = 1
+    code = codes.from_dense(H)
+    assert (oracle.layers(code) == 0).all()
+    L = rng.normal(0.5, 2, (8, 30))
+    u = rng.integers(0, 2, (8, 30), dtype=np.uint8)
+    s = oracle.syndrome(code, u, 0)
+    b1, c1, d1, p1 = oracle.bp_decode_layered(code, L, s, 3, stop_early=False)
+    c2v, p2 = oracle.bp_trace(code, L, s, 3)
+    assert np.allclose(p1, p2, atol=1e-12)
+    b1, c1, d1, _ = oracle.bp_decode_layered(code, L, s)
+    b2, c2, d2 = oracle.bp_decode(code, L, s)
+    assert np.array_equal(b1, b2) and np.array_equal(c1, c2) and np.array_equal(d1, d2)
+
+
+def test_layered_hamming_ml_and_fewer_iterations():
+    """(7,4) Hamming: layered-converged output == ML on >= 99 %; and on a (3,6) code the
+    layered schedule needs fewer mean iterations than flooding at the same frames."""
+    H = np.array([[1, 0, 1, 0, 1, 0, 1], [0, 1, 1, 0, 0, 1, 1], [0, 0, 0, 1, 1, 1, 1]], np.uint8)
+    code = codes.from_dense(H)
+    rng = np.random.default_rng(3)
+    T = 2000
+    sigma = awgn.biawgn_sigma(4 / 7, 3.0)
+    u = rng.integers(0, 2, (T, 7), dtype=np.uint8)
+    L = 2 * ((1 - 2.0 * u) + sigma * rng.normal(0, 1, (T, 7))) / sigma ** 2
+    s = (u.astype(np.int64) @ H.T) % 2
+    bits, conv, iters, _ = oracle.bp_decode_layered(code, L, _brute.pack_bits(s), max_iter=50)
+    dec = _brute.unpack_bits(bits, 7)
+    ok = [np.array_equal(dec[t], _brute.ml_decode(H, s[t], L[t])) for t in range(T) if conv[t]]
+    assert len(ok) > 0.9 * T and np.mean(ok) >= 0.99
+    code = codes.regular(1008, 3, 6, seed=3)
+    F = 24
+    sigma = awgn.biawgn_sigma(0.5, 1.6)
+    u = rng.integers(0, 2, (F, code.n), dtype=np.uint8)
+    L = 2 * ((1 - 2.0 * u) + sigma * rng.normal(0, 1, u.shape)) / sigma ** 2
+    s = oracle.syndrome(code, u, 0)
+    _, cf, df = oracle.bp_decode(code, L, s)
+    bl, cl, dl, _ = oracle.bp_decode_layered(code, L, s)
+    assert cl.sum() >= cf.sum()
+    both = (cf == 1) & (cl == 1)
+    assert both.sum() >= F // 2 and dl[both].mean() < 0.75 * df[both].mean()
+    assert np.array_equal(_brute.unpack_bits(bl, code.n)[cl == 1], u[cl == 1])
