@@ -182,6 +182,16 @@ int pick_subs(int32_t frames, int64_t E) {
 
 int tiles_for(int32_t frames, int subs) { return (frames + LANES * subs - 1) / (LANES * subs); }
 
+// BP schedule: CVSR_SCHEDULE=layered selects the row-layered schedule (reading R-9),
+// anything else the flooding schedule (reading A-8)
+bool layered_enabled() {
+    static const int v = [] {
+        const char *e = getenv("CVSR_SCHEDULE");
+        return (e && strcmp(e, "layered") == 0) ? 1 : 0;
+    }();
+    return v != 0;
+}
+
 // frame compaction (second arena) on/off: CVSR_COMPACT=0 disables
 // CUDA-graph replay of the iteration loop for small batches (launch-bound): CVSR_GRAPH=0 disables
 bool graph_enabled() {
@@ -321,12 +331,23 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
     // compaction arenas: index 0 = ds0's buffers, 1 = ca's; slot_frame alternates between ca's two maps
     int arena = 0, n_compact = 0;
     const int T = ds0.tile_frames;
-    if (smem_enabled() && !fused && decode_smem_bytes(cd) <= smem_limit() &&
+    const bool layered = layered_enabled();
+    if (layered && !layered_supported(cd))
+        return fail(CVSR_EINVAL, "layered schedule: code needs more than %d layers or has check degree %d > 12",
+                    MAX_LAYERS, cd.max_dc);
+    if (!layered && smem_enabled() && !fused && decode_smem_bytes(cd) <= smem_limit() &&
         launch_decode_smem(cd, ds0, max_iter, qmax, bits_out, s))
         return check_launch(ctx, 1);
     CK(cudaMemsetAsync(ds0.counts + 3, 0, sizeof(int32_t), s));  // device iteration counter (k_status)
     prof_begin(ctx, KC_INIT);
-    int launched = launch_vn(cd, ds, ds.tiles, qmax, true, nullptr, s);  // decision 0 -> hbuf[0]
+    int launched = 0;
+    if (layered) {  // r = 0, post = L (ds.L), decision 0 = [L < 0]
+        CK(cudaMemsetAsync(ds.msg, 0, (size_t)ds.tiles * cd.E * T * sizeof(float), s));
+        launch_layer_init(cd, ds, ds.tiles, s);
+        launched = 1;
+    } else {
+        launched = launch_vn(cd, ds, ds.tiles, qmax, true, nullptr, s);  // decision 0 -> hbuf[0]
+    }
     prof_end(ctx);
     int bound = ds.tiles;
     // Host look-ahead check (counts of iteration k - LOOKAHEAD + 1 are upper bounds of the
@@ -367,6 +388,31 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
         return true;
     };
     int k = 1;
+    if (layered) {
+        // iteration k: syndrome test of decision k-1 (k_cn check-only), status/retire, then the
+        // layers (reading R-9); compaction moves r (msg), post (L), hb and st of active frames
+        for (; k <= max_iter + 1; ++k) {
+            const int final_pass = (k == max_iter + 1);
+            prof_begin(ctx, KC_CN);
+            launch_cn(cd, ds, bound, qmax, 1, s);
+            prof_end(ctx);
+            prof_begin(ctx, KC_CTRL);
+            launch_status(ds, k, max_iter, final_pass, ctx->host_counts_dev, s);
+            launch_retire(ds, cd.n, bound, bits_out, s);
+            prof_end(ctx);
+            launched += 3;
+            if (final_pass) {
+                CK(cudaEventRecord(ctx->ring[k % RING], s));
+                break;
+            }
+            if (!check_and_compact(k, true)) break;
+            prof_begin(ctx, KC_VN);
+            launched += launch_layers(cd, ds, bound, qmax, s);
+            prof_end(ctx);
+            CK(cudaEventRecord(ctx->ring[k % RING], s));
+        }
+        return check_launch(ctx, launched);
+    }
     // Small batches are launch-bound: capture GRAPH_ITERS plain iterations (CN, status with the
     // device iteration counter, retire, VN; grids sized for all tiles, kernels exit on the
     // device counts) once and replay the graph, checking the mapped counters one graph behind.
@@ -645,13 +691,41 @@ cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, cons
         vc_cnt[k] = (int32_t)vc_vars.size() - vc_off[k];
     }
 
+    // row-layered schedule (reading R-9): greedy colouring in check order, check c takes the
+    // smallest colour not taken by an earlier check sharing a variable (bitmask per variable)
+    std::vector<uint64_t> taken((size_t)n_vars, 0ull);
+    std::vector<int32_t> colour((size_t)n_checks);
+    int32_t n_layers = 0;
+    for (int32_t c = 0; c < n_checks && n_layers >= 0; ++c) {
+        uint64_t m = 0ull;
+        for (int32_t e = row_ptr[c]; e < row_ptr[c + 1]; ++e) m |= taken[col_idx[e]];
+        const int k = __builtin_ctzll(~m);
+        if (k >= MAX_LAYERS) {
+            n_layers = -1;  // too many colours: flooding only
+            break;
+        }
+        colour[c] = k;
+        for (int32_t e = row_ptr[c]; e < row_ptr[c + 1]; ++e) taken[col_idx[e]] |= 1ull << k;
+        n_layers = std::max(n_layers, k + 1);
+    }
+    if (n_layers < 0) n_layers = 0;
+    std::vector<int32_t> layer_off(MAX_LAYERS + 1, 0), layer_chk;
+    if (n_layers > 0) {
+        for (int32_t c = 0; c < n_checks; ++c) layer_off[colour[c] + 1]++;
+        for (int l = 0; l < MAX_LAYERS; ++l) layer_off[l + 1] += layer_off[l];
+        layer_chk.resize((size_t)n_checks);
+        std::vector<int32_t> at(layer_off.begin(), layer_off.end() - 1);
+        for (int32_t c = 0; c < n_checks; ++c) layer_chk[at[colour[c]]++] = c;
+    }
+
     DeviceGuard g(ctx->device);
     cvsr_code *code = new cvsr_code();
     code->device = ctx->device;
     const size_t b_rp = align_up((size_t)(n_checks + 1) * 4), b_ci = align_up((size_t)E * 4);
     const size_t b_cp = align_up((size_t)(n_vars + 1) * 4), b_cs = align_up((size_t)E * 4);
     const size_t b_vv = align_up((size_t)n_vars * 4), b_vs = align_up((size_t)E * 4);
-    cudaError_t e = cudaMalloc(&code->mem, b_rp + b_ci + b_cp + b_cs + b_vv + b_vs);
+    const size_t b_lc = align_up((size_t)n_checks * 4);
+    cudaError_t e = cudaMalloc(&code->mem, b_rp + b_ci + b_cp + b_cs + b_vv + b_vs + b_lc);
     if (e != cudaSuccess) {
         delete code;
         cudaGetLastError();
@@ -670,6 +744,9 @@ cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, cons
     cudaError_t e4 = cudaMemcpy(d_cs, csc_slot.data(), (size_t)E * 4, cudaMemcpyHostToDevice);
     cudaError_t e5 = cudaMemcpy(d_vv, vc_vars.data(), (size_t)n_vars * 4, cudaMemcpyHostToDevice);
     cudaError_t e6 = cudaMemcpy(d_vs, vc_slots.data(), (size_t)E * 4, cudaMemcpyHostToDevice);
+    int32_t *d_lc = reinterpret_cast<int32_t *>(base + b_rp + b_ci + b_cp + b_cs + b_vv + b_vs);
+    if (e6 == cudaSuccess && n_layers > 0)
+        e6 = cudaMemcpy(d_lc, layer_chk.data(), (size_t)n_checks * 4, cudaMemcpyHostToDevice);
     if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess || e5 != cudaSuccess ||
         e6 != cudaSuccess) {
         cudaFree(code->mem);
@@ -695,6 +772,9 @@ cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, cons
         d.vc_cnt[k] = k < n_cls ? vc_cnt[k] : 0;
         d.vc_soff[k] = k < n_cls ? vc_soff[k] : 0;
     }
+    d.layer_chk = d_lc;
+    d.n_layers = n_layers;
+    for (int l = 0; l <= MAX_LAYERS; ++l) d.layer_off[l] = layer_off[l];
     code->d = d;
     *out = code;
     return CVSR_OK;

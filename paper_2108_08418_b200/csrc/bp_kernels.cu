@@ -1573,4 +1573,141 @@ void launch_set_counts(const DecState &ds, int32_t n_active, cudaStream_t s) {
     k_set_counts<<<1, 32, 0, s>>>(ds, n_active);
 }
 
+
+// ------------------------------------------------------------------ row-layered schedule
+//
+// Reading R-9 (PAPER.md:189 names sum-product BP without fixing its
+// schedule): the checks are greedily coloured into layers that share no variable
+// (cvsr_code_load) and one iteration updates the layers in order, each against
+// the posteriors the previous layers left:
+//     q_e = post_v - r_e,   r_e <- (1 - 2 s_c) BOXPLUS_{e' != e} clamp(q_e'),   post_v <- q_e + r_e.
+// Arena use: ds.L holds the running posterior post_v (initialised to L_v), ds.msg
+// holds r_e (initialised to 0), ds.hb the hard decisions [post_v < 0].  No VN pass:
+// a layer kernel reads and writes one posterior line and one message line per
+// edge (16 B per edge-frame per iteration, as flooding's CN + VN), but the
+// schedule converges in about half the iterations (tools/layered_study.py).
+// The syndrome test of an iteration is k_cn with check_only = 1.  Same CN
+// arithmetic as k_cn (cn_lanes), so results differ from the oracle's fp64 only by
+// rounding.
+
+// hb = [L < 0] for the active frames; r = 0 is a memset by the caller
+template <int S>
+__global__ void __launch_bounds__(BLOCK) k_layer_init(CodeDev cd, DecState ds) {
+    const int ti = blockIdx.y;
+    if (ti >= ds.counts[0]) return;
+    const int t = ds.active_list[ti];
+    const uint4 act = ds.tile_active[t];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int v = blockIdx.x * WARPS_PER_BLOCK + warp;
+    if (v >= cd.n) return;
+    const FV<S> p = ldv<S>(ds.L + (((size_t)t * cd.n + v) * LANES + lane) * S);
+    uint32_t wd[SUBS] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int s = 0; s < S; ++s) wd[s] = __ballot_sync(FULL, p.c[s] < 0.0f) & cmpu(act, s);
+    if (lane == 0) ds.hb[(size_t)t * cd.n + v] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+}
+
+// one check c of tile t: DC = code's maximum check degree (>= deg, <= 32)
+template <int DC, int S>
+__device__ __forceinline__ void layer_check(const CodeDev &cd, const DecState &ds, int t, const uint4 &act, int c,
+                                            int lane, float qmax2) {
+    const int lo = cd.row_ptr[c], deg = cd.row_ptr[c + 1] - lo;
+    const int myv = lane < deg ? cd.col_idx[lo + lane] : 0;
+    const uint32_t al = lane_act<S>(act, lane);
+    const uint32_t sb = lane_act<S>(ds.st[(size_t)t * cd.M + c], lane);
+    float *mt = ds.msg + ((size_t)t * cd.E + lo) * LANES * S + (size_t)lane * S;
+    float *Lt = ds.L + (size_t)t * cd.n * LANES * S + (size_t)lane * S;
+    int v[DC];
+    FV<S> qu[DC], q[DC];
+#pragma unroll
+    for (int k = 0; k < DC; ++k) {
+        v[k] = __shfl_sync(FULL, myv, k);
+        if (k < deg) {
+            const FV<S> p = ldv<S>(Lt + (size_t)v[k] * LANES * S);
+            const FV<S> r = ldv<S>(mt + (size_t)k * LANES * S);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                qu[k].c[s] = p.c[s] - r.c[s];
+                q[k].c[s] = clampf(qu[k].c[s], qmax2);
+            }
+        } else {
+            q[k] = splat<S>(DUMMY_Q);
+        }
+    }
+    cn_lanes<DC, S>(q, sb, al, qmax2);
+#pragma unroll
+    for (int k = 0; k < DC; ++k) {
+        if (k < deg) {
+            FV<S> p, r;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                // (retired frames' values are dead: their decisions were copied out)
+                r.c[s] = q[k].c[s];
+                p.c[s] = qu[k].c[s] + r.c[s];
+            }
+            uint32_t wd[SUBS] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int s = 0; s < S; ++s) wd[s] = __ballot_sync(FULL, p.c[s] < 0.0f) & cmpu(act, s);
+            if (al) {
+                stv<S>(mt + (size_t)k * LANES * S, r);
+                stv<S>(Lt + (size_t)v[k] * LANES * S, p);
+            }
+            if (lane == 0) ds.hb[(size_t)t * cd.n + v[k]] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+        }
+    }
+}
+
+template <int DC, int S>
+__global__ void __launch_bounds__(BLOCK, (DC * S <= 16) ? 4 : (DC * S <= 24 ? 3 : 2))
+    k_layer(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2) {
+    const int ti = blockIdx.y;
+    if (ti >= ds.counts[0]) return;
+    const int t = ds.active_list[ti];
+    const uint4 act = ds.tile_active[t];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * CPW;
+#pragma unroll 1
+    for (int i = i0; i < min(i0 + CPW, lcnt); ++i) layer_check<DC, S>(cd, ds, t, act, cd.layer_chk[lbeg + i], lane, qmax2);
+}
+
+template <int S>
+static bool launch_layer_s(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,
+                           cudaStream_t s) {
+    switch (cd.max_dc) {
+        case 1: case 2: k_layer<2, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 3: k_layer<3, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 4: k_layer<4, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 5: k_layer<5, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 6: k_layer<6, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 7: case 8: k_layer<8, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 9: case 10: case 11: case 12: k_layer<12, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        default: return false;
+    }
+}
+
+bool layered_supported(const CodeDev &cd) { return cd.n_layers > 0 && cd.max_dc <= 12; }
+
+void launch_layer_init(const CodeDev &cd, const DecState &ds, int grid_tiles, cudaStream_t s) {
+    if (grid_tiles <= 0) return;
+    dim3 grid((cd.n + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, grid_tiles);
+    if (ds.subs == 4) k_layer_init<4><<<grid, BLOCK, 0, s>>>(cd, ds);
+    else if (ds.subs == 2) k_layer_init<2><<<grid, BLOCK, 0, s>>>(cd, ds);
+    else k_layer_init<1><<<grid, BLOCK, 0, s>>>(cd, ds);
+}
+
+// all layers of one iteration (returns the number of launches)
+int launch_layers(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, cudaStream_t s) {
+    if (grid_tiles <= 0) return 0;
+    const float q2 = qmax * LOG2E;
+    const int per_block = WARPS_PER_BLOCK * CPW;
+    for (int l = 0; l < cd.n_layers; ++l) {
+        const int lbeg = cd.layer_off[l], lcnt = cd.layer_off[l + 1] - lbeg;
+        dim3 grid((lcnt + per_block - 1) / per_block, grid_tiles);
+        if (ds.subs == 4) launch_layer_s<4>(cd, ds, grid, lbeg, lcnt, q2, s);
+        else if (ds.subs == 2) launch_layer_s<2>(cd, ds, grid, lbeg, lcnt, q2, s);
+        else launch_layer_s<1>(cd, ds, grid, lbeg, lcnt, q2, s);
+    }
+    return cd.n_layers;
+}
+
 }  // namespace cvsr

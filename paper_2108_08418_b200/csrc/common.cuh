@@ -22,6 +22,8 @@ constexpr int BLOCK = 32 * WARPS_PER_BLOCK;
 constexpr int MAX_DC = 128;
 // variable-degree classes kept separate (more distinct degrees share a generic class)
 constexpr int MAX_VCLASS = 16;
+// layers of the row-layered schedule (codes needing more colours decode with flooding only)
+constexpr int MAX_LAYERS = 48;
 // arena values are LLR * log2(e)
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
@@ -44,6 +46,11 @@ struct CodeDev {
     int32_t vc_off[MAX_VCLASS];    // first position in vc_vars
     int32_t vc_cnt[MAX_VCLASS];    // number of variables
     int64_t vc_soff[MAX_VCLASS];   // first position in vc_slots
+    // row-layered schedule (reading R-9): checks grouped by greedy colour, no two checks of a
+    // layer share a variable; layer l is layer_chk[layer_off[l] .. layer_off[l + 1])
+    const int32_t *layer_chk;      // [M]
+    int32_t n_layers;              // 0: more than MAX_LAYERS colours (layered schedule unavailable)
+    int32_t layer_off[MAX_LAYERS + 1];
 };
 
 // Per-decode device state (lives in the context's scratch arena).
