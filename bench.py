@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--splits", type=int, default=1, help="concurrent frame ranges per GPU (streams)")
+    ap.add_argument("--schedule", default="layered", choices=["layered", "flooding"],
+                    help="BP schedule of the CUDA path (DESIGN.md R-9 layered, A-8 flooding)")
     return ap.parse_args()
 
 
@@ -170,6 +172,7 @@ def main():
     import torch.distributed as dist
 
     from cvsr_inputs.awgn import torch_quadratures
+    os.environ["CVSR_SCHEDULE"] = args.schedule  # read once by libcvsr.so
     from paper_2108_08418_b200 import cvsr
     from paper_2108_08418_b200 import dist as cdist
     from paper_2108_08418_b200.pipeline import SRPipeline
@@ -370,31 +373,43 @@ def main():
         # Units processed = this rank's sum over coded slices of E_j * D_j (edge-iterations).
         edge_it_rank = float(sum(st["edge_iters"]))
         var_it_rank = float(sum(st["iters_sum"][j] * n for j in range(m) if codes_l[j] is not None))
-        cn_bytes = 8.0 * edge_it_rank
-        ach = cn_bytes * args.steps / (cn_ms * 1e-3) / 1e9
+        layered = args.schedule == "layered"
+        if layered:
+            # k_layer (R-9): per edge-iteration it reads and writes the edge's message r_e
+            # and its variable's posterior line (each edge of a layer has its own variable): 16 B
+            kname, kms, kn, per_ef = "k_layer", vn_ms, vn_n, 16.0
+            kdesc = "k_layer (row-layered check update: r_e and posterior in place)"
+        else:
+            kname, kms, kn, per_ef = "k_cn", cn_ms, cn_n, 8.0
+            kdesc = "k_cn (check-node pass, fused syndrome test)"
+        cn_bytes = per_ef * edge_it_rank
+        ach = cn_bytes * args.steps / (kms * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                    "traffic": None, "kernel": "k_cn (check-node pass, fused syndrome test)",
-                    "launches_per_step": cn_n / args.steps, "avg_launch_us": 1e3 * cn_ms / max(cn_n, 1),
-                    "bytes_per_launch": cn_bytes / max(cn_n / args.steps, 1), "peak_source": peak_src,
-                    "share_of_step": cn_ms / args.steps / ms_step}
+                    "traffic": None, "kernel": kdesc,
+                    "launches_per_step": kn / args.steps, "avg_launch_us": 1e3 * kms / max(kn, 1),
+                    "bytes_per_launch": cn_bytes / max(kn / args.steps, 1), "peak_source": peak_src,
+                    "share_of_step": kms / args.steps / ms_step}
         # DRAM traffic of k_cn from the committed ncu --set full capture (profiles/ncu_traffic.json),
         # as bytes per edge-frame scaled to this run's average launch
         tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tj):
             with open(tj) as f:
                 tr = json.load(f)
-            cn_caps = [k for k in tr["kernels"] if "k_cn" in k["kernel"]]
-            if cn_caps and tr.get("k_cn_edge_frames"):
-                per_ef = (cn_caps[0]["dram_read_mb"] + cn_caps[0]["dram_write_mb"]) * 1e6 / tr["k_cn_edge_frames"]
-                roofline["traffic"] = per_ef * edge_it_rank / max(cn_n / args.steps, 1)
-                roofline["traffic_note"] = (f"ncu dram read+write of one full-tile k_cn launch ({tr['source']}) = "
-                                            f"{per_ef:.2f} B per edge-frame vs 8 algorithmic, times this run's "
-                                            f"edge-frames per launch")
-        it_bytes = 8.0 * edge_it_rank + 4.0 * var_it_rank
+            caps = [k for k in tr["kernels"] if kname + "<" in k["kernel"] or k["kernel"] == kname]
+            if caps and tr.get(f"{kname}_edge_frames"):
+                tb = (caps[0]["dram_read_mb"] + caps[0]["dram_write_mb"]) * 1e6 / tr[f"{kname}_edge_frames"]
+                roofline["traffic"] = tb * edge_it_rank / max(kn / args.steps, 1)
+                roofline["traffic_note"] = (f"ncu dram read+write of one full-tile {kname} launch "
+                                            f"({tr.get(kname + '_source', tr['source'])}) = {tb:.2f} B per "
+                                            f"edge-frame vs {per_ef:g} algorithmic, times this run's edge-frames "
+                                            f"per launch")
+        it_bytes = (16.0 * edge_it_rank) if layered else (8.0 * edge_it_rank + 4.0 * var_it_rank)
         it_ach = it_bytes * args.steps / ((cn_ms + vn_ms) * 1e-3) / 1e9
         extra["roofline_bp_iteration"] = {
             "bound": "hbm", "achieved": it_ach, "peak": peak, "unit": "GB/s", "frac": it_ach / peak,
-            "note": "whole flooding iteration (k_cn + k_vn): algorithmic 8 B/edge + 4 B/var per iteration",
+            "note": ("whole layered iteration (k_layer passes + check-only k_cn syndrome test): algorithmic "
+                     "16 B/edge per iteration" if layered else
+                     "whole flooding iteration (k_cn + k_vn): algorithmic 8 B/edge + 4 B/var per iteration"),
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()}}
         if args.splits == 1:
             # Bob-side time reported separately; the headline value above charges the
@@ -426,7 +441,8 @@ def main():
         "config": {"workload": f"{cfg.name}: {m}-slice SR, N_R={n}, gamma={cfg.gamma} (SNR {10*np.log10(cfg.gamma):.1f} dB), "
                                f"codes {[('disclosed' if c is None else f'R={c.rate:.3f}') for c in codes_l]}",
                    "frames_per_gpu": F, "symbols_per_gpu": F * n, "max_iter": cfg.max_iter,
-                   "l2": "inputs and message arena > L2 (no flush needed)", "parallelism": f"frames sharded x{world}"},
+                   "l2": "inputs and message arena > L2 (no flush needed)", "parallelism": f"frames sharded x{world}",
+                   "bp_schedule": args.schedule},
         "fer": fer, "fer_ci95": fer_ci, "beta": beta, "undetected_frames": int(undet),
         "iters_percentiles_rank0": iter_pct,
         "mean_iters": [float(iters_sum[j] / max(frames_all, 1)) for j in range(m)],

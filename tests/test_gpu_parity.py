@@ -790,7 +790,8 @@ def test_layered_decode_parity(tmp_path):
     np.savez(tmp_path / "in.npz", **src)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = subprocess.run([sys.executable, os.path.join(root, "tests", "_layered_child.py"), str(tmp_path / "in.npz"),
-                          str(tmp_path / "out.npz")], cwd=root, env=dict(os.environ, CVSR_SCHEDULE="layered"),
+                          str(tmp_path / "out.npz")], cwd=root, env=dict(os.environ, CVSR_SCHEDULE="layered",
+                                                         PYTHONPATH=os.pathsep.join([root, os.environ.get("PYTHONPATH", "")])),
                          capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-3000:]
     got = np.load(tmp_path / "out.npz")
