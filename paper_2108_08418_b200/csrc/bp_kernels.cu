@@ -1607,21 +1607,19 @@ __global__ void __launch_bounds__(BLOCK) k_layer_init(CodeDev cd, DecState ds) {
     if (lane == 0) ds.hb[(size_t)t * cd.n + v] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
 }
 
-// one check c of tile t: DC = code's maximum check degree (>= deg, <= 32)
-template <int DC, int S>
-__device__ __forceinline__ void layer_check(const CodeDev &cd, const DecState &ds, int t, const uint4 &act, int c,
-                                            int lane, float qmax2) {
-    const int lo = cd.row_ptr[c], deg = cd.row_ptr[c + 1] - lo;
-    const int myv = lane < deg ? cd.col_idx[lo + lane] : 0;
+// one check of tile t: DC = code's maximum check degree (>= deg).  lo/deg/sbits describe the
+// check; v(k) returns the variable of its k-th edge (indices were fetched by the caller).
+template <int DC, int S, typename VarOf>
+__device__ __forceinline__ void layer_check(const CodeDev &cd, const DecState &ds, int t, const uint4 &act, int lo,
+                                            int deg, uint32_t sb, VarOf var_of, int lane, float qmax2) {
     const uint32_t al = lane_act<S>(act, lane);
-    const uint32_t sb = lane_act<S>(ds.st[(size_t)t * cd.M + c], lane);
     float *mt = ds.msg + ((size_t)t * cd.E + lo) * LANES * S + (size_t)lane * S;
     float *Lt = ds.L + (size_t)t * cd.n * LANES * S + (size_t)lane * S;
     int v[DC];
     FV<S> qu[DC], q[DC];
 #pragma unroll
     for (int k = 0; k < DC; ++k) {
-        v[k] = __shfl_sync(FULL, myv, k);
+        v[k] = var_of(k);
         if (k < deg) {
             const FV<S> p = ldv<S>(Lt + (size_t)v[k] * LANES * S);
             const FV<S> r = ldv<S>(mt + (size_t)k * LANES * S);
@@ -1638,18 +1636,14 @@ __device__ __forceinline__ void layer_check(const CodeDev &cd, const DecState &d
 #pragma unroll
     for (int k = 0; k < DC; ++k) {
         if (k < deg) {
-            FV<S> p, r;
+            FV<S> p;
 #pragma unroll
-            for (int s = 0; s < S; ++s) {
-                // (retired frames' values are dead: their decisions were copied out)
-                r.c[s] = q[k].c[s];
-                p.c[s] = qu[k].c[s] + r.c[s];
-            }
+            for (int s = 0; s < S; ++s) p.c[s] = qu[k].c[s] + q[k].c[s];  // (retired frames' values are dead)
             uint32_t wd[SUBS] = {0u, 0u, 0u, 0u};
 #pragma unroll
             for (int s = 0; s < S; ++s) wd[s] = __ballot_sync(FULL, p.c[s] < 0.0f) & cmpu(act, s);
             if (al) {
-                stv<S>(mt + (size_t)k * LANES * S, r);
+                stv<S>(mt + (size_t)k * LANES * S, q[k]);
                 stv<S>(Lt + (size_t)v[k] * LANES * S, p);
             }
             if (lane == 0) ds.hb[(size_t)t * cd.n + v[k]] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
@@ -1657,8 +1651,14 @@ __device__ __forceinline__ void layer_check(const CodeDev &cd, const DecState &d
     }
 }
 
+#ifndef CVSR_LAYER_MINB
+#define CVSR_LAYER_MINB 4
+#endif
+// A warp takes CPW checks of the layer.  When CPW x DC <= 32 their check ids, row bounds and
+// column indices are fetched up front with one load per lane (no dependent index loads per
+// check); otherwise per check.
 template <int DC, int S>
-__global__ void __launch_bounds__(BLOCK, (DC * S <= 16) ? 4 : (DC * S <= 24 ? 3 : 2))
+__global__ void __launch_bounds__(BLOCK, (DC * S <= 20) ? CVSR_LAYER_MINB : (DC * S <= 24 ? 3 : 2))
     k_layer(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
@@ -1666,8 +1666,36 @@ __global__ void __launch_bounds__(BLOCK, (DC * S <= 16) ? 4 : (DC * S <= 24 ? 3 
     const uint4 act = ds.tile_active[t];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * CPW;
+    const int nc = min(CPW, lcnt - i0);
+    if (nc <= 0) return;
+    const int myc = lane < nc ? cd.layer_chk[lbeg + i0 + lane] : 0;
+    const int mylo = lane < nc ? cd.row_ptr[myc] : 0;
+    const int myhi = lane < nc ? cd.row_ptr[myc + 1] : 0;
+    const uint4 *stt = ds.st + (size_t)t * cd.M;
+    if constexpr (CPW * DC <= LANES) {
+        const int ii = lane / DC, kk = lane - ii * DC;
+        const int lo_ii = __shfl_sync(FULL, mylo, ii < CPW ? ii : 0);
+        const int hi_ii = __shfl_sync(FULL, myhi, ii < CPW ? ii : 0);
+        const int myv = (ii < nc && kk < hi_ii - lo_ii) ? cd.col_idx[lo_ii + kk] : 0;
 #pragma unroll 1
-    for (int i = i0; i < min(i0 + CPW, lcnt); ++i) layer_check<DC, S>(cd, ds, t, act, cd.layer_chk[lbeg + i], lane, qmax2);
+        for (int i = 0; i < nc; ++i) {
+            const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
+            const int c = __shfl_sync(FULL, myc, i);
+            const uint32_t sb = lane_act<S>(stt[c], lane);
+            layer_check<DC, S>(cd, ds, t, act, lo, deg, sb,
+                               [&](int k) { return __shfl_sync(FULL, myv, i * DC + k); }, lane, qmax2);
+        }
+    } else {
+#pragma unroll 1
+        for (int i = 0; i < nc; ++i) {
+            const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
+            const int c = __shfl_sync(FULL, myc, i);
+            const uint32_t sb = lane_act<S>(stt[c], lane);
+            const int myv = lane < deg ? cd.col_idx[lo + lane] : 0;
+            layer_check<DC, S>(cd, ds, t, act, lo, deg, sb, [&](int k) { return __shfl_sync(FULL, myv, k); },
+                               lane, qmax2);
+        }
+    }
 }
 
 template <int S>
