@@ -42,7 +42,13 @@
  *    CVSR_SUBS [auto]: frames per lane (1, 2, 4); CVSR_FUSED [0] and
  *    CVSR_CN_TMA [0]: experimental schedulers.  The SMEM, GRAPH,
  *    COMPACT, SUBS and FUSED variants are tested bit-identical to the default
- *    path.
+ *    path.  CVSR_SCHEDULE [flooding]: "layered" selects the row-layered BP
+ *    schedule (reading R-9; PAPER.md:189 leaves the schedule open)
+ *    for cvsr_decode, cvsr_reconcile and the sessions -- a different
+ *    algorithm, tested against the oracle's layered decoder rather than
+ *    bit-identical to flooding; cvsr_decode_trace stays flooding.  A code
+ *    needing more than 48 layers or with check degree > 12 then fails with
+ *    CVSR_EINVAL.  bench.py selects it by default (--schedule).
  *  - Layouts.  "frame-major" arrays are [frames][n] row-major.  Packed bit
  *    vectors put bit i at bit (i mod 32) of 32-bit word floor(i/32); a
  *    vector of B bits occupies ceil(B/32) words per frame; padding bits are
