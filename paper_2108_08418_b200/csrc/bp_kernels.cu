@@ -1654,6 +1654,10 @@ __device__ __forceinline__ void layer_check(const CodeDev &cd, const DecState &d
 #ifndef CVSR_LAYER_MINB
 #define CVSR_LAYER_MINB 4
 #endif
+#ifndef CVSR_LAYER_CPW
+#define CVSR_LAYER_CPW 4
+#endif
+constexpr int LCPW = CVSR_LAYER_CPW;  // checks per warp in k_layer
 // A warp takes CPW checks of the layer.  When CPW x DC <= 32 their check ids, row bounds and
 // column indices are fetched up front with one load per lane (no dependent index loads per
 // check); otherwise per check.
@@ -1665,17 +1669,17 @@ __global__ void __launch_bounds__(BLOCK, (DC * S <= 20) ? CVSR_LAYER_MINB : (DC 
     const int t = ds.active_list[ti];
     const uint4 act = ds.tile_active[t];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * CPW;
-    const int nc = min(CPW, lcnt - i0);
+    const int i0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * LCPW;
+    const int nc = min(LCPW, lcnt - i0);
     if (nc <= 0) return;
     const int myc = lane < nc ? cd.layer_chk[lbeg + i0 + lane] : 0;
     const int mylo = lane < nc ? cd.row_ptr[myc] : 0;
     const int myhi = lane < nc ? cd.row_ptr[myc + 1] : 0;
     const uint4 *stt = ds.st + (size_t)t * cd.M;
-    if constexpr (CPW * DC <= LANES) {
+    if constexpr (LCPW * DC <= LANES) {
         const int ii = lane / DC, kk = lane - ii * DC;
-        const int lo_ii = __shfl_sync(FULL, mylo, ii < CPW ? ii : 0);
-        const int hi_ii = __shfl_sync(FULL, myhi, ii < CPW ? ii : 0);
+        const int lo_ii = __shfl_sync(FULL, mylo, ii < LCPW ? ii : 0);
+        const int hi_ii = __shfl_sync(FULL, myhi, ii < LCPW ? ii : 0);
         const int myv = (ii < nc && kk < hi_ii - lo_ii) ? cd.col_idx[lo_ii + kk] : 0;
 #pragma unroll 1
         for (int i = 0; i < nc; ++i) {
@@ -1727,7 +1731,7 @@ void launch_layer_init(const CodeDev &cd, const DecState &ds, int grid_tiles, cu
 int launch_layers(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, cudaStream_t s) {
     if (grid_tiles <= 0) return 0;
     const float q2 = qmax * LOG2E;
-    const int per_block = WARPS_PER_BLOCK * CPW;
+    const int per_block = WARPS_PER_BLOCK * LCPW;
     for (int l = 0; l < cd.n_layers; ++l) {
         const int lbeg = cd.layer_off[l], lcnt = cd.layer_off[l + 1] - lbeg;
         dim3 grid((lcnt + per_block - 1) / per_block, grid_tiles);
