@@ -425,12 +425,37 @@ static void layered_iteration(const orc_graph *g, const int32_t *colour, int32_t
     for (int32_t v = 0; v < g->n; ++v) xhat[v] = post[v] < 0.0 ? 1 : 0;
 }
 
-/* stop_early = 1: decode (O3 stopping rule); 0: exactly max_iter iterations (trace).
- * post_out (nullable): posteriors [frames][n] when the frame stops. */
+/* One frame of the layered decoder: r (E entries) and post (n) are the frame's state.
+ * stop_early = 1: the O5 stopping rule (first k with H xhat = s); 0: exactly max_iter
+ * iterations (trace).  Returns D, sets *conv. */
+static int32_t bp_frame_layered(const orc_graph *g, const int32_t *colour, int32_t n_layers, const double *L,
+                                const uint32_t *s, int32_t max_iter, double q_max, int stop_early, uint8_t *xhat,
+                                int *conv, double *r, double *post) {
+    const int64_t E = g->row_ptr[g->M];
+    double *q = (double *)malloc(sizeof(double) * (size_t)(E + 1));
+    for (int64_t e = 0; e < E; ++e) r[e] = 0.0;
+    for (int32_t v = 0; v < g->n; ++v) {
+        post[v] = L[v];
+        xhat[v] = L[v] < 0.0 ? 1 : 0;
+    }
+    *conv = syndrome_ok(g, xhat, s);
+    int32_t D = 0;
+    for (int32_t k = 1; k <= max_iter && !(stop_early && *conv); ++k) {
+        layered_iteration(g, colour, n_layers, s, q_max, r, post, q, xhat);
+        D = k;
+        *conv = syndrome_ok(g, xhat, s);
+    }
+    free(q);
+    return D;
+}
+
+/* stop_early = 1: decode (O5 stopping rule); 0: exactly max_iter iterations (trace).
+ * post_out (nullable): posteriors [frames][n] when the frame stops; r_out (nullable): the
+ * check-to-variable messages r_e [frames][E] (CSR edge order) when the frame stops. */
 int orc_bp_layered(int32_t n, int32_t n_checks, const int32_t *row_ptr, const int32_t *col_idx,
                    const double *llr, const uint32_t *synd, int32_t frames, int32_t max_iter, double q_max,
                    int stop_early, uint32_t *bits_out, uint8_t *converged_out, int32_t *iters_out,
-                   double *post_out) {
+                   double *post_out, double *r_out) {
     if (n <= 0 || n_checks <= 0 || !row_ptr || !col_idx || !llr || !synd || max_iter < 0) return ORC_EINVAL;
     int32_t *colour = (int32_t *)malloc(sizeof(int32_t) * (size_t)n_checks);
     if (!colour) return ORC_EINVAL;
@@ -444,23 +469,12 @@ int orc_bp_layered(int32_t n, int32_t n_checks, const int32_t *row_ptr, const in
     const int32_t Wn = words_of(n), Wm = words_of(n_checks);
 #pragma omp parallel for schedule(dynamic, 1)
     for (int32_t f = 0; f < frames; ++f) {
-        const double *L = llr + (int64_t)f * n;
-        const uint32_t *s = synd + (int64_t)f * Wm;
-        double *r = (double *)calloc((size_t)(E + 1), sizeof(double));
-        double *q = (double *)malloc(sizeof(double) * (size_t)(E + 1));
+        double *r = (double *)malloc(sizeof(double) * (size_t)(E + 1));
         double *post = (double *)malloc(sizeof(double) * (size_t)n);
         uint8_t *xhat = (uint8_t *)malloc((size_t)n);
-        for (int32_t v = 0; v < n; ++v) {
-            post[v] = L[v];
-            xhat[v] = L[v] < 0.0 ? 1 : 0;
-        }
-        int conv = syndrome_ok(&g, xhat, s);
-        int32_t D = 0;
-        for (int32_t k = 1; k <= max_iter && !(stop_early && conv); ++k) {
-            layered_iteration(&g, colour, n_layers, s, q_max, r, post, q, xhat);
-            D = k;
-            conv = syndrome_ok(&g, xhat, s);
-        }
+        int conv = 0;
+        const int32_t D = bp_frame_layered(&g, colour, n_layers, llr + (int64_t)f * n, synd + (int64_t)f * Wm,
+                                           max_iter, q_max, stop_early, xhat, &conv, r, post);
         if (bits_out) {
             uint32_t *w = bits_out + (int64_t)f * Wn;
             memset(w, 0, sizeof(uint32_t) * (size_t)Wn);
@@ -469,7 +483,8 @@ int orc_bp_layered(int32_t n, int32_t n_checks, const int32_t *row_ptr, const in
         if (converged_out) converged_out[f] = (uint8_t)conv;
         if (iters_out) iters_out[f] = D;
         if (post_out) memcpy(post_out + (int64_t)f * n, post, sizeof(double) * (size_t)n);
-        free(r); free(q); free(post); free(xhat);
+        if (r_out) memcpy(r_out + (int64_t)f * E, r, sizeof(double) * (size_t)E);
+        free(r); free(post); free(xhat);
     }
     graph_free(&g);
     free(colour);
@@ -481,7 +496,8 @@ int orc_bp_layered(int32_t n, int32_t n_checks, const int32_t *row_ptr, const in
  *   K = {}; for j in order:
  *     disclosed slice (codes[j] == NULL): Alice's l_j := Bob's l_j (bits passed in
  *       synd[j]), K += {j}
- *     else: L <- O4(x, K); decode with (H_j, s_j); Alice's l_j <- xhat;
+ *     else: L <- O4(x, K); decode with (H_j, s_j) -- O5 flooding (schedule 0) or the
+ *       row-layered O5' (schedule 1, reading R-9); Alice's l_j <- xhat;
  *       not converged => frame fails, later slices not attempted (A-13);
  *       else K += {j}.
  * Outputs: Alice's labels, frame_ok, iters[f][j] (= D; 0 disclosed; -1 not attempted).
@@ -489,14 +505,26 @@ int orc_bp_layered(int32_t n, int32_t n_checks, const int32_t *row_ptr, const in
 int orc_reconcile(int32_t m, int32_t n, const int32_t *n_checks, const int32_t *const *row_ptrs,
                   const int32_t *const *col_idxs, const int32_t *order, const float *edges,
                   double sigma_n, const float *x, const uint32_t *const *synd, int32_t frames,
-                  int32_t max_iter, double q_max, double llr_max, uint8_t *label_out,
+                  int32_t max_iter, double q_max, double llr_max, int32_t schedule, uint8_t *label_out,
                   uint8_t *frame_ok, int32_t *iters) {
     if (m < 1 || m > 8 || n <= 0 || !order || !edges || !x || !synd || !label_out || !frame_ok || !iters)
         return ORC_EINVAL;
+    if (schedule != 0 && schedule != 1) return ORC_EINVAL;
     orc_graph g[8];
+    int32_t *colour[8];
+    int32_t n_layers[8];
     memset(g, 0, sizeof(g));
-    for (int32_t j = 0; j < m; ++j)
-        if (row_ptrs[j] && graph_init(&g[j], n, n_checks[j], row_ptrs[j], col_idxs[j]) != ORC_OK) return ORC_EINVAL;
+    memset(colour, 0, sizeof(colour));
+    memset(n_layers, 0, sizeof(n_layers));
+    for (int32_t j = 0; j < m; ++j) {
+        if (!row_ptrs[j]) continue;
+        if (graph_init(&g[j], n, n_checks[j], row_ptrs[j], col_idxs[j]) != ORC_OK) return ORC_EINVAL;
+        if (schedule == 1) {
+            colour[j] = (int32_t *)malloc(sizeof(int32_t) * (size_t)n_checks[j]);
+            n_layers[j] = orc_layers(n, n_checks[j], row_ptrs[j], col_idxs[j], colour[j]);
+            if (n_layers[j] <= 0) return ORC_EINVAL;
+        }
+    }
     const int32_t Wn = words_of(n);
 #pragma omp parallel for schedule(dynamic, 1)
     for (int32_t f = 0; f < frames; ++f) {
@@ -520,7 +548,16 @@ int orc_reconcile(int32_t m, int32_t n, const int32_t *n_checks, const int32_t *
                 L[v] = llr_one(m, edges, sigma_n, (double)x[(int64_t)f * n + v], j, known, lab[v], llr_max);
             int conv = 0;
             const int32_t Wm = words_of(n_checks[j]);
-            int32_t D = bp_frame(&g[j], L, synd[j] + (int64_t)f * Wm, max_iter, q_max, xhat, &conv);
+            const uint32_t *sj = synd[j] + (int64_t)f * Wm;
+            int32_t D;
+            if (schedule == 1) {
+                double *r = (double *)malloc(sizeof(double) * (size_t)(row_ptrs[j][n_checks[j]] + 1));
+                double *post = (double *)malloc(sizeof(double) * (size_t)n);
+                D = bp_frame_layered(&g[j], colour[j], n_layers[j], L, sj, max_iter, q_max, 1, xhat, &conv, r, post);
+                free(r); free(post);
+            } else {
+                D = bp_frame(&g[j], L, sj, max_iter, q_max, xhat, &conv);
+            }
             for (int32_t v = 0; v < n; ++v) lab[v] |= (uint8_t)(xhat[v] << j);
             iters[(int64_t)f * m + j] = D;
             if (!conv) ok = 0;
@@ -529,7 +566,9 @@ int orc_reconcile(int32_t m, int32_t n, const int32_t *n_checks, const int32_t *
         frame_ok[f] = (uint8_t)ok;
         free(xhat); free(L);
     }
-    for (int32_t j = 0; j < m; ++j)
+    for (int32_t j = 0; j < m; ++j) {
         if (row_ptrs[j]) graph_free(&g[j]);
+        free(colour[j]);
+    }
     return ORC_OK;
 }

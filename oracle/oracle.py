@@ -59,11 +59,11 @@ def _load():
             L.orc_layers.argtypes = [ctypes.c_int32, ctypes.c_int32, _i32p, _i32p, _i32p]
             L.orc_bp_layered.argtypes = [ctypes.c_int32, ctypes.c_int32, _i32p, _i32p, _f64p, _u32p,
                                          ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_int,
-                                         _u32p, _u8p, _i32p, _f64p]
+                                         _u32p, _u8p, _i32p, _f64p, _f64p]
             L.orc_reconcile.argtypes = [ctypes.c_int32, ctypes.c_int32, _i32p, ctypes.POINTER(_i32p),
                                         ctypes.POINTER(_i32p), _i32p, _f32p, ctypes.c_double, _f32p,
                                         ctypes.POINTER(_u32p), ctypes.c_int32, ctypes.c_int32,
-                                        ctypes.c_double, ctypes.c_double, _u8p, _u8p, _i32p]
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_int32, _u8p, _u8p, _i32p]
             for name in ("orc_quantise", "orc_slice_bits", "orc_syndrome", "orc_llr_slice",
                          "orc_llr_biawgn", "orc_bp_decode", "orc_bp_trace", "orc_reconcile", "orc_layers", "orc_bp_layered"):
                 getattr(L, name).restype = ctypes.c_int
@@ -164,8 +164,9 @@ def layers(code) -> np.ndarray:
 
 
 def bp_decode_layered(code, llr: np.ndarray, synd: np.ndarray, max_iter: int = 100, q_max: float = 40.0,
-                      stop_early: bool = True):
-    """Row-layered sum-product (reading R-9).  -> (bits, converged, iters, post float64[F][n])."""
+                      stop_early: bool = True, want_r: bool = False):
+    """Row-layered sum-product (reading R-9).  -> (bits, converged, iters, post float64[F][n])
+    (+ r float64[F][E], the check-to-variable messages in CSR edge order, if want_r)."""
     llr = np.ascontiguousarray(llr, np.float64).reshape(-1, code.n)
     F = llr.shape[0]
     synd = np.ascontiguousarray(synd, np.uint32).reshape(F, words(code.m_checks))
@@ -173,11 +174,19 @@ def bp_decode_layered(code, llr: np.ndarray, synd: np.ndarray, max_iter: int = 1
     conv = np.empty(F, np.uint8)
     iters = np.empty(F, np.int32)
     post = np.empty((F, code.n), np.float64)
+    r = np.empty((F, code.n_edges), np.float64) if want_r else None
     _chk(_load().orc_bp_layered(code.n, code.m_checks, _p(code.row_ptr, _i32p), _p(code.col_idx, _i32p),
                                 _p(llr, _f64p), _p(synd, _u32p), F, max_iter, float(q_max), int(stop_early),
-                                _p(bits, _u32p), _p(conv, _u8p), _p(iters, _i32p), _p(post, _f64p)),
+                                _p(bits, _u32p), _p(conv, _u8p), _p(iters, _i32p), _p(post, _f64p),
+                                _p(r, _f64p) if want_r else None),
          "bp_layered")
-    return bits, conv, iters, post
+    return (bits, conv, iters, post, r) if want_r else (bits, conv, iters, post)
+
+
+def bp_trace_layered(code, llr: np.ndarray, synd: np.ndarray, k_iters: int, q_max: float = 40.0):
+    """Row-layered schedule after exactly k iterations: -> (r float64[F][E] CSR order, post float64[F][n])."""
+    _, _, _, post, r = bp_decode_layered(code, llr, synd, k_iters, q_max, stop_early=False, want_r=True)
+    return r, post
 
 
 def bp_trace(code, llr: np.ndarray, synd: np.ndarray, k_iters: int, q_max: float = 40.0):
@@ -193,10 +202,14 @@ def bp_trace(code, llr: np.ndarray, synd: np.ndarray, k_iters: int, q_max: float
     return c2v, post
 
 
+SCHEDULES = {"flooding": 0, "layered": 1}
+
+
 def reconcile(codes: Sequence, order: Sequence[int], edges: np.ndarray, sigma_n: float,
               x: np.ndarray, synd: Sequence[np.ndarray], max_iter: int = 100,
-              q_max: float = 40.0, llr_max: float = 40.0):
+              q_max: float = 40.0, llr_max: float = 40.0, schedule: str = "flooding"):
     """Multi-stage driver O6.  codes[j] None => disclosed, synd[j] = Bob's packed bits.
+    schedule: "flooding" (O5, reading A-8) or "layered" (O5', reading R-9) BP for the coded slices.
 
     -> (label uint8[F][n], frame_ok uint8[F], iters int32[F][m])."""
     m = len(codes)
@@ -214,6 +227,7 @@ def reconcile(codes: Sequence, order: Sequence[int], edges: np.ndarray, sigma_n:
     iters = np.empty((F, m), np.int32)
     _chk(_load().orc_reconcile(m, n, _p(nch, _i32p), rp, ci, _p(order, _i32p), _p(edges, _f32p),
                                float(sigma_n), _p(x, _f32p), sp, F, max_iter, float(q_max),
-                               float(llr_max), _p(label, _u8p), _p(ok, _u8p), _p(iters, _i32p)),
+                               float(llr_max), SCHEDULES[schedule], _p(label, _u8p), _p(ok, _u8p),
+                               _p(iters, _i32p)),
          "reconcile")
     return label, ok, iters
