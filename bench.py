@@ -37,7 +37,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cvsr", choices=["cvsr", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4",
+                    help="workload (cvsr_inputs/configs.py): C4 = the metric's standard settings, N_R = 1e6, "
+                         "125 frames per GPU (1/8 of N = 1e9); C4b = N_R = 5e6, 25 frames per GPU; C2; C3")
     ap.add_argument("--frames", type=int, default=0, help="frames per GPU (0 = config default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -50,6 +52,31 @@ def parse():
 
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def launch_plan(gpus: int, env) -> str:
+    """How this invocation runs: "single" (one process, N = 1), "spawn" (N > 1 requested without a
+    torchrun environment: start N ranks with torch.distributed.run and relay rank 0's line) or
+    "rank" (already one rank of a torchrun job whose WORLD_SIZE must equal --gpus)."""
+    if gpus < 1:
+        raise SystemExit(f"--gpus must be >= 1 (got {gpus})")
+    if "WORLD_SIZE" in env:
+        ws = int(env["WORLD_SIZE"])
+        if ws != gpus:
+            raise SystemExit(f"WORLD_SIZE={ws} but --gpus {gpus}: launch one rank per GPU")
+        return "rank"
+    return "spawn" if gpus > 1 else "single"
+
+
+def spawn_ranks(argv, gpus: int) -> int:
+    """Re-launch this script as `gpus` ranks (one per GPU, NCCL, 127.0.0.1 rendezvous)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
 
 
 def host_cores() -> int:
@@ -120,43 +147,47 @@ def build_workload(cfg_name: str):
 
 # ---------------------------------------------------------------- oracle legs (CPU)
 
-def oracle_sample(cfg, codes_l, frames: int, first_frame: int = 0):
-    """Bounded sample of the workload on the host: the oracle (as it stands) runs
-    Bob (quantise + syndromes) and Alice (reconcile) on `frames` frames."""
+def oracle_sample(cfg, codes_l, frames: int, first_frame: int = 0, schedule: str = "layered"):
+    """Bounded sample of the workload on the host: the oracle (as it stands) runs Bob (quantise +
+    syndromes) and Alice (the multi-stage reconcile with the same BP schedule as the CUDA arm) on
+    `frames` frames; OpenMP spreads the frames over the host cores (one frame per core at a time)."""
     import oracle
     from cvsr_inputs import awgn
     x, y = awgn.quadratures(frames, cfg.n, cfg.gamma, seed=awgn.DATA_SEED + 7, first_frame=first_frame)
     t0 = time.perf_counter()
     lab = oracle.quantise(cfg.edges(), y)
     synd = [oracle.slice_bits(lab, j) if c is None else oracle.syndrome(c, lab, j) for j, c in enumerate(codes_l)]
-    _, ok, _ = oracle.reconcile(codes_l, cfg.order, cfg.edges(), cfg.sigma_n, x, synd, cfg.max_iter)
+    _, ok, _ = oracle.reconcile(codes_l, cfg.order, cfg.edges(), cfg.sigma_n, x, synd, cfg.max_iter,
+                                schedule=schedule)
     dt = time.perf_counter() - t0
     return int(ok.sum()) * cfg.m * cfg.n, dt, int(ok.sum())
 
 
 def run_reference(args):
+    """The reference arm: the fp64 oracle on the box's host cores, same config, metric and BP
+    schedule.  One frame takes a single core tens of seconds at N_R = 1e6, so the K timed steps are
+    K frames reconciled concurrently (OpenMP over frames) and ms_per_step = wall time / K; the W
+    warm-up steps are W frames, untimed."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     import oracle
     cfg, codes_l = build_workload(args.config)
     cores = oracle.num_threads()
-    frames = 4 * max(2, min(cores, 16))  # a few seconds of oracle work per step
-    for _ in range(args.warmup):
-        oracle_sample(cfg, codes_l, frames)
-    bits_total, t_total = 0, 0.0
-    for s in range(args.steps):
-        b, dt, _ = oracle_sample(cfg, codes_l, frames, first_frame=s * frames)
-        bits_total += b
-        t_total += dt
-    v = bits_total / t_total
+    if args.warmup:
+        oracle_sample(cfg, codes_l, min(args.warmup, cores), first_frame=10_000, schedule=args.schedule)
+    frames = max(1, args.steps)
+    bits, t_total, okf = oracle_sample(cfg, codes_l, frames, schedule=args.schedule)
+    v = bits / t_total
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg.name}: m={cfg.m} slices, N_R={cfg.n}, gamma={cfg.gamma}",
-                       "frames_per_step": frames, "sample": True},
+                       "frames_timed": frames, "sample": True, "bp_schedule": args.schedule},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"{frames} frames x N_R={cfg.n} per step (bounded sample of {cfg.name})"},
+                             "sample": f"{frames} frames x N_R={cfg.n} of {cfg.name} (one per step, reconciled "
+                                       f"concurrently on {cores} cores; {args.schedule} BP), {t_total:.1f} s wall, "
+                                       f"{okf} ok"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -165,6 +196,8 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if launch_plan(args.gpus, os.environ) == "spawn":
+        sys.exit(spawn_ranks(sys.argv[1:], args.gpus))
     if args.impl == "reference":
         run_reference(args)
         return
@@ -172,7 +205,6 @@ def main():
     import torch.distributed as dist
 
     from cvsr_inputs.awgn import torch_quadratures
-    os.environ["CVSR_SCHEDULE"] = args.schedule  # read once by libcvsr.so
     from paper_2108_08418_b200 import cvsr
     from paper_2108_08418_b200 import dist as cdist
     from paper_2108_08418_b200.pipeline import SRPipeline
@@ -191,10 +223,10 @@ def main():
     if args.splits > 1:
         from paper_2108_08418_b200.pipeline import SplitPipeline
         pipe = SplitPipeline(args.splits, cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, device,
-                             cfg.max_iter, cfg.q_max)
+                             cfg.max_iter, cfg.q_max, schedule=args.schedule)
     else:
         pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, device, cfg.max_iter, cfg.q_max,
-                          stream)
+                          stream, schedule=args.schedule)
     # rank r owns frames [r F, (r+1) F): per-frame-chunk seeding => identical data for any GPU count
     first, _ = cdist.shard(F, rank)
     x, y = torch_quadratures(F, n, cfg.gamma, device, first_frame=first)
@@ -304,7 +336,7 @@ def main():
         code_h = pipe.parts[0].code_h if args.splits > 1 else pipe.code_h
         ectx = cvsr.cvsr_ctx_create(local, stream)
         sess = cvsr.cvsr_session_create(ectx, cfg.m, code_h, cfg.order, cvsr.make_quantiser(cfg.edges()),
-                                        cfg.sigma_n, n, F, cvsr.decode_opts(cfg.max_iter, cfg.q_max))
+                                        cfg.sigma_n, n, F, cvsr.decode_opts(cfg.max_iter, cfg.q_max, args.schedule))
         cvsr.cvsr_session_set_verify(sess, 0x5DEECE66D)
         # the serving loop: K batches through cvsr_session_run_host_stream, batch b+1's H2D and
         # batch b-1's D2H overlapping batch b's kernels; every batch's copies are inside the
@@ -422,17 +454,18 @@ def main():
     if not args.no_cpu_baseline:
         import oracle
         cores = oracle.num_threads()
-        # batches of one frame per core until ~10 s of CPU work (a bounded sample of the workload)
+        # one wave of one frame per core (a bounded sample of the workload: tens of seconds at
+        # N_R = 1e6, ~10 s at 2^16), batches repeated until ~10 s of CPU work for small frames
         frames_s = max(2, min(cores, 16))
         b = okc = nb = 0
         dt = 0.0
         while nb == 0 or (dt < 10.0 and nb < 40):
-            bb, tt, oo = oracle_sample(cfg, codes_l, frames_s, first_frame=nb * frames_s)
+            bb, tt, oo = oracle_sample(cfg, codes_l, frames_s, first_frame=nb * frames_s, schedule=args.schedule)
             b, dt, okc, nb = b + bb, dt + tt, okc + oo, nb + 1
         frames_s *= nb
         cpu = {"value": b / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{frames_s} frames x N_R={n} of {cfg.name} (quantise+syndromes+reconcile), "
-                         f"{dt:.1f} s wall, {okc} ok"}
+               "sample": f"{frames_s} frames x N_R={n} of {cfg.name} (quantise+syndromes+reconcile, "
+                         f"{args.schedule} BP as the CUDA arm), {dt:.1f} s wall, {okc} ok"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

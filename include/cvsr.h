@@ -42,13 +42,9 @@
  *    CVSR_SUBS [auto]: frames per lane (1, 2, 4); CVSR_FUSED [0] and
  *    CVSR_CN_TMA [0]: experimental schedulers.  The SMEM, GRAPH,
  *    COMPACT, SUBS and FUSED variants are tested bit-identical to the default
- *    path.  CVSR_SCHEDULE [flooding]: "layered" selects the row-layered BP
- *    schedule (reading R-9; PAPER.md:189 leaves the schedule open)
- *    for cvsr_decode, cvsr_reconcile and the sessions -- a different
- *    algorithm, tested against the oracle's layered decoder rather than
- *    bit-identical to flooding; cvsr_decode_trace stays flooding.  A code
- *    needing more than 48 layers or with check degree > 12 then fails with
- *    CVSR_EINVAL.  bench.py selects it by default (--schedule).
+ *    path.  CVSR_SCHEDULE [flooding]: "layered" makes the row-layered
+ *    schedule the default of calls whose cvsr_decode_opts.flags leave the
+ *    schedule unset (CVSR_SCHED_DEFAULT); the flags select it per call.
  *  - Layouts.  "frame-major" arrays are [frames][n] row-major.  Packed bit
  *    vectors put bit i at bit (i mod 32) of 32-bit word floor(i/32); a
  *    vector of B bits occupies ceil(B/32) words per frame; padding bits are
@@ -65,7 +61,7 @@
 extern "C" {
 #endif
 
-#define CVSR_ABI_VERSION 1
+#define CVSR_ABI_VERSION 2
 
 typedef int32_t cvsr_status;
 #define CVSR_OK 0
@@ -162,15 +158,31 @@ cvsr_status cvsr_llr_biawgn(cvsr_ctx *ctx, const float *y, int64_t count, float 
 
 /* ------------------------------------------------------------- Alice: BP */
 /* max_iter >= 0 (reading A-9); msg_clamp = Q_MAX > 0, the V2C clamp
- * (reading A-10, 40); flags reserved (0). */
+ * (reading A-10, 40); flags bits 0-1 = BP schedule (PAPER.md:189 names
+ * sum-product BP without fixing its schedule):
+ *   CVSR_SCHED_DEFAULT   the process default (env CVSR_SCHEDULE=layered, else flooding);
+ *   CVSR_SCHED_FLOODING  flooding: all checks, then all variables (reading A-8);
+ *   CVSR_SCHED_LAYERED   row-layered (reading R-9): the checks are greedily
+ *     coloured in index order into layers that share no variable (check c takes the
+ *     smallest colour not used by an earlier check sharing a variable) and an iteration
+ *     updates the layers in order against the running posteriors:
+ *     q_e = post_v - r_e, r_e <- (1 - 2 s_c) BOXPLUS_{e' != e} clamp(q_e'), post_v <- q_e + r_e.
+ *     Same stopping rule as flooding.  A code that needs more than 48 layers or has a
+ *     check degree > 12 is decoded with flooding instead (cvsr_stats.schedule reports
+ *     what ran).  Other flag bits must be 0. */
+#define CVSR_SCHED_DEFAULT 0
+#define CVSR_SCHED_FLOODING 1
+#define CVSR_SCHED_LAYERED 2
+#define CVSR_SCHED_MASK 3
 typedef struct {
     int32_t max_iter;
     float msg_clamp;
     int32_t flags;
 } cvsr_decode_opts;
 
-/* Syndrome-based flooding sum-product BP (
- * SURVEY.md §8(c) O5) of `frames` independent sub-blocks sharing code H:
+/* Syndrome-based sum-product BP (SURVEY.md §8(c)
+ * O5, flooding, or O5' row-layered per opts->flags) of `frames` independent
+ * sub-blocks sharing code H (flooding shown; layered: see CVSR_SCHED_LAYERED):
  *  k = 0 decision xhat = [L < 0]; iterations k = 1..max_iter of
  *  CN r_e = (1-2 s_c) BOXPLUS_{e' != e} q_e', VN post = L + sum r,
  *  q_e = clamp(post - r_e), xhat = [post < 0]; a frame stops at the first k
@@ -185,9 +197,12 @@ cvsr_status cvsr_decode(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, 
 /* Parity/debug: exactly k_iters >= 1 iterations, no early stop; c2v_out
  * float[frames][E] = C2V messages r_e of iteration k in CSR edge order,
  * post_out float[frames][n_vars] = posteriors of iteration k.  Either output
- * may be NULL. */
+ * may be NULL.  flags: the schedule, as cvsr_decode_opts.flags
+ * (CVSR_SCHED_LAYERED on a code the layered schedule does not support:
+ * CVSR_EINVAL). */
 cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, const uint32_t *synd,
-                              int32_t frames, int32_t k_iters, float msg_clamp, float *c2v_out, float *post_out);
+                              int32_t frames, int32_t k_iters, float msg_clamp, int32_t flags, float *c2v_out,
+                              float *post_out);
 
 /* ------------------------------------------------------------- scheduler */
 /* Per-run statistics (host struct).  Slice arrays are indexed by slice j. */
@@ -200,6 +215,8 @@ typedef struct {
     int64_t iters_sum[8];     /* sum of BP iterations D_j over attempted frames       */
     int64_t edge_iters[8];    /* sum over attempted frames of E_j * D_j               */
     double alice_seconds;     /* device time of the call (CUDA events)                */
+    int32_t schedule[8];      /* schedule slice j ran with: 0 disclosed, CVSR_SCHED_FLOODING or
+                                 CVSR_SCHED_LAYERED                                    */
 } cvsr_stats;
 
 /* Multi-stage sliced reconciliation, Alice's side (PAPER.md:114 steps 4-6,

@@ -160,9 +160,9 @@ bool fused_enabled() {
     return v == 1;
 }
 
-// BP schedule: CVSR_SCHEDULE=layered selects the row-layered schedule (reading R-9),
-// anything else the flooding schedule (reading A-8)
-bool layered_enabled() {
+// Process-default BP schedule: CVSR_SCHEDULE=layered selects the row-layered schedule (reading
+// R-9), anything else the flooding schedule (reading A-8); per call, cvsr_decode_opts.flags wins.
+bool layered_env() {
     static const int v = [] {
         const char *e = getenv("CVSR_SCHEDULE");
         return (e && strcmp(e, "layered") == 0) ? 1 : 0;
@@ -170,9 +170,17 @@ bool layered_enabled() {
     return v != 0;
 }
 
+bool layered_requested(int32_t flags) {
+    const int sch = flags & CVSR_SCHED_MASK;
+    if (sch == CVSR_SCHED_LAYERED) return true;
+    if (sch == CVSR_SCHED_FLOODING) return false;
+    return layered_env();
+}
+
 // frames per lane: choose_subs(frames), narrowed in fused mode so that one tile's
-// message lines (E x 128 S bytes) stay well inside L2 for the CN -> VN hand-off
-int pick_subs(int32_t frames, int64_t E) {
+// message lines (E x 128 S bytes) stay well inside L2 for the CN -> VN hand-off.
+// layered: the schedule that will actually run for this code (after the fallback).
+int pick_subs(int32_t frames, int64_t E, bool layered, int32_t max_dc) {
     int s = choose_subs(frames);
     static int forced = -1;
     if (forced < 0) {
@@ -180,9 +188,12 @@ int pick_subs(int32_t frames, int64_t E) {
         forced = e ? atoi(e) : 0;
     }
     if (forced == 1 || forced == 2 || forced == 4) return std::min(forced, s == 4 ? 4 : std::max(s, forced));
-    // layered schedule: 2 frames per lane (64-frame tiles) measured faster on C2 (51.6 vs 56.0 ms per
-    // step): k_layer<5, 2> needs 60 registers without spills, k_layer<5, 4> spills at 64
-    if (layered_enabled() && s > 2) s = 2;
+    if (layered) {
+        // 2 frames per lane (64-frame tiles) measured faster on C2 (51.6 vs 56.0 ms per step):
+        // k_layer<5, 2> needs 60 registers without spills, k_layer<5, 4> spills at 64.  Check
+        // degrees above 6 take one frame per lane (k_layer<DC, 1>: no spills up to DC = 12).
+        s = std::min(s, max_dc > 6 ? 1 : 2);
+    }
     static double cap = -1.0;
     if (cap < 0.0) {
         const char *e = getenv("CVSR_FUSED_MB");  // experiment switch: per-tile L2 budget (MB)
@@ -321,7 +332,7 @@ DecState carve_decstate(Carve &cv, int tiles, int frames, int subs, int64_t n, i
 // are launched LOOKAHEAD ahead of a mapped-memory progress counter written by
 // the status kernel; the counter also bounds the grid's tile dimension.
 cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0, int max_iter, float qmax,
-                       uint32_t *bits_out, const CompactArena *ca = nullptr) {
+                       uint32_t *bits_out, const CompactArena *ca, bool layered) {
     cudaStream_t s = ctx->stream;
     const CodeDev &cd = code->d;
     volatile int32_t *hc = ctx->host_counts;
@@ -335,10 +346,7 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
     // compaction arenas: index 0 = ds0's buffers, 1 = ca's; slot_frame alternates between ca's two maps
     int arena = 0, n_compact = 0;
     const int T = ds0.tile_frames;
-    const bool layered = layered_enabled();
-    if (layered && !layered_supported(cd))
-        return fail(CVSR_EINVAL, "layered schedule: code needs more than %d layers or has check degree %d > 12",
-                    MAX_LAYERS, cd.max_dc);
+    layered = layered && layered_supported(cd);  // otherwise flooding (cvsr_decode_opts doc)
     if (!layered && smem_enabled() && !fused && decode_smem_bytes(cd) <= smem_limit() &&
         launch_decode_smem(cd, ds0, max_iter, qmax, bits_out, s))
         return check_launch(ctx, 1);
@@ -927,6 +935,8 @@ static cvsr_status check_opts(const cvsr_decode_opts *o) {
     if (!o) return fail(CVSR_EINVAL, "null decode opts");
     if (o->max_iter < 0 || o->max_iter > 1000000) return fail(CVSR_EINVAL, "max_iter=%d", o->max_iter);
     if (!(o->msg_clamp > 0.0f)) return fail(CVSR_EINVAL, "msg_clamp must be > 0");
+    if ((o->flags & ~CVSR_SCHED_MASK) || (o->flags & CVSR_SCHED_MASK) == CVSR_SCHED_MASK)
+        return fail(CVSR_EINVAL, "flags=%d: unknown bits", o->flags);
     return CVSR_OK;
 }
 
@@ -942,7 +952,8 @@ cvsr_status cvsr_decode(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, 
     if (!llr || !synd || !bits_out || !converged_out || !iters_out) return fail(CVSR_EINVAL, "null buffer");
     DeviceGuard g(ctx->device);
     const CodeDev &cd = code->d;
-    const int subs = pick_subs(frames, cd.E);
+    const bool layered = layered_requested(opts->flags) && layered_supported(cd);
+    const int subs = pick_subs(frames, cd.E, layered, cd.max_dc);
     const int tiles = tiles_for(frames, subs);
     const bool comp = compact_enabled() && tiles >= 2;
     char *base;
@@ -960,22 +971,29 @@ cvsr_status cvsr_decode(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, 
     launch_init_tiles(ds, nullptr, s);
     launch_set_counts(ds, tiles, s);
     if (cvsr_status st = check_launch(ctx, 4)) return st;
-    return run_decode(ctx, code, ds, opts->max_iter, opts->msg_clamp, bits_out, comp ? &ca : nullptr);
+    return run_decode(ctx, code, ds, opts->max_iter, opts->msg_clamp, bits_out, comp ? &ca : nullptr, layered);
 }
 
 cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, const uint32_t *synd,
-                              int32_t frames, int32_t k_iters, float msg_clamp, float *c2v_out, float *post_out) {
+                              int32_t frames, int32_t k_iters, float msg_clamp, int32_t flags, float *c2v_out,
+                              float *post_out) {
     if (cvsr_status st = check_ctx(ctx)) return st;
     if (!code) return fail(CVSR_EINVAL, "null code");
     if (code->device != ctx->device) return fail(CVSR_EINVAL, "code and context on different devices");
     if (k_iters < 1) return fail(CVSR_EINVAL, "k_iters must be >= 1");
     if (!(msg_clamp > 0.0f)) return fail(CVSR_EINVAL, "msg_clamp must be > 0");
+    if ((flags & ~CVSR_SCHED_MASK) || (flags & CVSR_SCHED_MASK) == CVSR_SCHED_MASK)
+        return fail(CVSR_EINVAL, "flags=%d: unknown bits", flags);
+    const CodeDev &cd = code->d;
+    const bool layered = layered_requested(flags);
+    if (layered && !layered_supported(cd))
+        return fail(CVSR_EINVAL, "layered trace: code needs more than %d layers or has check degree %d > 12",
+                    MAX_LAYERS, cd.max_dc);
     if (frames < 0) return fail(CVSR_ESHAPE, "frames < 0");
     if (frames == 0) return CVSR_OK;
     if (!llr || !synd) return fail(CVSR_EINVAL, "null buffer");
     DeviceGuard g(ctx->device);
-    const CodeDev &cd = code->d;
-    const int subs = choose_subs(frames);
+    const int subs = layered ? pick_subs(frames, cd.E, true, cd.max_dc) : choose_subs(frames);
     const int tiles = tiles_for(frames, subs);
     const size_t post_bytes = align_up((size_t)tiles * cd.n * LANES * subs * sizeof(float));
     char *base;
@@ -989,7 +1007,24 @@ cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float 
     launch_synd_transpose(synd, frames, cd.M, ds.subs, ds.st, tiles, s);
     launch_init_tiles(ds, nullptr, s);
     launch_set_counts(ds, tiles, s);
-    int launched = 4 + launch_vn(cd, ds, tiles, msg_clamp, true, nullptr, s);
+    int launched = 4;
+    if (layered) {
+        // r = 0, post = L; k sweeps over the layers; r_e is in ds.msg (CSR slots), post_v in ds.L
+        CK(cudaMemsetAsync(ds.msg, 0, (size_t)tiles * cd.E * LANES * subs * sizeof(float), s));
+        launch_layer_init(cd, ds, tiles, s);
+        ++launched;
+        for (int k = 1; k <= k_iters; ++k) launched += launch_layers(cd, ds, tiles, msg_clamp, s);
+        if (c2v_out) {
+            launch_from_interleaved(ds.msg, c2v_out, frames, cd.E, tiles, ds.subs, LN2, s);
+            ++launched;
+        }
+        if (post_out) {
+            launch_from_interleaved(ds.L, post_out, frames, cd.n, tiles, ds.subs, LN2, s);
+            ++launched;
+        }
+        return check_launch(ctx, launched);
+    }
+    launched += launch_vn(cd, ds, tiles, msg_clamp, true, nullptr, s);
     for (int k = 1; k <= k_iters; ++k) {
         launch_cn(cd, ds, tiles, msg_clamp, 0, s);
         ++launched;
@@ -1018,7 +1053,6 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
     if (frames < 0 || n <= 0) return fail(CVSR_ESHAPE, "frames=%d n=%d", frames, n);
     if (!(sigma_n > 0.0f)) return fail(CVSR_EINVAL, "sigma_n must be > 0");
     uint32_t seen = 0u;
-    int64_t maxE = 1, maxM = 1;
     for (int t = 0; t < m; ++t) {
         const int j = order[t];
         if (j < 0 || j >= m || ((seen >> j) & 1u)) return fail(CVSR_EINVAL, "order is not a permutation of 0..m-1");
@@ -1028,8 +1062,6 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
         if (codes[j]) {
             if (codes[j]->device != ctx->device) return fail(CVSR_EINVAL, "code %d on another device", j);
             if (codes[j]->d.n != n) return fail(CVSR_ESHAPE, "code %d has n=%d, expected %d", j, codes[j]->d.n, n);
-            maxE = std::max<int64_t>(maxE, codes[j]->d.E);
-            maxM = std::max<int64_t>(maxM, codes[j]->d.M);
         }
         if (frames > 0 && !synd[j]) return fail(CVSR_EINVAL, "synd[%d] is null", j);
     }
@@ -1039,23 +1071,43 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
     }
     if (!x || !label_out || !frame_ok || !iters) return fail(CVSR_EINVAL, "null buffer");
     DeviceGuard g(ctx->device);
-    const int subs = pick_subs(frames, maxE);
-    const int tiles = tiles_for(frames, subs);
-    const bool comp = compact_enabled() && tiles >= 2;
+    // per coded slice: the schedule that runs (layered falls back to flooding for codes it does not
+    // support), frames per lane and decoder state size; the decoder state of every slice is carved
+    // from the same region after the per-call buffers
+    const bool want_layered = layered_requested(opts->flags);
+    bool lay_j[8] = {};
+    int subs_j[8] = {}, tiles_j[8] = {};
+    bool comp_j[8] = {};
+    size_t dec_bytes = 0;
+    for (int j = 0; j < m; ++j) {
+        if (!codes[j]) continue;
+        const CodeDev &cd = codes[j]->d;
+        lay_j[j] = want_layered && layered_supported(cd);
+        subs_j[j] = pick_subs(frames, cd.E, lay_j[j], cd.max_dc);
+        tiles_j[j] = tiles_for(frames, subs_j[j]);
+        comp_j[j] = compact_enabled() && tiles_j[j] >= 2;
+        size_t b = decstate_bytes(tiles_j[j], frames, subs_j[j], n, cd.M, cd.E);
+        if (comp_j[j]) b += compact_bytes(tiles_j[j], subs_j[j], n, cd.M, cd.E);
+        dec_bytes = std::max(dec_bytes, b);
+    }
     const int Wn = words_of(n);
-    size_t bytes = decstate_bytes(tiles, frames, subs, n, maxM, maxE);
-    if (comp) bytes += compact_bytes(tiles, subs, n, maxM, maxE);
-    bytes += (size_t)m * align_up((size_t)frames * Wn * 4) + 3 * align_up((size_t)frames);
+    size_t bytes = (size_t)m * align_up((size_t)frames * Wn * 4) + 3 * align_up((size_t)frames) +
+                   align_up((size_t)frames * sizeof(int32_t)) + align_up((size_t)frames);
+    bytes += dec_bytes;
     char *base;
     if (cvsr_status st = scratch_reserve(ctx, bytes, &base)) return st;
     Carve cv{base};
-    DecState ds = carve_decstate(cv, tiles, frames, subs, n, maxM, maxE, nullptr, nullptr);
-    CompactArena ca;
-    if (comp) ca = carve_compact(cv, tiles, subs, n, maxM, maxE);
     uint32_t *bits_dec[8] = {};
     for (int j = 0; j < m; ++j) bits_dec[j] = cv.take<uint32_t>((size_t)frames * Wn * 4);
     uint8_t *alive = cv.take<uint8_t>((size_t)frames);
     uint8_t *attempt = cv.take<uint8_t>((size_t)2 * frames);
+    int32_t *dec_iters = cv.take<int32_t>((size_t)frames * sizeof(int32_t));
+    uint8_t *dec_conv = cv.take<uint8_t>((size_t)frames);
+    char *dec_base = base + cv.off;
+    DecState ds0{};  // frame count for the hand-off of disclosed slices
+    ds0.frames = frames;
+    ds0.iters = dec_iters;
+    ds0.conv = dec_conv;
     cudaStream_t s = ctx->stream;
     CK(cudaEventRecord(ctx->t0, s));
     launch_fill_i32(iters, (int64_t)frames * m, -1, s);
@@ -1067,26 +1119,30 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
     for (int t = 0; t < m; ++t) {
         const int j = order[t];
         if (!codes[j]) {
-            launch_slice_done(ds, m, j, 1, alive, attempt, iters, s);
+            launch_slice_done(ds0, m, j, 1, alive, attempt, iters, s);
             ++launched;
             known_bits[j] = synd[j];
         } else {
             const CodeDev &cd = codes[j]->d;
+            Carve cvd{dec_base};
+            DecState ds = carve_decstate(cvd, tiles_j[j], frames, subs_j[j], n, cd.M, cd.E, dec_iters, dec_conv);
+            CompactArena ca;
+            if (comp_j[j]) ca = carve_compact(cvd, tiles_j[j], subs_j[j], n, cd.M, cd.E);
             CK(cudaMemsetAsync(bits_dec[j], 0, (size_t)frames * Wn * 4, s));
             launch_init_tiles(ds, alive, s);
-            launch_set_counts(ds, tiles, s);
-            launch_synd_transpose(synd[j], frames, cd.M, ds.subs, ds.st, tiles, s);
+            launch_set_counts(ds, tiles_j[j], s);
+            launch_synd_transpose(synd[j], frames, cd.M, ds.subs, ds.st, tiles_j[j], s);
             LlrParams p;
             fill_llr_params(p, q, j, known_mask, sigma_n, opts->msg_clamp);
             for (int jj = 0; jj < m; ++jj) p.known_bits[jj] = known_bits[jj];
             prof_begin(ctx, KC_INIT);
             if (cvsr_status st = prepare_llr_table(ctx, p, &launched)) return st;
-            launch_llr_interleaved(p, x, frames, n, tiles, ds.subs, ds.L, s);
+            launch_llr_interleaved(p, x, frames, n, tiles_j[j], ds.subs, ds.L, s);
             prof_end(ctx);
             launched += 4;
             if (cvsr_status st = check_launch(ctx, 0)) return st;
             if (cvsr_status st = run_decode(ctx, codes[j], ds, opts->max_iter, opts->msg_clamp, bits_dec[j],
-                                            comp ? &ca : nullptr))
+                                            comp_j[j] ? &ca : nullptr, lay_j[j]))
                 return st;
             launch_slice_done(ds, m, j, 0, alive, attempt, iters, s);
             ++launched;
@@ -1115,6 +1171,7 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
             stats_out->converged[j] = (int64_t)acc[9 + j];
             stats_out->iters_sum[j] = (int64_t)acc[17 + j];
             stats_out->edge_iters[j] = codes[j] ? (int64_t)acc[17 + j] * codes[j]->d.E : 0;
+            stats_out->schedule[j] = codes[j] ? (lay_j[j] ? CVSR_SCHED_LAYERED : CVSR_SCHED_FLOODING) : 0;
         }
         float ms = 0.0f;
         CK(cudaEventElapsedTime(&ms, ctx->t0, ctx->t1));

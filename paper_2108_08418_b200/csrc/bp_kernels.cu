@@ -1612,6 +1612,14 @@ __global__ void __launch_bounds__(BLOCK) k_layer_init(CodeDev cd, DecState ds) {
 template <int DC, int S, typename VarOf>
 __device__ __forceinline__ void layer_check(const CodeDev &cd, const DecState &ds, int t, const uint4 &act, int lo,
                                             int deg, uint32_t sb, VarOf var_of, int lane, float qmax2) {
+    if constexpr (DC >= 6) {
+        // degree-2 checks in a code with a large maximum degree (MET-style type-A checks): a
+        // 2-edge body instead of DC - 2 dummy edges (deg is warp-uniform)
+        if (deg <= 2) {
+            layer_check<2, S>(cd, ds, t, act, lo, deg, sb, var_of, lane, qmax2);
+            return;
+        }
+    }
     const uint32_t al = lane_act<S>(act, lane);
     float *mt = ds.msg + ((size_t)t * cd.E + lo) * LANES * S + (size_t)lane * S;
     float *Lt = ds.L + (size_t)t * cd.n * LANES * S + (size_t)lane * S;
@@ -1661,9 +1669,15 @@ constexpr int LCPW = CVSR_LAYER_CPW;  // checks per warp in k_layer
 // A warp takes CPW checks of the layer.  When CPW x DC <= 32 their check ids, row bounds and
 // column indices are fetched up front with one load per lane (no dependent index loads per
 // check); otherwise per check.
+// Blocks per SM: the most that ptxas fits without spills (64 / 80 / 128 registers per thread
+// for 4 / 3 / 2 blocks of 256 threads; -Xptxas -v of this build)
+__host__ __device__ constexpr int layer_minb(int DC, int S) {
+    return S == 1 ? (DC <= 7 ? CVSR_LAYER_MINB : (DC <= 10 ? 3 : 2))
+                  : (S == 2 ? (DC <= 5 ? CVSR_LAYER_MINB : (DC <= 6 ? 3 : 2)) : (DC <= 3 ? 3 : 2));
+}
 template <int DC, int S>
-__global__ void __launch_bounds__(BLOCK, (DC * S <= 20) ? CVSR_LAYER_MINB : (DC * S <= 24 ? 3 : 2))
-    k_layer(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2) {
+__global__ void __launch_bounds__(BLOCK, layer_minb(DC, S)) k_layer(CodeDev cd, DecState ds, int lbeg, int lcnt,
+                                                                    float qmax2) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
     const int t = ds.active_list[ti];
@@ -1711,8 +1725,11 @@ static bool launch_layer_s(const CodeDev &cd, const DecState &ds, dim3 grid, int
         case 4: k_layer<4, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
         case 5: k_layer<5, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
         case 6: k_layer<6, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
-        case 7: case 8: k_layer<8, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
-        case 9: case 10: case 11: case 12: k_layer<12, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 7: k_layer<7, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 8: k_layer<8, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 9: k_layer<9, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 10: k_layer<10, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 11: case 12: k_layer<12, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
         default: return false;
     }
 }

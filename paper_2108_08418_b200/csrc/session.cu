@@ -187,6 +187,7 @@ cvsr_status cvsr_session_run_host(cvsr_session *s, const float *x_host, const fl
                 stats_out->converged[j] += cst.converged[j];
                 stats_out->iters_sum[j] += cst.iters_sum[j];
                 stats_out->edge_iters[j] += cst.edge_iters[j];
+                stats_out->schedule[j] = cst.schedule[j];
             }
             stats_out->alice_seconds += cst.alice_seconds;
         }

@@ -45,13 +45,13 @@ class cvsr_stats(ctypes.Structure):
     _fields_ = [("frames", ctypes.c_int64), ("frames_ok", ctypes.c_int64), ("bits_reconciled", ctypes.c_int64),
                 ("attempted", ctypes.c_int64 * 8), ("converged", ctypes.c_int64 * 8),
                 ("iters_sum", ctypes.c_int64 * 8), ("edge_iters", ctypes.c_int64 * 8),
-                ("alice_seconds", ctypes.c_double)]
+                ("alice_seconds", ctypes.c_double), ("schedule", ctypes.c_int32 * 8)]
 
     def as_dict(self, m: int) -> dict:
         return {"frames": self.frames, "frames_ok": self.frames_ok, "bits_reconciled": self.bits_reconciled,
                 "attempted": list(self.attempted)[:m], "converged": list(self.converged)[:m],
                 "iters_sum": list(self.iters_sum)[:m], "edge_iters": list(self.edge_iters)[:m],
-                "alice_seconds": self.alice_seconds}
+                "alice_seconds": self.alice_seconds, "schedule": list(self.schedule)[:m]}
 
 
 _vp = ctypes.c_void_p
@@ -77,7 +77,7 @@ _SIGS = {
     "cvsr_llr_slice": ([_vp, _P(cvsr_quantiser), _vp, _i32, _i32, _f32, _i32, _u32, _vp, _f32, _vp], _i32),
     "cvsr_llr_biawgn": ([_vp, _vp, _i64, _f32, _f32, _vp], _i32),
     "cvsr_decode": ([_vp, _vp, _vp, _vp, _i32, _P(cvsr_decode_opts), _vp, _vp, _vp], _i32),
-    "cvsr_decode_trace": ([_vp, _vp, _vp, _vp, _i32, _i32, _f32, _vp, _vp], _i32),
+    "cvsr_decode_trace": ([_vp, _vp, _vp, _vp, _i32, _i32, _f32, _i32, _vp, _vp], _i32),
     "cvsr_reconcile": ([_vp, _i32, _P(_vp), _P(_i32), _P(cvsr_quantiser), _f32, _vp, _P(_vp), _i32, _i32,
                         _P(cvsr_decode_opts), _vp, _vp, _vp, _P(cvsr_stats)], _i32),
     "cvsr_count_errors": ([_vp, _vp, _vp, _vp, _i32, _i32, _P(_i64)], _i32),
@@ -228,7 +228,14 @@ def cvsr_llr_biawgn(ctx: int, y, count: int, sigma2: float, llr_max: float, llr_
     _call("cvsr_llr_biawgn", ctx, _ptr(y), count, sigma2, llr_max, _ptr(llr_out))
 
 
+CVSR_SCHED_DEFAULT, CVSR_SCHED_FLOODING, CVSR_SCHED_LAYERED = 0, 1, 2
+SCHED = {"default": CVSR_SCHED_DEFAULT, "flooding": CVSR_SCHED_FLOODING, "layered": CVSR_SCHED_LAYERED}
+
+
 def decode_opts(max_iter: int = 100, msg_clamp: float = 40.0, flags: int = 0) -> cvsr_decode_opts:
+    """flags: CVSR_SCHED_* (an int, or a schedule name "flooding" / "layered" / "default")."""
+    if isinstance(flags, str):
+        flags = SCHED[flags]
     return cvsr_decode_opts(max_iter, msg_clamp, flags)
 
 
@@ -239,8 +246,10 @@ def cvsr_decode(ctx: int, code: int, llr, synd, frames: int, opts: cvsr_decode_o
 
 
 def cvsr_decode_trace(ctx: int, code: int, llr, synd, frames: int, k_iters: int, msg_clamp: float, c2v_out,
-                      post_out) -> None:
-    _call("cvsr_decode_trace", ctx, code, _ptr(llr), _ptr(synd), frames, k_iters, msg_clamp, _ptr(c2v_out),
+                      post_out, flags=CVSR_SCHED_FLOODING) -> None:
+    if isinstance(flags, str):
+        flags = SCHED[flags]
+    _call("cvsr_decode_trace", ctx, code, _ptr(llr), _ptr(synd), frames, k_iters, msg_clamp, flags, _ptr(c2v_out),
           _ptr(post_out))
 
 

@@ -21,14 +21,15 @@ class SRPipeline:
     """
 
     def __init__(self, m: int, edges, codes: Sequence, order: Sequence[int], sigma_n: float, n: int, frames: int,
-                 device: torch.device, max_iter: int = 100, msg_clamp: float = 40.0, stream=None):
+                 device: torch.device, max_iter: int = 100, msg_clamp: float = 40.0, stream=None,
+                 schedule: str = "default"):
         self.m, self.n, self.frames, self.device = m, n, frames, device
         self.order = list(order)
         self.sigma_n = float(sigma_n)
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
         self.ctx = cvsr.cvsr_ctx_create(device.index or 0, self.stream)
         self.q = cvsr.make_quantiser(edges)
-        self.opts = cvsr.decode_opts(max_iter, msg_clamp)
+        self.opts = cvsr.decode_opts(max_iter, msg_clamp, schedule)  # BP schedule: cvsr_decode_opts.flags
         self.code_h: List[Optional[int]] = []
         self.code_E: List[int] = []
         for c in codes:
@@ -106,14 +107,16 @@ class SplitPipeline:
     """
 
     def __init__(self, k: int, m: int, edges, codes: Sequence, order: Sequence[int], sigma_n: float, n: int,
-                 frames: int, device: torch.device, max_iter: int = 100, msg_clamp: float = 40.0):
+                 frames: int, device: torch.device, max_iter: int = 100, msg_clamp: float = 40.0,
+                 schedule: str = "default"):
         import concurrent.futures as cf
         self.k = k
         self.frames, self.n, self.m = frames, n, m
         bounds = [frames * i // k for i in range(k + 1)]
         self.ranges = [(bounds[i], bounds[i + 1]) for i in range(k)]
         self.streams = [torch.cuda.Stream(device) for _ in range(k)]
-        self.parts = [SRPipeline(m, edges, codes, order, sigma_n, n, b - a, device, max_iter, msg_clamp, stream=s)
+        self.parts = [SRPipeline(m, edges, codes, order, sigma_n, n, b - a, device, max_iter, msg_clamp, stream=s,
+                                 schedule=schedule)
                       for (a, b), s in zip(self.ranges, self.streams)]
         self.pool = cf.ThreadPoolExecutor(max_workers=k)
         self.device = device

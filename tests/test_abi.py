@@ -41,7 +41,7 @@ def test_sass_is_sm100a(lib):
 
 def test_abi_version_and_error_paths_without_gpu(lib):
     from paper_2108_08418_b200 import cvsr
-    assert cvsr.cvsr_abi_version() == 1
+    assert cvsr.cvsr_abi_version() == 2
     with pytest.raises(cvsr.CvsrError) as ei:
         cvsr._call("cvsr_ctx_sync", None)
     assert ei.value.status == cvsr.CVSR_EINVAL

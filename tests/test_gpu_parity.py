@@ -278,10 +278,10 @@ def test_decode_edge_cases(cv, ctx):
 
 # ------------------------------------------------------------------ reconcile
 
-def _run_reconcile(cv, cfg, codes_l, x, y, F, n, max_iter=100):
+def _run_reconcile(cv, cfg, codes_l, x, y, F, n, max_iter=100, schedule="default"):
     from paper_2108_08418_b200.pipeline import SRPipeline
     pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, torch.device("cuda:0"),
-                      max_iter=max_iter)
+                      max_iter=max_iter, schedule=schedule)
     stats_ = pipe.step(dev(x), dev(y), want_stats=True)
     torch.cuda.synchronize()
     out = dict(label=pipe.label_alice.cpu().numpy(), ok=pipe.frame_ok.cpu().numpy(), iters=pipe.iters.cpu().numpy(),
@@ -757,60 +757,3 @@ np.savez(sys.argv[1], lab=p.label_alice.cpu().numpy(), ok=p.frame_ok.cpu().numpy
 
 
 # ------------------------------------------------------------------ row-layered schedule (reading R-9)
-
-def _layered_cases():
-    """(name, code, llr float32[F][n], synd, max_iter): C1, C2's coded-slice ensemble at n = 4096
-    (ragged 200 frames) and n = 2048 with 600 frames (compaction), one frame, max_iter = 0."""
-    c1 = codes.regular(1024, 3, 6, seed=configs.CODE_SEED)
-    c2 = codes.irregular_rate(4096, 0.356, seed=3, lam=dict(configs.LAMBDA_C2))
-    c2b = codes.irregular_rate(2048, 0.257, seed=4, lam=dict(configs.LAMBDA_C2))
-    out = []
-    for name, code, F, ebn0, seed, mi in (("c1", c1, 100, 1.5, 1, 100), ("c2s2", c2, 200, 1.0, 2, 100),
-                                           ("c2s3", c2b, 600, 1.5, 3, 100), ("one", c1, 1, 2.0, 4, 100),
-                                           ("zero", c1, 40, 1.5, 5, 0)):
-        u, llr, synd = _channel(code, F, ebn0, seed)
-        out.append((name, code, llr, synd, mi))
-    return out
-
-
-def test_layered_decode_parity(tmp_path):
-    """CVSR_SCHEDULE=layered (subprocess: the switch is read once per process) vs the oracle's
-    row-layered decoder: decisions identical on every frame where the oracle converges, at most
-    2 % of frames with a different D or convergence flag, FER inside the oracle's 95 % interval,
-    and fewer mean iterations than the flooding oracle on the same frames."""
-    import os
-    import subprocess
-    import sys
-    cases = _layered_cases()
-    src = {"names": np.array([c[0] for c in cases])}
-    for name, code, llr, synd, mi in cases:
-        src[f"{name}_dims"] = np.array([code.n, code.m_checks, mi])
-        src[f"{name}_rp"], src[f"{name}_ci"] = code.row_ptr, code.col_idx
-        src[f"{name}_llr"], src[f"{name}_synd"] = llr, synd
-    np.savez(tmp_path / "in.npz", **src)
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = subprocess.run([sys.executable, os.path.join(root, "tests", "_layered_child.py"), str(tmp_path / "in.npz"),
-                          str(tmp_path / "out.npz")], cwd=root, env=dict(os.environ, CVSR_SCHEDULE="layered",
-                                                         PYTHONPATH=os.pathsep.join([root, os.environ.get("PYTHONPATH", "")])),
-                         capture_output=True, text=True, timeout=600)
-    assert res.returncode == 0, res.stderr[-3000:]
-    got = np.load(tmp_path / "out.npz")
-    for name, code, llr, synd, mi in cases:
-        b, cg, it = got[f"{name}_bits"], got[f"{name}_conv"], got[f"{name}_iters"]
-        b_ref, c_ref, i_ref, _ = oracle.bp_decode_layered(code, llr.astype(np.float64), synd, mi)
-        F = len(c_ref)
-        ok = c_ref.astype(bool)
-        assert np.array_equal(b[ok & (cg == 1)], b_ref[ok & (cg == 1)]), name
-        assert np.sum(cg != c_ref) <= max(1, F // 50), (name, int(np.sum(cg != c_ref)))
-        assert np.sum(it != i_ref) <= max(1, F // 50), (name, int(np.sum(it != i_ref)))
-        lo, hi = _clopper_pearson(int(np.sum(c_ref == 0)), F)
-        assert lo <= float(np.mean(cg == 0)) <= hi, name
-        dec = _brute.unpack_bits(b, code.n)
-        s_dec = oracle.syndrome(code, dec, 0)
-        for f in range(F):
-            if cg[f]:
-                assert np.array_equal(s_dec[f], synd[f]), (name, f)
-        if name in ("c1", "c2s2", "c2s3"):
-            _, cf, df = oracle.bp_decode(code, llr.astype(np.float64), synd, mi)
-            both = (cf == 1) & (cg == 1)
-            assert both.sum() >= F // 2 and it[both].mean() < 0.8 * df[both].mean(), name
