@@ -410,7 +410,8 @@ def main():
             # k_layer (R-9): per edge-iteration it reads and writes the edge's message r_e
             # and its variable's posterior line (each edge of a layer has its own variable): 16 B
             kname, kms, kn, per_ef = "k_layer", vn_ms, vn_n, 16.0
-            kdesc = "k_layer (row-layered check update: r_e and posterior in place)"
+            kdesc = ("k_layer_tma (row-layered check update, lines staged by cp.async.bulk: r_e and posterior "
+                     "read and written in place)")
         else:
             kname, kms, kn, per_ef = "k_cn", cn_ms, cn_n, 8.0
             kdesc = "k_cn (check-node pass, fused syndrome test)"
@@ -421,20 +422,21 @@ def main():
                     "launches_per_step": kn / args.steps, "avg_launch_us": 1e3 * kms / max(kn, 1),
                     "bytes_per_launch": cn_bytes / max(kn / args.steps, 1), "peak_source": peak_src,
                     "share_of_step": kms / args.steps / ms_step}
-        # DRAM traffic of k_cn from the committed ncu --set full capture (profiles/ncu_traffic.json),
-        # as bytes per edge-frame scaled to this run's average launch
-        tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        # live DRAM traffic: ncu over EVERY launch of the kernel in one complete step of this
+        # config and schedule (tools/ncu_traffic.py -> profiles/ncu_traffic_live.json): DRAM bytes
+        # per useful edge-frame, times this run's useful edge-frames per launch
+        tj = os.path.join(ROOT, "profiles", "ncu_traffic_live.json")
         if os.path.exists(tj):
             with open(tj) as f:
                 tr = json.load(f)
-            caps = [k for k in tr["kernels"] if kname + "<" in k["kernel"] or k["kernel"] == kname]
-            if caps and tr.get(f"{kname}_edge_frames"):
-                tb = (caps[0]["dram_read_mb"] + caps[0]["dram_write_mb"]) * 1e6 / tr[f"{kname}_edge_frames"]
+            if tr.get("config") == cfg.name and tr.get("schedule") == args.schedule and kname.startswith(tr["kernel"]):
+                tb = tr["bytes_per_useful_edge_frame"]
                 roofline["traffic"] = tb * edge_it_rank / max(kn / args.steps, 1)
-                roofline["traffic_note"] = (f"ncu dram read+write of one full-tile {kname} launch "
-                                            f"({tr.get(kname + '_source', tr['source'])}) = {tb:.2f} B per "
-                                            f"edge-frame vs {per_ef:g} algorithmic, times this run's edge-frames "
-                                            f"per launch")
+                roofline["traffic_note"] = (f"ncu dram__bytes_read+write summed over all {tr['launches']} "
+                                            f"{tr['kernel']} launches of one {cfg.name} step = {tb:.2f} B per useful "
+                                            f"edge-frame vs {per_ef:g} algorithmic ({100 * tr['wasted_fraction']:.1f} % "
+                                            f"above), times this run's useful edge-frames per launch "
+                                            f"(profiles/ncu_traffic_live.json)")
         it_bytes = (16.0 * edge_it_rank) if layered else (8.0 * edge_it_rank + 4.0 * var_it_rank)
         it_ach = it_bytes * args.steps / ((cn_ms + vn_ms) * 1e-3) / 1e9
         extra["roofline_bp_iteration"] = {

@@ -14,14 +14,17 @@ Parity-pin status per function:
   layers, bp_decode_layered       -- pinned (colouring validity + greedy minimality by brute
                                      force, tree exactness, repetition-chain sum, one-layer
                                      = flooding, Hamming ML statistics)
-  reconcile                       -- pinned (composition: reduces to the pinned parts;
-                                     noiseless limit; MC posterior of the LLR feed)
+  bp_trace_layered                -- pinned through bp_decode_layered (same code path, fixed k)
+  reconcile (both schedules)      -- pinned (tests/test_oracle_reconcile_pins.py: two-slice
+                                     conditioning vs the two-bin closed form through an exactly
+                                     solvable check, forced failure skips later slices (A-13),
+                                     noiseless D = 0, one slice = the decoder, schedules agree)
   verify.frame_hash               -- pinned (key = 1 word checksum, key = 2^32 shifted
                                      integer, zero string, bit-flip detection)
   pa.toeplitz_hash                -- pinned (numpy convolution window, unit / all-ones
                                      seeds, linearity, 2-universality statistics)
 """
 from .oracle import (  # noqa: F401
-    build, bp_decode, bp_decode_layered, bp_trace, layers, llr_biawgn, llr_slice, quantise, reconcile, slice_bits,
+    build, bp_decode, bp_decode_layered, bp_trace, bp_trace_layered, layers, llr_biawgn, llr_slice, quantise, reconcile, slice_bits,
     syndrome, num_threads,
 )

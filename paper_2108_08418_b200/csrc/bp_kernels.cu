@@ -36,106 +36,14 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "vec.cuh"
+#include "bp_device.cuh"
 
 namespace cvsr {
 
-constexpr unsigned FULL = 0xffffffffu;
 #ifndef CVSR_CPW
 #define CVSR_CPW 4
 #endif
 constexpr int CPW = CVSR_CPW;  // checks per warp
-
-__device__ __forceinline__ float ex2f(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-__device__ __forceinline__ float lg2f(float x) {
-    float y;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-__device__ __forceinline__ float rcpf(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-// a (+) b = 1 - (1 - a)(1 - b)
-__device__ __forceinline__ float cplus(float a, float b) { return fmaf(b, 1.0f - a, a); }
-__device__ __forceinline__ uint32_t sgnbit(float x) { return __float_as_uint(x) >> 31; }
-__device__ __forceinline__ float clampf(float x, float lim) { return fminf(fmaxf(x, -lim), lim); }
-
-// this lane's active bit per sub-tile, and "any" over the lane's S frames
-template <int S>
-__device__ __forceinline__ uint32_t lane_act(const uint4 &m, int lane) {
-    uint32_t a = 0u;
-#pragma unroll
-    for (int s = 0; s < S; ++s) a |= ((cmpu(m, s) >> lane) & 1u) << s;
-    return a;
-}
-
-// ------------------------------------------------------------------ check nodes
-
-// q (log2 units) -> r (log2 units), in registers.
-// "Sum/difference" form of the tanh rule: with u = 2^-|q| every edge is the pair
-// (1, u) ~ (D + N, D - N) of t = N / D = (1 - u) / (1 + u), and a product of t's
-// is tracked as (S, Delta) = (prod D + prod N, prod D - prod N) up to a common
-// factor:  (S1, d1) x (S2, d2) = (S1 S2 + d1 d2, S1 d2 + d1 S2).  Every term is
-// non-negative (no cancellation), the leave-one-out pairs come from prefix and
-// suffix products, and |r| = ln((1 + P) / (1 - P)) = lg2(S) - lg2(Delta) in log2
-// units: 3 MUFU per edge (ex2, 2 lg2) and no reciprocal.  A zero message gives
-// S = Delta, r = 0 exactly; an empty fold (degree-1 check) gives Delta = 0,
-// |r| = +inf -> Q_MAX.
-template <int DC>
-__device__ __forceinline__ void cn_update(float (&q)[DC], uint32_t sbit, float qmax2) {
-    float u[DC];
-    uint32_t par = sbit;
-#pragma unroll
-    for (int i = 0; i < DC; ++i) {
-        u[i] = ex2f(-fabsf(q[i]));
-        par ^= sgnbit(q[i]);
-    }
-    float ps[DC], pd[DC];
-    ps[0] = 1.0f;
-    pd[0] = 0.0f;
-#pragma unroll
-    for (int i = 1; i < DC; ++i) {
-        ps[i] = fmaf(u[i - 1], pd[i - 1], ps[i - 1]);
-        pd[i] = fmaf(u[i - 1], ps[i - 1], pd[i - 1]);
-    }
-    float ss = 1.0f, sd = 0.0f;
-#pragma unroll
-    for (int i = DC - 1; i >= 0; --i) {
-        const float S = fmaf(ps[i], ss, pd[i] * sd);
-        const float D = fmaf(ps[i], sd, pd[i] * ss);
-        const float mag = fmaxf(fminf(lg2f(S) - lg2f(D), qmax2), 0.0f);
-        const float ns = fmaf(u[i], sd, ss);
-        sd = fmaf(u[i], ss, sd);
-        ss = ns;
-        q[i] = (par ^ sgnbit(q[i])) ? -mag : mag;
-    }
-}
-
-// One check for the S frames of this lane.  DC is the code's maximum check
-// degree; a check of degree deg < DC is padded with "certain" dummy edges
-// (|q| = 200 in log2 units: w = 0, the neutral element of (+), sign +), which
-// are neither loaded nor stored: one code body per code keeps the i-cache hot.
-constexpr float DUMMY_Q = 200.0f;
-
-// the S frames of this lane (frames that are not active keep their message)
-template <int DC, int S>
-__device__ __forceinline__ void cn_lanes(FV<S> (&q)[DC], uint32_t sb, uint32_t al, float qmax2) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-        if (!((al >> s) & 1u)) continue;
-        float a[DC];
-#pragma unroll
-        for (int k = 0; k < DC; ++k) a[k] = q[k].c[s];
-        cn_update<DC>(a, (sb >> s) & 1u, qmax2);
-#pragma unroll
-        for (int k = 0; k < DC; ++k) q[k].c[s] = a[k];
-    }
-}
 
 template <int DC, int S>
 __device__ __forceinline__ void cn_check(float *__restrict__ m, int deg, uint32_t sb, uint32_t al, float qmax2) {
@@ -309,37 +217,6 @@ __global__ void __launch_bounds__(BLOCK, (DCT > 0 && DCT * S <= 16) ? CVSR_CN_MI
 constexpr int CPI = 8;                 // checks per work item = consumer warps per CTA
 constexpr int CN_TMA_THREADS = (CPI + 1) * 32;
 constexpr int CN_TMA_MAX_STAGES = 8;
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
 
 // one check of one item: DC lines from the stage, release the stage, update, store
 template <int DC, int S>
@@ -1573,190 +1450,5 @@ void launch_set_counts(const DecState &ds, int32_t n_active, cudaStream_t s) {
     k_set_counts<<<1, 32, 0, s>>>(ds, n_active);
 }
 
-
-// ------------------------------------------------------------------ row-layered schedule
-//
-// Reading R-9 (PAPER.md:189 names sum-product BP without fixing its
-// schedule): the checks are greedily coloured into layers that share no variable
-// (cvsr_code_load) and one iteration updates the layers in order, each against
-// the posteriors the previous layers left:
-//     q_e = post_v - r_e,   r_e <- (1 - 2 s_c) BOXPLUS_{e' != e} clamp(q_e'),   post_v <- q_e + r_e.
-// Arena use: ds.L holds the running posterior post_v (initialised to L_v), ds.msg
-// holds r_e (initialised to 0), ds.hb the hard decisions [post_v < 0].  No VN pass:
-// a layer kernel reads and writes one posterior line and one message line per
-// edge (16 B per edge-frame per iteration, as flooding's CN + VN), but the
-// schedule converges in about half the iterations (tools/layered_study.py).
-// The syndrome test of an iteration is k_cn with check_only = 1.  Same CN
-// arithmetic as k_cn (cn_lanes), so results differ from the oracle's fp64 only by
-// rounding.
-
-// hb = [L < 0] for the active frames; r = 0 is a memset by the caller
-template <int S>
-__global__ void __launch_bounds__(BLOCK) k_layer_init(CodeDev cd, DecState ds) {
-    const int ti = blockIdx.y;
-    if (ti >= ds.counts[0]) return;
-    const int t = ds.active_list[ti];
-    const uint4 act = ds.tile_active[t];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int v = blockIdx.x * WARPS_PER_BLOCK + warp;
-    if (v >= cd.n) return;
-    const FV<S> p = ldv<S>(ds.L + (((size_t)t * cd.n + v) * LANES + lane) * S);
-    uint32_t wd[SUBS] = {0u, 0u, 0u, 0u};
-#pragma unroll
-    for (int s = 0; s < S; ++s) wd[s] = __ballot_sync(FULL, p.c[s] < 0.0f) & cmpu(act, s);
-    if (lane == 0) ds.hb[(size_t)t * cd.n + v] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-}
-
-// one check of tile t: DC = code's maximum check degree (>= deg).  lo/deg/sbits describe the
-// check; v(k) returns the variable of its k-th edge (indices were fetched by the caller).
-template <int DC, int S, typename VarOf>
-__device__ __forceinline__ void layer_check(const CodeDev &cd, const DecState &ds, int t, const uint4 &act, int lo,
-                                            int deg, uint32_t sb, VarOf var_of, int lane, float qmax2) {
-    if constexpr (DC >= 6) {
-        // degree-2 checks in a code with a large maximum degree (MET-style type-A checks): a
-        // 2-edge body instead of DC - 2 dummy edges (deg is warp-uniform)
-        if (deg <= 2) {
-            layer_check<2, S>(cd, ds, t, act, lo, deg, sb, var_of, lane, qmax2);
-            return;
-        }
-    }
-    const uint32_t al = lane_act<S>(act, lane);
-    float *mt = ds.msg + ((size_t)t * cd.E + lo) * LANES * S + (size_t)lane * S;
-    float *Lt = ds.L + (size_t)t * cd.n * LANES * S + (size_t)lane * S;
-    int v[DC];
-    FV<S> qu[DC], q[DC];
-#pragma unroll
-    for (int k = 0; k < DC; ++k) {
-        v[k] = var_of(k);
-        if (k < deg) {
-            const FV<S> p = ldv<S>(Lt + (size_t)v[k] * LANES * S);
-            const FV<S> r = ldv<S>(mt + (size_t)k * LANES * S);
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                qu[k].c[s] = p.c[s] - r.c[s];
-                q[k].c[s] = clampf(qu[k].c[s], qmax2);
-            }
-        } else {
-            q[k] = splat<S>(DUMMY_Q);
-        }
-    }
-    cn_lanes<DC, S>(q, sb, al, qmax2);
-#pragma unroll
-    for (int k = 0; k < DC; ++k) {
-        if (k < deg) {
-            FV<S> p;
-#pragma unroll
-            for (int s = 0; s < S; ++s) p.c[s] = qu[k].c[s] + q[k].c[s];  // (retired frames' values are dead)
-            uint32_t wd[SUBS] = {0u, 0u, 0u, 0u};
-#pragma unroll
-            for (int s = 0; s < S; ++s) wd[s] = __ballot_sync(FULL, p.c[s] < 0.0f) & cmpu(act, s);
-            if (al) {
-                stv<S>(mt + (size_t)k * LANES * S, q[k]);
-                stv<S>(Lt + (size_t)v[k] * LANES * S, p);
-            }
-            if (lane == 0) ds.hb[(size_t)t * cd.n + v[k]] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-        }
-    }
-}
-
-#ifndef CVSR_LAYER_MINB
-#define CVSR_LAYER_MINB 4
-#endif
-#ifndef CVSR_LAYER_CPW
-#define CVSR_LAYER_CPW 4
-#endif
-constexpr int LCPW = CVSR_LAYER_CPW;  // checks per warp in k_layer
-// A warp takes CPW checks of the layer.  When CPW x DC <= 32 their check ids, row bounds and
-// column indices are fetched up front with one load per lane (no dependent index loads per
-// check); otherwise per check.
-// Blocks per SM: the most that ptxas fits without spills (64 / 80 / 128 registers per thread
-// for 4 / 3 / 2 blocks of 256 threads; -Xptxas -v of this build)
-__host__ __device__ constexpr int layer_minb(int DC, int S) {
-    return S == 1 ? (DC <= 7 ? CVSR_LAYER_MINB : (DC <= 10 ? 3 : 2))
-                  : (S == 2 ? (DC <= 5 ? CVSR_LAYER_MINB : (DC <= 6 ? 3 : 2)) : (DC <= 3 ? 3 : 2));
-}
-template <int DC, int S>
-__global__ void __launch_bounds__(BLOCK, layer_minb(DC, S)) k_layer(CodeDev cd, DecState ds, int lbeg, int lcnt,
-                                                                    float qmax2) {
-    const int ti = blockIdx.y;
-    if (ti >= ds.counts[0]) return;
-    const int t = ds.active_list[ti];
-    const uint4 act = ds.tile_active[t];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * LCPW;
-    const int nc = min(LCPW, lcnt - i0);
-    if (nc <= 0) return;
-    const int myc = lane < nc ? cd.layer_chk[lbeg + i0 + lane] : 0;
-    const int mylo = lane < nc ? cd.row_ptr[myc] : 0;
-    const int myhi = lane < nc ? cd.row_ptr[myc + 1] : 0;
-    const uint4 *stt = ds.st + (size_t)t * cd.M;
-    if constexpr (LCPW * DC <= LANES) {
-        const int ii = lane / DC, kk = lane - ii * DC;
-        const int lo_ii = __shfl_sync(FULL, mylo, ii < LCPW ? ii : 0);
-        const int hi_ii = __shfl_sync(FULL, myhi, ii < LCPW ? ii : 0);
-        const int myv = (ii < nc && kk < hi_ii - lo_ii) ? cd.col_idx[lo_ii + kk] : 0;
-#pragma unroll 1
-        for (int i = 0; i < nc; ++i) {
-            const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
-            const int c = __shfl_sync(FULL, myc, i);
-            const uint32_t sb = lane_act<S>(stt[c], lane);
-            layer_check<DC, S>(cd, ds, t, act, lo, deg, sb,
-                               [&](int k) { return __shfl_sync(FULL, myv, i * DC + k); }, lane, qmax2);
-        }
-    } else {
-#pragma unroll 1
-        for (int i = 0; i < nc; ++i) {
-            const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
-            const int c = __shfl_sync(FULL, myc, i);
-            const uint32_t sb = lane_act<S>(stt[c], lane);
-            const int myv = lane < deg ? cd.col_idx[lo + lane] : 0;
-            layer_check<DC, S>(cd, ds, t, act, lo, deg, sb, [&](int k) { return __shfl_sync(FULL, myv, k); },
-                               lane, qmax2);
-        }
-    }
-}
-
-template <int S>
-static bool launch_layer_s(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,
-                           cudaStream_t s) {
-    switch (cd.max_dc) {
-        case 1: case 2: k_layer<2, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
-        case 3: k_layer<3, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
-        case 4: k_layer<4, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
-        case 5: k_layer<5, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
-        case 6: k_layer<6, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
-        case 7: k_layer<7, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
-        case 8: k_layer<8, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
-        case 9: k_layer<9, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
-        case 10: k_layer<10, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
-        case 11: case 12: k_layer<12, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
-        default: return false;
-    }
-}
-
-bool layered_supported(const CodeDev &cd) { return cd.n_layers > 0 && cd.max_dc <= 12; }
-
-void launch_layer_init(const CodeDev &cd, const DecState &ds, int grid_tiles, cudaStream_t s) {
-    if (grid_tiles <= 0) return;
-    dim3 grid((cd.n + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, grid_tiles);
-    if (ds.subs == 4) k_layer_init<4><<<grid, BLOCK, 0, s>>>(cd, ds);
-    else if (ds.subs == 2) k_layer_init<2><<<grid, BLOCK, 0, s>>>(cd, ds);
-    else k_layer_init<1><<<grid, BLOCK, 0, s>>>(cd, ds);
-}
-
-// all layers of one iteration (returns the number of launches)
-int launch_layers(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, cudaStream_t s) {
-    if (grid_tiles <= 0) return 0;
-    const float q2 = qmax * LOG2E;
-    const int per_block = WARPS_PER_BLOCK * LCPW;
-    for (int l = 0; l < cd.n_layers; ++l) {
-        const int lbeg = cd.layer_off[l], lcnt = cd.layer_off[l + 1] - lbeg;
-        dim3 grid((lcnt + per_block - 1) / per_block, grid_tiles);
-        if (ds.subs == 4) launch_layer_s<4>(cd, ds, grid, lbeg, lcnt, q2, s);
-        else if (ds.subs == 2) launch_layer_s<2>(cd, ds, grid, lbeg, lcnt, q2, s);
-        else launch_layer_s<1>(cd, ds, grid, lbeg, lcnt, q2, s);
-    }
-    return cd.n_layers;
-}
 
 }  // namespace cvsr

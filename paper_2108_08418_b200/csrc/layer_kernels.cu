@@ -1,0 +1,398 @@
+// Row-layered BP schedule (reading R-9) for sm_100a.
+#include <stdlib.h>
+
+#include "bp_device.cuh"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "vec.cuh"
+
+namespace cvsr {
+
+// ------------------------------------------------------------------ row-layered schedule
+//
+// Reading R-9 (PAPER.md:189 names sum-product BP without fixing its
+// schedule): the checks are greedily coloured into layers that share no variable
+// (cvsr_code_load) and one iteration updates the layers in order, each against
+// the posteriors the previous layers left:
+//     q_e = post_v - r_e,   r_e <- (1 - 2 s_c) BOXPLUS_{e' != e} clamp(q_e'),   post_v <- q_e + r_e.
+// Arena use: ds.L holds the running posterior post_v (initialised to L_v), ds.msg
+// holds r_e (initialised to 0), ds.hb the hard decisions [post_v < 0].  No VN pass:
+// a layer kernel reads and writes one posterior line and one message line per
+// edge (16 B per edge-frame per iteration, as flooding's CN + VN), but the
+// schedule converges in about half the iterations (tools/layered_study.py).
+// The syndrome test of an iteration is k_cn with check_only = 1.  Same CN
+// arithmetic as k_cn (cn_lanes), so results differ from the oracle's fp64 only by
+// rounding.
+
+// hb = [L < 0] for the active frames; r = 0 is a memset by the caller
+template <int S>
+__global__ void __launch_bounds__(BLOCK) k_layer_init(CodeDev cd, DecState ds) {
+    const int ti = blockIdx.y;
+    if (ti >= ds.counts[0]) return;
+    const int t = ds.active_list[ti];
+    const uint4 act = ds.tile_active[t];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int v = blockIdx.x * WARPS_PER_BLOCK + warp;
+    if (v >= cd.n) return;
+    const FV<S> p = ldv<S>(ds.L + (((size_t)t * cd.n + v) * LANES + lane) * S);
+    uint32_t wd[SUBS] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int s = 0; s < S; ++s) wd[s] = __ballot_sync(FULL, p.c[s] < 0.0f) & cmpu(act, s);
+    if (lane == 0) ds.hb[(size_t)t * cd.n + v] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+}
+
+// one check of tile t: DC = code's maximum check degree (>= deg).  lo/deg/sbits describe the
+// check; v(k) returns the variable of its k-th edge (indices were fetched by the caller).
+template <int DC, int S, typename VarOf>
+__device__ __forceinline__ void layer_check(const CodeDev &cd, const DecState &ds, int t, const uint4 &act, int lo,
+                                            int deg, uint32_t sb, VarOf var_of, int lane, float qmax2) {
+    if constexpr (DC >= 6) {
+        // degree-2 checks in a code with a large maximum degree (MET-style type-A checks): a
+        // 2-edge body instead of DC - 2 dummy edges (deg is warp-uniform)
+        if (deg <= 2) {
+            layer_check<2, S>(cd, ds, t, act, lo, deg, sb, var_of, lane, qmax2);
+            return;
+        }
+    }
+    const uint32_t al = lane_act<S>(act, lane);
+    float *mt = ds.msg + ((size_t)t * cd.E + lo) * LANES * S + (size_t)lane * S;
+    float *Lt = ds.L + (size_t)t * cd.n * LANES * S + (size_t)lane * S;
+    int v[DC];
+    FV<S> qu[DC], q[DC];
+#pragma unroll
+    for (int k = 0; k < DC; ++k) {
+        v[k] = var_of(k);
+        if (k < deg) {
+            const FV<S> p = ldv<S>(Lt + (size_t)v[k] * LANES * S);
+            const FV<S> r = ldv<S>(mt + (size_t)k * LANES * S);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                qu[k].c[s] = p.c[s] - r.c[s];
+                q[k].c[s] = clampf(qu[k].c[s], qmax2);
+            }
+        } else {
+            q[k] = splat<S>(DUMMY_Q);
+        }
+    }
+    cn_lanes<DC, S>(q, sb, al, qmax2);
+#pragma unroll
+    for (int k = 0; k < DC; ++k) {
+        if (k < deg) {
+            FV<S> p;
+#pragma unroll
+            for (int s = 0; s < S; ++s) p.c[s] = qu[k].c[s] + q[k].c[s];  // (retired frames' values are dead)
+            uint32_t wd[SUBS] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int s = 0; s < S; ++s) wd[s] = __ballot_sync(FULL, p.c[s] < 0.0f) & cmpu(act, s);
+            if (al) {
+                stv<S>(mt + (size_t)k * LANES * S, q[k]);
+                stv<S>(Lt + (size_t)v[k] * LANES * S, p);
+            }
+            if (lane == 0) ds.hb[(size_t)t * cd.n + v[k]] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+        }
+    }
+}
+
+#ifndef CVSR_LAYER_MINB
+#define CVSR_LAYER_MINB 4
+#endif
+#ifndef CVSR_LAYER_CPW
+#define CVSR_LAYER_CPW 4
+#endif
+constexpr int LCPW = CVSR_LAYER_CPW;  // checks per warp in k_layer
+// A warp takes CPW checks of the layer.  When CPW x DC <= 32 their check ids, row bounds and
+// column indices are fetched up front with one load per lane (no dependent index loads per
+// check); otherwise per check.
+// Blocks per SM: the most that ptxas fits without spills (64 / 80 / 128 registers per thread
+// for 4 / 3 / 2 blocks of 256 threads; -Xptxas -v of this build)
+__host__ __device__ constexpr int layer_minb(int DC, int S) {
+    return S == 1 ? (DC <= 7 ? CVSR_LAYER_MINB : (DC <= 10 ? 3 : 2))
+                  : (S == 2 ? (DC <= 5 ? CVSR_LAYER_MINB : (DC <= 6 ? 3 : 2)) : (DC <= 3 ? 3 : 2));
+}
+template <int DC, int S>
+__global__ void __launch_bounds__(BLOCK, layer_minb(DC, S)) k_layer(CodeDev cd, DecState ds, int lbeg, int lcnt,
+                                                                    float qmax2) {
+    const int ti = blockIdx.y;
+    if (ti >= ds.counts[0]) return;
+    const int t = ds.active_list[ti];
+    const uint4 act = ds.tile_active[t];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = (blockIdx.x * WARPS_PER_BLOCK + warp) * LCPW;
+    const int nc = min(LCPW, lcnt - i0);
+    if (nc <= 0) return;
+    const int myc = lane < nc ? cd.layer_chk[lbeg + i0 + lane] : 0;
+    const int mylo = lane < nc ? cd.row_ptr[myc] : 0;
+    const int myhi = lane < nc ? cd.row_ptr[myc + 1] : 0;
+    const uint4 *stt = ds.st + (size_t)t * cd.M;
+    if constexpr (LCPW * DC <= LANES) {
+        const int ii = lane / DC, kk = lane - ii * DC;
+        const int lo_ii = __shfl_sync(FULL, mylo, ii < LCPW ? ii : 0);
+        const int hi_ii = __shfl_sync(FULL, myhi, ii < LCPW ? ii : 0);
+        const int myv = (ii < nc && kk < hi_ii - lo_ii) ? cd.col_idx[lo_ii + kk] : 0;
+#pragma unroll 1
+        for (int i = 0; i < nc; ++i) {
+            const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
+            const int c = __shfl_sync(FULL, myc, i);
+            const uint32_t sb = lane_act<S>(stt[c], lane);
+            layer_check<DC, S>(cd, ds, t, act, lo, deg, sb,
+                               [&](int k) { return __shfl_sync(FULL, myv, i * DC + k); }, lane, qmax2);
+        }
+    } else {
+#pragma unroll 1
+        for (int i = 0; i < nc; ++i) {
+            const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
+            const int c = __shfl_sync(FULL, myc, i);
+            const uint32_t sb = lane_act<S>(stt[c], lane);
+            const int myv = lane < deg ? cd.col_idx[lo + lane] : 0;
+            layer_check<DC, S>(cd, ds, t, act, lo, deg, sb, [&](int k) { return __shfl_sync(FULL, myv, k); },
+                               lane, qmax2);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ TMA-staged layer kernel
+//
+// k_layer_tma<DC, S>: same check update and arena as k_layer, but the lines a check reads are
+// staged in shared memory by bulk asynchronous copies (cp.async.bulk, the TMA engine's
+// non-tensor path) instead of register loads, so the number of bytes in flight no longer
+// depends on registers.  Each warp owns LT_P stages and walks LT_CH checks of the layer:
+//   issue:   one elected lane arms the stage's mbarrier with the stage's byte count; lane k < deg
+//            copies the posterior line of the check's k-th variable (128 S bytes, gathered), lane 0
+//            copies the check's deg message lines (one contiguous span: CSR slots are contiguous);
+//   compute: after the mbarrier phase completes, every lane reads its S frames of each line
+//            from shared memory, runs the sum/difference CN update (cn_update) per frame and
+//            writes r_e and post_v = q_e + r_e back into the stage, plus the hard decisions;
+//   store:   lane-vectorised stores of the deg message lines and deg posterior lines;
+//   refill:  the stage is re-armed with check i + LT_P.
+// Checks of one layer share no variable, so prefetching the next checks' posterior lines while
+// the current check is being written is exact.  The arithmetic is k_layer's operation for
+// operation (results are bit-identical).
+constexpr int LT_WARPS = 8;  // warps per block
+#ifndef CVSR_LT_CH
+#define CVSR_LT_CH 8
+#endif
+#ifndef CVSR_LT_P
+#define CVSR_LT_P 3
+#endif
+constexpr int LT_CH = CVSR_LT_CH;  // checks per warp
+constexpr int LT_P = CVSR_LT_P;    // stages per warp
+
+template <int DC, int S>
+struct LtLayout {
+    static constexpr int LINE = LANES * S;                 // floats per line
+    static constexpr int STAGE = 2 * DC * LINE;            // floats: DC posterior lines, then DC message lines
+    static constexpr size_t RAW = (size_t)LT_P * STAGE * 4 + LT_P * 8 + (size_t)LT_CH * DC * 4;
+    static constexpr size_t WARP_BYTES = (RAW + 127) & ~(size_t)127;
+    static constexpr size_t BLOCK_BYTES = WARP_BYTES * LT_WARPS;
+    // blocks per SM the shared memory allows (228 KB per SM, 1 KB reserved per block)
+    static constexpr int BLOCKS = (int)((228 * 1024) / (BLOCK_BYTES + 1024)) < 1
+                                      ? 1
+                                      : ((int)((228 * 1024) / (BLOCK_BYTES + 1024)) > 4
+                                             ? 4
+                                             : (int)((228 * 1024) / (BLOCK_BYTES + 1024)));
+};
+
+// the check update of one check from its stage: DCT = compute width (>= deg; DCL = the stage
+// layout's DC).  Results overwrite the stage: posterior lines <- post_v, message lines <- r_e.
+template <int DCT, int DCL, int S>
+__device__ __forceinline__ void lt_compute(float *__restrict__ sp, int deg, uint32_t sb, const uint4 &act, int lane,
+                                           float qmax2, uint32_t *__restrict__ hbt, const int *__restrict__ vrow) {
+    constexpr int LINE = LANES * S;
+    float *pp = sp + lane * S;               // posterior lines
+    float *rp = sp + DCL * LINE + lane * S;  // message lines
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        float a[DCT];
+#pragma unroll
+        for (int k = 0; k < DCT; ++k) a[k] = (k < deg) ? clampf(pp[k * LINE + s] - rp[k * LINE + s], qmax2) : DUMMY_Q;
+        cn_update<DCT>(a, (sb >> s) & 1u, qmax2);
+        const uint32_t am = cmpu(act, s);
+#pragma unroll
+        for (int k = 0; k < DCT; ++k) {
+            if (k < deg) {
+                const float post = (pp[k * LINE + s] - rp[k * LINE + s]) + a[k];
+                rp[k * LINE + s] = a[k];
+                pp[k * LINE + s] = post;
+                const uint32_t w = __ballot_sync(FULL, post < 0.0f) & am;
+                if (lane == 0) hbt[(size_t)vrow[k] * 4 + s] = w;
+            }
+        }
+    }
+}
+
+template <int DC, int S>
+__global__ void __launch_bounds__(LT_WARPS * 32, LtLayout<DC, S>::BLOCKS)
+    k_layer_tma(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2) {
+    using LY = LtLayout<DC, S>;
+    constexpr int LINE = LY::LINE;
+    extern __shared__ __align__(128) unsigned char lt_smem[];
+    const int ti = blockIdx.y;
+    if (ti >= ds.counts[0]) return;
+    const int t = ds.active_list[ti];
+    const uint4 act = ds.tile_active[t];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = (blockIdx.x * LT_WARPS + warp) * LT_CH;
+    const int nc = min(LT_CH, lcnt - i0);
+    if (nc <= 0) return;
+    unsigned char *wb = lt_smem + (size_t)warp * LY::WARP_BYTES;
+    float *stage = reinterpret_cast<float *>(wb);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(wb + (size_t)LT_P * LY::STAGE * 4);
+    int *vidx = reinterpret_cast<int *>(bar + LT_P);
+    if (lane == 0) {
+#pragma unroll
+        for (int p = 0; p < LT_P; ++p) mbar_init(&bar[p], 1);
+        mbar_init_fence();
+    }
+    // the chunk's check ids, row bounds, syndrome words and column indices, fetched up front
+    const int myc = lane < nc ? cd.layer_chk[lbeg + i0 + lane] : 0;
+    const int mylo = lane < nc ? cd.row_ptr[myc] : 0;
+    const int myhi = lane < nc ? cd.row_ptr[myc + 1] : 0;
+    const uint4 mys = lane < nc ? ds.st[(size_t)t * cd.M + myc] : make_uint4(0u, 0u, 0u, 0u);
+    for (int f0 = 0; f0 < LT_CH * DC; f0 += LANES) {
+        const int f = f0 + lane;
+        const int i = min(f / DC, LT_CH - 1), k = f - i * DC;
+        const int lo = __shfl_sync(FULL, mylo, i), hi = __shfl_sync(FULL, myhi, i);
+        if (f < LT_CH * DC) vidx[f] = (i < nc && k < hi - lo) ? cd.col_idx[lo + k] : 0;
+    }
+    __syncwarp();
+    const float *Lt = ds.L + (size_t)t * cd.n * LINE;
+    const float *mt = ds.msg + (size_t)t * cd.E * LINE;
+    auto issue = [&](int i, int p) {
+        const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
+        float *sp = stage + (size_t)p * LY::STAGE;
+        if (lane == 0) mbar_arrive_tx(&bar[p], 2u * (uint32_t)deg * LINE * 4u);
+        if (lane < deg) bulk_g2s(sp + lane * LINE, Lt + (size_t)vidx[i * DC + lane] * LINE, LINE * 4, &bar[p]);
+        if (lane == 0 && deg > 0) bulk_g2s(sp + DC * LINE, mt + (size_t)lo * LINE, (uint32_t)deg * LINE * 4, &bar[p]);
+    };
+    const int npre = min(LT_P, nc);
+    for (int i = 0; i < npre; ++i) issue(i, i);
+    const uint32_t al = lane_act<S>(act, lane);
+    uint32_t *hbt = reinterpret_cast<uint32_t *>(ds.hb + (size_t)t * cd.n);
+    float *Lw = ds.L + (size_t)t * cd.n * LINE + lane * S;
+    float *mw = ds.msg + (size_t)t * cd.E * LINE + lane * S;
+    uint32_t phase = 0u;
+    for (int i = 0; i < nc; ++i) {
+        const int p = i % LT_P;
+        mbar_wait(&bar[p], (phase >> p) & 1u);
+        phase ^= 1u << p;
+        const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
+        uint4 sw;
+        sw.x = __shfl_sync(FULL, mys.x, i);
+        sw.y = (S > 1) ? __shfl_sync(FULL, mys.y, i) : 0u;
+        sw.z = (S > 2) ? __shfl_sync(FULL, mys.z, i) : 0u;
+        sw.w = (S > 2) ? __shfl_sync(FULL, mys.w, i) : 0u;
+        const uint32_t sb = lane_act<S>(sw, lane);
+        float *sp = stage + (size_t)p * LY::STAGE;
+        const int *vrow = vidx + i * DC;
+        if constexpr (DC >= 6) {
+            // degree-2 checks of a code with a large maximum degree (MET type-A checks)
+            if (deg <= 2) lt_compute<2, DC, S>(sp, deg, sb, act, lane, qmax2, hbt, vrow);
+            else lt_compute<DC, DC, S>(sp, deg, sb, act, lane, qmax2, hbt, vrow);
+        } else {
+            lt_compute<DC, DC, S>(sp, deg, sb, act, lane, qmax2, hbt, vrow);
+        }
+        __syncwarp();
+        if (al) {
+#pragma unroll
+            for (int k = 0; k < DC; ++k) {
+                if (k < deg) {
+                    stv<S>(mw + (size_t)(lo + k) * LINE, ldv<S>(sp + (DC + k) * LINE + lane * S));
+                    stv<S>(Lw + (size_t)vrow[k] * LINE, ldv<S>(sp + k * LINE + lane * S));
+                }
+            }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (i + LT_P < nc) issue(i + LT_P, p);
+    }
+}
+
+template <int DC, int S>
+static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,
+                               cudaStream_t s) {
+    static bool attr = false;
+    constexpr size_t smem = LtLayout<DC, S>::BLOCK_BYTES;
+    if (!attr) {
+        cudaFuncSetAttribute(k_layer_tma<DC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    k_layer_tma<DC, S><<<grid, LT_WARPS * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2);
+}
+
+template <int S>
+static bool launch_layer_tma_s(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,
+                               cudaStream_t s) {
+    switch (cd.max_dc) {
+        case 1: case 2: launch_layer_tma_t<2, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
+        case 3: launch_layer_tma_t<3, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
+        case 4: launch_layer_tma_t<4, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
+        case 5: launch_layer_tma_t<5, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
+        case 6: launch_layer_tma_t<6, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
+        case 7: launch_layer_tma_t<7, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
+        case 8: launch_layer_tma_t<8, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
+        case 9: launch_layer_tma_t<9, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
+        case 10: launch_layer_tma_t<10, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
+        case 11: case 12: launch_layer_tma_t<12, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
+        default: return false;
+    }
+}
+
+// TMA-staged layer kernel on/off (CVSR_LAYER_TMA=0: the register-staged k_layer)
+static bool layer_tma_enabled() {
+    static const int v = [] {
+        const char *e = getenv("CVSR_LAYER_TMA");
+        return (e && *e) ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
+template <int S>
+static bool launch_layer_s(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,
+                           cudaStream_t s) {
+    switch (cd.max_dc) {
+        case 1: case 2: k_layer<2, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 3: k_layer<3, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 4: k_layer<4, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 5: k_layer<5, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 6: k_layer<6, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 7: k_layer<7, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 8: k_layer<8, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 9: k_layer<9, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 10: k_layer<10, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        case 11: case 12: k_layer<12, S><<<grid, BLOCK, 0, s>>>(cd, ds, lbeg, lcnt, q2); return true;
+        default: return false;
+    }
+}
+
+bool layered_supported(const CodeDev &cd) { return cd.n_layers > 0 && cd.max_dc <= 12; }
+
+void launch_layer_init(const CodeDev &cd, const DecState &ds, int grid_tiles, cudaStream_t s) {
+    if (grid_tiles <= 0) return;
+    dim3 grid((cd.n + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, grid_tiles);
+    if (ds.subs == 4) k_layer_init<4><<<grid, BLOCK, 0, s>>>(cd, ds);
+    else if (ds.subs == 2) k_layer_init<2><<<grid, BLOCK, 0, s>>>(cd, ds);
+    else k_layer_init<1><<<grid, BLOCK, 0, s>>>(cd, ds);
+}
+
+// all layers of one iteration (returns the number of launches)
+int launch_layers(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, cudaStream_t s) {
+    if (grid_tiles <= 0) return 0;
+    const float q2 = qmax * LOG2E;
+    const bool tma = layer_tma_enabled() && ds.subs <= 2;
+    const int per_block = tma ? LT_WARPS * LT_CH : WARPS_PER_BLOCK * LCPW;
+    for (int l = 0; l < cd.n_layers; ++l) {
+        const int lbeg = cd.layer_off[l], lcnt = cd.layer_off[l + 1] - lbeg;
+        dim3 grid((lcnt + per_block - 1) / per_block, grid_tiles);
+        if (tma) {
+            if (ds.subs == 2) launch_layer_tma_s<2>(cd, ds, grid, lbeg, lcnt, q2, s);
+            else launch_layer_tma_s<1>(cd, ds, grid, lbeg, lcnt, q2, s);
+            continue;
+        }
+        if (ds.subs == 4) launch_layer_s<4>(cd, ds, grid, lbeg, lcnt, q2, s);
+        else if (ds.subs == 2) launch_layer_s<2>(cd, ds, grid, lbeg, lcnt, q2, s);
+        else launch_layer_s<1>(cd, ds, grid, lbeg, lcnt, q2, s);
+    }
+    return cd.n_layers;
+}
+
+}  // namespace cvsr
