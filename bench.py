@@ -192,6 +192,30 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def keyrate_at_standard_settings(cfg, beta: float, symbols_per_s: float, fer: float, s_be: float = 0.6721):
+    """The paper's figure of merit next to the throughput (host fp64): the
+    finite-key rate K' = N_o K / Delta t (eq:BPSRate) with K from eq:BPSKeyRate
+     at the REALISED efficiency beta I_AB, Delta t = the time this run needs to
+    reconcile N = 1e9 quadratures (N / symbols per second), standard settings,
+    eps_EC = 2.5e-10, N_o = 2 N, S_BE = 0.6721 (a parameter); frames that fail are
+    discarded, so K scales with 1 - FER.  None for configs not at the standard settings."""
+    if not cfg.name.startswith("C4"):
+        return None
+    from paper_2108_08418_b200 import keyrate as K
+    eps = 2.5e-10
+    N, N_o = 1e9, 2e9
+    e = K.eps_total(eps, eps / 2, eps, eps)
+    d_aep = K.delta_aep(cfg.m, N, eps / 2, e)
+    dt = N / symbols_per_s
+    k_beta = K.key_rate(N, N_o, beta * K.i_ab(cfg.gamma), s_be, d_aep, eps) * (1.0 - fer)
+    k_fin = K.k_finite(N, N_o, cfg.gamma, cfg.n, eps, s_be, d_aep, eps)
+    return {"K_prime_bits_per_s": K.k_prime(N_o, k_beta, dt), "K_bits_per_pulse": k_beta, "beta_I_AB": beta *
+            K.i_ab(cfg.gamma), "S_BE": s_be, "delta_t_s_for_N_1e9": dt,
+            "K_prime_finite_bits_per_s": K.k_prime(N_o, k_fin, dt),
+            "note": "eq:BPSKeyRate with the realised beta (K_prime) and eq:FiniteK with C_Finite(N_R) "
+                    "(K_prime_finite), per Delta t of this run; K < 0 means beta I_AB < S_BE"}
+
+
 # ---------------------------------------------------------------- CUDA leg
 
 def main():
@@ -451,6 +475,7 @@ def main():
             extra["stage_ms_rank0"] = {"bob": stage_ms[0], "alice": stage_ms[1], "hash_check": stage_ms[2]}
             extra["alice_only_bits_per_s_rank0"] = bits_per_step / (stage_ms[1] * 1e-3)
     ops = 7.0 * float(edge_iters.sum())  # eq: EP, E_j = 7 G per iteration
+    keyrate = keyrate_at_standard_settings(cfg, beta, frames_all * n / (ms_step * 1e-3), fer)
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -485,7 +510,7 @@ def main():
         "symbols_per_s": frames_all * n / (ms_step * 1e-3),
         "decoded_slice_bits_per_s": frames_all * n * sum(c is not None for c in codes_l) / (ms_step * 1e-3),
         "paper_ops_per_s": ops / (ms_step * 1e-3),
-        "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+        "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "keyrate": keyrate,
         "gpu_launches": int(launches),
         "splits": args.splits,
         "e2e": ({"value": bits_step / (tmax[1] / args.steps * 1e-3), "unit": UNIT,

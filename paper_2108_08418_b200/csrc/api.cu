@@ -188,12 +188,7 @@ int pick_subs(int32_t frames, int64_t E, bool layered, int32_t max_dc) {
         forced = e ? atoi(e) : 0;
     }
     if (forced == 1 || forced == 2 || forced == 4) return std::min(forced, s == 4 ? 4 : std::max(s, forced));
-    if (layered) {
-        // 2 frames per lane (64-frame tiles) measured faster on C2 (51.6 vs 56.0 ms per step):
-        // k_layer<5, 2> needs 60 registers without spills, k_layer<5, 4> spills at 64.  Check
-        // degrees above 6 take one frame per lane (k_layer<DC, 1>: no spills up to DC = 12).
-        s = std::min(s, max_dc > 6 ? 1 : 2);
-    }
+    if (layered) s = std::min(s, layer_subs(max_dc));  // layer_kernels.cu
     static double cap = -1.0;
     if (cap < 0.0) {
         const char *e = getenv("CVSR_FUSED_MB");  // experiment switch: per-tile L2 budget (MB)
@@ -235,6 +230,16 @@ size_t smem_limit() {
 }
 constexpr int GRAPH_ITERS = 8;      // iterations per captured graph
 constexpr int GRAPH_MAX_TILES = 2;  // batches of at most this many tiles take the graph path
+
+// layered schedule's syndrome test: k_synd_test (thread per check; default) or the check-only
+// k_cn (CVSR_SYND_CN=1)
+bool synd_test_kernel() {
+    static const int v = [] {
+        const char *e = getenv("CVSR_SYND_CN");
+        return (e && e[0] == '1') ? 0 : 1;
+    }();
+    return v != 0;
+}
 
 bool compact_enabled() {
     static int v = -1;
@@ -401,12 +406,13 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
     };
     int k = 1;
     if (layered) {
-        // iteration k: syndrome test of decision k-1 (k_cn check-only), status/retire, then the
+        // iteration k: syndrome test of decision k-1 (k_synd_test), status/retire, then the
         // layers (reading R-9); compaction moves r (msg), post (L), hb and st of active frames
         for (; k <= max_iter + 1; ++k) {
             const int final_pass = (k == max_iter + 1);
             prof_begin(ctx, KC_CN);
-            launch_cn(cd, ds, bound, qmax, 1, s);
+            if (synd_test_kernel()) launch_synd_test(cd, ds, bound, s);
+            else launch_cn(cd, ds, bound, qmax, 1, s);
             prof_end(ctx);
             prof_begin(ctx, KC_CTRL);
             launch_status(ds, k, max_iter, final_pass, ctx->host_counts_dev, s);

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(BLOCK, layer_minb(DC, S)) k_layer(CodeDev cd, 
 // k_layer_tma<DC, S>: same check update and arena as k_layer, but the lines a check reads are
 // staged in shared memory by bulk asynchronous copies (cp.async.bulk, the TMA engine's
 // non-tensor path) instead of register loads, so the number of bytes in flight no longer
-// depends on registers.  Each warp owns LT_P stages and walks LT_CH checks of the layer:
+// depends on registers.  Each warp owns P (2-3) stages and walks LT_CH checks of the layer:
 //   issue:   one elected lane arms the stage's mbarrier with the stage's byte count; lane k < deg
 //            copies the posterior line of the check's k-th variable (128 S bytes, gathered), lane 0
 //            copies the check's deg message lines (one contiguous span: CSR slots are contiguous);
@@ -163,7 +163,9 @@ __global__ void __launch_bounds__(BLOCK, layer_minb(DC, S)) k_layer(CodeDev cd, 
 //            from shared memory, runs the sum/difference CN update (cn_update) per frame and
 //            writes r_e and post_v = q_e + r_e back into the stage, plus the hard decisions;
 //   store:   lane-vectorised stores of the deg message lines and deg posterior lines;
-//   refill:  the stage is re-armed with check i + LT_P.
+//   refill:  the stage is re-armed with check i + P.
+// (Measured against storing r_e / post_v straight from registers, which needs all S frames'
+// q_e in registers and scalar stores: C4 95.6 vs 88.8 ms per step, C2 57.6 vs 51.6.)
 // Checks of one layer share no variable, so prefetching the next checks' posterior lines while
 // the current check is being written is exact.  The arithmetic is k_layer's operation for
 // operation (results are bit-identical).
@@ -171,25 +173,23 @@ constexpr int LT_WARPS = 8;  // warps per block
 #ifndef CVSR_LT_CH
 #define CVSR_LT_CH 8
 #endif
-#ifndef CVSR_LT_P
-#define CVSR_LT_P 3
+#ifndef CVSR_LT_STAGE_KB
+#define CVSR_LT_STAGE_KB 3
 #endif
 constexpr int LT_CH = CVSR_LT_CH;  // checks per warp
-constexpr int LT_P = CVSR_LT_P;    // stages per warp
 
 template <int DC, int S>
 struct LtLayout {
     static constexpr int LINE = LANES * S;                 // floats per line
     static constexpr int STAGE = 2 * DC * LINE;            // floats: DC posterior lines, then DC message lines
-    static constexpr size_t RAW = (size_t)LT_P * STAGE * 4 + LT_P * 8 + (size_t)LT_CH * DC * 4;
+    // stages per warp: 3 while a stage is at most CVSR_LT_STAGE_KB, else 2 (shared memory per SM)
+    static constexpr int P = (STAGE * 4 <= CVSR_LT_STAGE_KB * 1024) ? 3 : 2;
+    static constexpr size_t RAW = (size_t)P * STAGE * 4 + P * 8 + (size_t)LT_CH * DC * 4;
     static constexpr size_t WARP_BYTES = (RAW + 127) & ~(size_t)127;
     static constexpr size_t BLOCK_BYTES = WARP_BYTES * LT_WARPS;
-    // blocks per SM the shared memory allows (228 KB per SM, 1 KB reserved per block)
-    static constexpr int BLOCKS = (int)((228 * 1024) / (BLOCK_BYTES + 1024)) < 1
-                                      ? 1
-                                      : ((int)((228 * 1024) / (BLOCK_BYTES + 1024)) > 4
-                                             ? 4
-                                             : (int)((228 * 1024) / (BLOCK_BYTES + 1024)));
+    // blocks per SM the shared memory allows (228 KB per SM, 1 KB reserved per block), at most 4
+    static constexpr int SMEM_BLOCKS = (int)((228 * 1024) / (BLOCK_BYTES + 1024));
+    static constexpr int BLOCKS = SMEM_BLOCKS < 1 ? 1 : (SMEM_BLOCKS > 4 ? 4 : SMEM_BLOCKS);
 };
 
 // the check update of one check from its stage: DCT = compute width (>= deg; DCL = the stage
@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtLayout<DC, S>::BLOCKS)
     k_layer_tma(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2) {
     using LY = LtLayout<DC, S>;
     constexpr int LINE = LY::LINE;
+    constexpr int P = LY::P;
     extern __shared__ __align__(128) unsigned char lt_smem[];
     const int ti = blockIdx.y;
     if (ti >= ds.counts[0]) return;
@@ -236,11 +237,11 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtLayout<DC, S>::BLOCKS)
     if (nc <= 0) return;
     unsigned char *wb = lt_smem + (size_t)warp * LY::WARP_BYTES;
     float *stage = reinterpret_cast<float *>(wb);
-    uint64_t *bar = reinterpret_cast<uint64_t *>(wb + (size_t)LT_P * LY::STAGE * 4);
-    int *vidx = reinterpret_cast<int *>(bar + LT_P);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(wb + (size_t)P * LY::STAGE * 4);
+    int *vidx = reinterpret_cast<int *>(bar + P);
     if (lane == 0) {
 #pragma unroll
-        for (int p = 0; p < LT_P; ++p) mbar_init(&bar[p], 1);
+        for (int p = 0; p < P; ++p) mbar_init(&bar[p], 1);
         mbar_init_fence();
     }
     // the chunk's check ids, row bounds, syndrome words and column indices, fetched up front
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtLayout<DC, S>::BLOCKS)
         if (lane < deg) bulk_g2s(sp + lane * LINE, Lt + (size_t)vidx[i * DC + lane] * LINE, LINE * 4, &bar[p]);
         if (lane == 0 && deg > 0) bulk_g2s(sp + DC * LINE, mt + (size_t)lo * LINE, (uint32_t)deg * LINE * 4, &bar[p]);
     };
-    const int npre = min(LT_P, nc);
+    const int npre = min(P, nc);
     for (int i = 0; i < npre; ++i) issue(i, i);
     const uint32_t al = lane_act<S>(act, lane);
     uint32_t *hbt = reinterpret_cast<uint32_t *>(ds.hb + (size_t)t * cd.n);
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtLayout<DC, S>::BLOCKS)
     float *mw = ds.msg + (size_t)t * cd.E * LINE + lane * S;
     uint32_t phase = 0u;
     for (int i = 0; i < nc; ++i) {
-        const int p = i % LT_P;
+        const int p = i % P;
         mbar_wait(&bar[p], (phase >> p) & 1u);
         phase ^= 1u << p;
         const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
@@ -303,8 +304,64 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtLayout<DC, S>::BLOCKS)
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (i + LT_P < nc) issue(i + LT_P, p);
+        if (i + P < nc) issue(i + P, p);
     }
+}
+
+// ------------------------------------------------------------------ syndrome test (layered)
+//
+// H xhat = s for every active frame of the listed tiles (stopping rule A-12, decision of the
+// previous iteration): one thread per (check, tile) XORs the hard-decision words of the check's
+// variables (bit = lane, component = sub-tile) into its syndrome word; any nonzero bit marks that
+// frame unsatisfied.  Unlike the check-only k_cn (a warp per 4 checks), every thread has its own
+// independent gathers in flight.
+template <int S>
+__global__ void __launch_bounds__(256) k_synd_test(CodeDev cd, DecState ds) {
+    const int ti = blockIdx.y;
+    if (ti >= ds.counts[0]) return;
+    const int t = ds.active_list[ti];
+    const uint4 act = ds.tile_active[t];
+    __shared__ uint32_t s_unsat[SUBS];
+    if (threadIdx.x < SUBS) s_unsat[threadIdx.x] = 0u;
+    __syncthreads();
+    const int c = blockIdx.x * 256 + threadIdx.x;
+    uint32_t u[SUBS] = {0u, 0u, 0u, 0u};
+    if (c < cd.M) {
+        const uint4 sw = ds.st[(size_t)t * cd.M + c];
+        u[0] = sw.x;
+        u[1] = sw.y;
+        u[2] = sw.z;
+        u[3] = sw.w;
+        const uint4 *hbt = ds.hb + (size_t)t * cd.n;
+        const int lo = cd.row_ptr[c], hi = cd.row_ptr[c + 1];
+#pragma unroll 4
+        for (int e = lo; e < hi; ++e) {
+            const uint4 h = hbt[cd.col_idx[e]];
+            u[0] ^= h.x;
+            if (S > 1) u[1] ^= h.y;
+            if (S > 2) {
+                u[2] ^= h.z;
+                u[3] ^= h.w;
+            }
+        }
+    }
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+        const uint32_t v = __reduce_or_sync(FULL, u[q]) & cmpu(act, q);
+        if (lane == 0 && v) atomicOr(&s_unsat[q], v);
+    }
+    __syncthreads();
+    if (threadIdx.x < S && s_unsat[threadIdx.x])
+        atomicOr(reinterpret_cast<uint32_t *>(&ds.tile_unsat[t]) + threadIdx.x, s_unsat[threadIdx.x]);
+}
+
+void launch_synd_test(const CodeDev &cd, const DecState &ds, int grid_tiles, cudaStream_t s) {
+    if (grid_tiles <= 0) return;
+    dim3 grid((cd.M + 255) / 256, grid_tiles);
+    if (ds.subs == 4) k_synd_test<4><<<grid, 256, 0, s>>>(cd, ds);
+    else if (ds.subs == 2) k_synd_test<2><<<grid, 256, 0, s>>>(cd, ds);
+    else k_synd_test<1><<<grid, 256, 0, s>>>(cd, ds);
 }
 
 template <int DC, int S>
@@ -345,6 +402,11 @@ static bool layer_tma_enabled() {
     }();
     return v != 0;
 }
+
+// frames per lane of the layered kernels: 2 (64-frame tiles) for k_layer_tma at every supported
+// check degree (its registers do not hold whole lines: C4 88.8 vs 100.0 ms per step with one
+// frame per lane) and for k_layer up to degree 6; 1 for k_layer above (no spills)
+int layer_subs(int32_t max_dc) { return (layer_tma_enabled() || max_dc <= 6) ? 2 : 1; }
 
 template <int S>
 static bool launch_layer_s(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,

@@ -1,0 +1,15 @@
+# A/B of k_layer_tma variants on C4 (and C2) + layered parity tests
+cd $GRAFT_REPO_ROOT
+one() { timeout 300 env $1 python bench.py ${@:2} --no-e2e --no-cpu-baseline --steps 5 --warmup 3 2>gpurun_out/ab_err.txt | python -c "
+import json,sys
+d=json.loads(sys.stdin.readlines()[-1]); r=d['roofline']; b=d['roofline_bp_iteration']
+print('$*'.replace('build/variants/',''),'val %.4g'%d['value'],'ms %.2f'%d['ms_per_step'],'layer_frac %.3f'%r['frac'],'iter_frac %.3f'%b['frac'],'fer',d['fer'],[round(x,2) for x in d['mean_iters']],{k:round(v,2) for k,v in b['kernel_ms_per_step'].items()})" || tail -3 gpurun_out/ab_err.txt; }
+timeout 900 python -m pytest tests -m gpu -x -q -k "layered" > gpurun_out/t3_layered.log 2>&1; echo "layered rc $?"; tail -2 gpurun_out/t3_layered.log
+one CVSR_X=0
+one CVSR_SUBS=1
+one CVSR_LIB=build/variants/ch8.so
+one CVSR_LIB=build/variants/st2.so
+one CVSR_LIB=build/variants/st8.so
+one CVSR_LAYER_TMA=0
+one CVSR_X=0 --config C2
+one CVSR_LIB=build/variants/st8.so --config C2
