@@ -258,7 +258,8 @@ def main():
 
     # per-step hash keys (a fresh public key for every verification)
     key_rng = np.random.default_rng(1000 + rank)
-    keys = [int(k) for k in key_rng.integers(1, (1 << 61) - 2, size=args.warmup + 4 * args.steps + 1)]
+    keys = [[int(k) for k in key_rng.integers(1, (1 << 61) - 2, size=cvsr.CVSR_HASH_KEYS)]
+            for _ in range(args.warmup + 4 * args.steps + 1)]
     # untimed reference run for statistics (the batch is identical every step)
     st = pipe.step(x, y, want_stats=True, key=keys.pop())
     undetected = pipe.count_errors()[1]
@@ -361,7 +362,7 @@ def main():
         ectx = cvsr.cvsr_ctx_create(local, stream)
         sess = cvsr.cvsr_session_create(ectx, cfg.m, code_h, cfg.order, cvsr.make_quantiser(cfg.edges()),
                                         cfg.sigma_n, n, F, cvsr.decode_opts(cfg.max_iter, cfg.q_max, args.schedule))
-        cvsr.cvsr_session_set_verify(sess, 0x5DEECE66D)
+        cvsr.cvsr_session_set_verify(sess, [0x5DEECE66D, 0x2545F4914F6CDD1D % ((1 << 61) - 1), 0x9E3779B97F4A7C15 % ((1 << 61) - 1)])
         # the serving loop: K batches through cvsr_session_run_host_stream, batch b+1's H2D and
         # batch b-1's D2H overlapping batch b's kernels; every batch's copies are inside the
         # timed region (the same pinned buffers are re-sent each step)

@@ -99,17 +99,19 @@ C3 = SRConfig(
     order=(0,), max_iter=500,
 )
 
-# C4: standard settings: gamma = 2.21468, m = 5, delta* = 0.21359,
-# LSB-first caps (0.0006, 0.0022, 0.1670, 0.6485, 0.4918): S0, S1 disclosed; S2..S4 start
-# at 0.9*cap (0.150, 0.583, 0.442) and are backed off per tools/calibrate_rates.py: on B200
-# (512 frames) S2 irregular 0.150 and 0.100 give FER 1.0; 0.050 is below 0.1, where the paper
-# uses MET codes: the MET-style code at 0.05 gives FER 0 (6.4 iterations).
+# C4: standard settings: gamma = 2.21468, m = 5, delta* = 0.21359, LSB-first
+# capacities (0.0006, 0.0022, 0.1670, 0.6485, 0.4918).  Rates from the code database's back-off
+# (cvsr_inputs/codebook.json, tools/backoff.py on B200; PAPER.md:394 with reading R-2': start at
+# the database rate closest to capacity, Delta R = 0.05 until 1000 frames decode with no failure
+# and no undetected error): S0, S1 disclosed (below the floor 0.01); S2 0.166 and
+# 0.116 fail (irregular and MET-style), 0.066 MET-style good (5.8 iterations); S3 0.648 fails,
+# 0.598 good (16.5); S4 0.491 fails, 0.441 good (22.6).  beta = 0.7505 (round 1: 0.715).
 # N_R = 1e6 (the "~1e6" sub-block of Fig. 5), 125 frames per GPU of N = 1e9 on 8 GPUs.
 C4 = SRConfig(
     name="C4", m=5, gamma=2.214676, delta=0.21359, n=1_000_000, frames=125,
     slices=(SliceSpec(0, "disclosed"), SliceSpec(1, "disclosed"),
-            SliceSpec(2, "met", 0.05, (0.10, 0.05, 3, 6)), SliceSpec(3, "irregular", 0.583),
-            SliceSpec(4, "irregular", 0.442)),
+            SliceSpec(2, "met", 0.066, (0.132, 0.066, 3, 6)), SliceSpec(3, "irregular", 0.598),
+            SliceSpec(4, "irregular", 0.441)),
     order=(0, 1, 2, 3, 4),
 )
 

@@ -6,8 +6,9 @@
  * data-parallel hot path named by BASELINE.json's north star and scoped by
  * Gray-labelled constant-step quantisation (Bob), slice
  * syndromes (Bob), per-slice LLRs conditioned on already-known slices
- * (Alice), and syndrome-based flooding sum-product BP over many independent
- * LDPC sub-blocks ("frames") with per-frame early termination.
+ * (Alice), and syndrome-based sum-product BP (flooding, or row-layered per
+ * cvsr_decode_opts.flags) over many independent LDPC sub-blocks ("frames")
+ * with per-frame early termination.
  *
  * Conventions (apply to every entry point unless stated):
  *  - Ownership.  Every data buffer argument is CALLER-OWNED DEVICE memory of
@@ -249,14 +250,19 @@ cvsr_status cvsr_frame_hash(cvsr_ctx *ctx, const uint8_t *label, int32_t frames,
                             uint64_t *hash_out);
 
 /* Both sides of the PAPER.md:90 check in one launch (simulation: Bob's labels
- * are on the same device): hashes label_alice and label_bob (uint8[frames][n])
- * with cvsr_frame_hash's definition and key, and writes
- * verified_out[f] = frame_ok[f] && h_alice[f] == h_bob[f]  (uint8, 0/1).
+ * are on the same device), with CVSR_HASH_KEYS independent keys: hashes
+ * label_alice and label_bob (uint8[frames][n]) with cvsr_frame_hash's definition
+ * under each key keys[q] (HOST array; each in [1, 2^61 - 2], drawn independently
+ * and uniformly per check) and writes verified_out[f] = frame_ok[f] && h_alice[f][q]
+ * == h_bob[f][q] for every q (uint8, 0/1).  Two different strings pass with
+ * probability <= (W/(p-1))^CVSR_HASH_KEYS over the keys, W = ceil(n/4): <= 2^-122
+ * up to n = 5e6 (reading R-6; the 2^-120 target of the reference specification).
  * verified_out may alias frame_ok.  hash_alice_out / hash_bob_out
- * (uint64[frames]) may be NULL.  A frame that fails is discarded (reading R-6:
- * per-sub-block abort instead of restarting the whole protocol). */
+ * (uint64[frames][CVSR_HASH_KEYS]) may be NULL.  A frame that fails is discarded
+ * (reading R-6: per-sub-block abort instead of restarting the whole protocol). */
+#define CVSR_HASH_KEYS 3
 cvsr_status cvsr_verify(cvsr_ctx *ctx, const uint8_t *label_alice, const uint8_t *label_bob, const uint8_t *frame_ok,
-                        int32_t frames, int32_t n, uint64_t key, uint8_t *verified_out, uint64_t *hash_alice_out,
+                        int32_t frames, int32_t n, const uint64_t *keys, uint8_t *verified_out, uint64_t *hash_alice_out,
                         uint64_t *hash_bob_out);
 
 /* ------------------------------------------------------------ privacy amplification
@@ -319,12 +325,12 @@ cvsr_status cvsr_session_run_host_stream(cvsr_session *s, int32_t n_batches, con
                                          const float *const *y_host, uint8_t *const *label_host,
                                          uint8_t *const *frame_ok_host);
 
-/* Hash verification inside the session step: key != 0 makes
- * every later run / run_host call end with cvsr_verify on the session's
- * labels, so frame_ok (device buffer and frame_ok_host) reports
- * "converged AND hashes equal".  key = 0 turns it off (default).  stats_out
- * counts are taken before the hash check.  key must be 0 or in [1, 2^61 - 2]. */
-cvsr_status cvsr_session_set_verify(cvsr_session *s, uint64_t key);
+/* Hash verification inside the session step: keys != NULL (HOST
+ * array of CVSR_HASH_KEYS keys, as cvsr_verify) makes every later run / run_host
+ * call end with cvsr_verify on the session's labels, so frame_ok (device buffer
+ * and frame_ok_host) reports "converged AND all hashes equal".  keys = NULL turns
+ * it off (default).  stats_out counts are taken before the hash check. */
+cvsr_status cvsr_session_set_verify(cvsr_session *s, const uint64_t *keys);
 
 /* device pointers of the session's result buffers (any output may be NULL) */
 cvsr_status cvsr_session_buffers(const cvsr_session *s, uint8_t **label_bob, uint8_t **label_alice,

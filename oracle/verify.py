@@ -13,8 +13,12 @@ over GF(p), p = 2^61 - 1, applied per frame (sub-block):
 
 w_i = the i-th little-endian 32-bit word of the frame's label bytes, zero-padded
 to W = ceil(n/4) words.  Two different strings collide for at most W of the
-p - 1 keys (a nonzero polynomial of degree <= W has <= W roots), which is the
-bound eps_h the key-rate equation charges (PAPER.md:354 lists eps_h).
+p - 1 keys (a nonzero polynomial of degree <= W has <= W roots).  The check of
+PAPER.md:90 uses 3 independent keys (cvsr_verify): a wrong frame passes with
+probability <= (W/(p-1))^3 <= 2^-122 up to n = 5e6.  (PAPER.md:354 quotes a
+hashing parameter eps_h = 4.7e-13 for the alternate key-rate equation of
+[pirandola2021limits]; the adopted equation charges reconciliation failure to
+eps_EC, PAPER.md:266.)
 
 Pinned in tests/test_oracle_pins.py (key = 1 is the word checksum, key = 2^32
 is 2^32 * int.from_bytes(label, 'little') mod p, zero string, padding).

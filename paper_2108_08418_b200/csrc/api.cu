@@ -231,16 +231,6 @@ size_t smem_limit() {
 constexpr int GRAPH_ITERS = 8;      // iterations per captured graph
 constexpr int GRAPH_MAX_TILES = 2;  // batches of at most this many tiles take the graph path
 
-// layered schedule's syndrome test: k_synd_test (thread per check; default) or the check-only
-// k_cn (CVSR_SYND_CN=1)
-bool synd_test_kernel() {
-    static const int v = [] {
-        const char *e = getenv("CVSR_SYND_CN");
-        return (e && e[0] == '1') ? 0 : 1;
-    }();
-    return v != 0;
-}
-
 bool compact_enabled() {
     static int v = -1;
     if (v < 0) {
@@ -411,8 +401,7 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
         for (; k <= max_iter + 1; ++k) {
             const int final_pass = (k == max_iter + 1);
             prof_begin(ctx, KC_CN);
-            if (synd_test_kernel()) launch_synd_test(cd, ds, bound, s);
-            else launch_cn(cd, ds, bound, qmax, 1, s);
+            launch_synd_test(cd, ds, bound, s);
             prof_end(ctx);
             prof_begin(ctx, KC_CTRL);
             launch_status(ds, k, max_iter, final_pass, ctx->host_counts_dev, s);
@@ -736,6 +725,21 @@ cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, cons
         for (int32_t c = 0; c < n_checks; ++c) layer_chk[at[colour[c]]++] = c;
     }
 
+    // layer-ordered check descriptors + padded column table (layered kernels; CodeDev comment)
+    const int32_t ldc = n_layers > 0 ? layer_width(max_dc) : 0;
+    std::vector<int32_t> ldesc, lcol;
+    if (ldc > 0) {
+        ldesc.resize((size_t)n_checks * 4);
+        lcol.assign((size_t)n_checks * ldc, 0);
+        for (int32_t i = 0; i < n_checks; ++i) {
+            const int32_t c = layer_chk[i], lo = row_ptr[c], deg = row_ptr[c + 1] - lo;
+            ldesc[(size_t)i * 4 + 0] = lo;
+            ldesc[(size_t)i * 4 + 1] = deg;
+            ldesc[(size_t)i * 4 + 2] = c;
+            ldesc[(size_t)i * 4 + 3] = 0;
+            for (int32_t k = 0; k < deg; ++k) lcol[(size_t)i * ldc + k] = col_idx[lo + k];
+        }
+    }
     DeviceGuard g(ctx->device);
     cvsr_code *code = new cvsr_code();
     code->device = ctx->device;
@@ -743,7 +747,9 @@ cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, cons
     const size_t b_cp = align_up((size_t)(n_vars + 1) * 4), b_cs = align_up((size_t)E * 4);
     const size_t b_vv = align_up((size_t)n_vars * 4), b_vs = align_up((size_t)E * 4);
     const size_t b_lc = align_up((size_t)n_checks * 4);
-    cudaError_t e = cudaMalloc(&code->mem, b_rp + b_ci + b_cp + b_cs + b_vv + b_vs + b_lc);
+    const size_t b_ld = align_up(ldesc.size() * 4), b_lcol = align_up(lcol.size() * 4);
+    const size_t b_lp = ldc > 0 ? b_lc : 0;
+    cudaError_t e = cudaMalloc(&code->mem, b_rp + b_ci + b_cp + b_cs + b_vv + b_vs + b_lc + b_ld + b_lcol + b_lp);
     if (e != cudaSuccess) {
         delete code;
         cudaGetLastError();
@@ -765,6 +771,16 @@ cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, cons
     int32_t *d_lc = reinterpret_cast<int32_t *>(base + b_rp + b_ci + b_cp + b_cs + b_vv + b_vs);
     if (e6 == cudaSuccess && n_layers > 0)
         e6 = cudaMemcpy(d_lc, layer_chk.data(), (size_t)n_checks * 4, cudaMemcpyHostToDevice);
+    int4 *d_ld = reinterpret_cast<int4 *>(base + b_rp + b_ci + b_cp + b_cs + b_vv + b_vs + b_lc);
+    int32_t *d_lcol = reinterpret_cast<int32_t *>(base + b_rp + b_ci + b_cp + b_cs + b_vv + b_vs + b_lc + b_ld);
+    if (e6 == cudaSuccess && ldc > 0) e6 = cudaMemcpy(d_ld, ldesc.data(), ldesc.size() * 4, cudaMemcpyHostToDevice);
+    if (e6 == cudaSuccess && ldc > 0) e6 = cudaMemcpy(d_lcol, lcol.data(), lcol.size() * 4, cudaMemcpyHostToDevice);
+    int32_t *d_lp = reinterpret_cast<int32_t *>(base + b_rp + b_ci + b_cp + b_cs + b_vv + b_vs + b_lc + b_ld + b_lcol);
+    if (e6 == cudaSuccess && ldc > 0) {
+        std::vector<int32_t> lpos((size_t)n_checks);
+        for (int32_t i = 0; i < n_checks; ++i) lpos[layer_chk[i]] = i;
+        e6 = cudaMemcpy(d_lp, lpos.data(), (size_t)n_checks * 4, cudaMemcpyHostToDevice);
+    }
     if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess || e5 != cudaSuccess ||
         e6 != cudaSuccess) {
         cudaFree(code->mem);
@@ -792,6 +808,10 @@ cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, cons
     }
     d.layer_chk = d_lc;
     d.n_layers = n_layers;
+    d.layer_desc = ldc > 0 ? d_ld : nullptr;
+    d.layer_col = ldc > 0 ? d_lcol : nullptr;
+    d.layer_pos = ldc > 0 ? d_lp : nullptr;
+    d.layer_dc = ldc;
     for (int l = 0; l <= MAX_LAYERS; ++l) d.layer_off[l] = layer_off[l];
     code->d = d;
     *out = code;
@@ -973,7 +993,7 @@ cvsr_status cvsr_decode(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, 
     if (comp) ca = carve_compact(cv, tiles, subs, cd.n, cd.M, cd.E);
     cudaStream_t s = ctx->stream;
     launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, ds.subs, LOG2E, s);
-    launch_synd_transpose(synd, frames, cd.M, ds.subs, ds.st, tiles, s);
+    launch_synd_transpose(synd, frames, cd.M, ds.subs, ds.st, tiles, layered ? cd.layer_pos : nullptr, s);
     launch_init_tiles(ds, nullptr, s);
     launch_set_counts(ds, tiles, s);
     if (cvsr_status st = check_launch(ctx, 4)) return st;
@@ -1010,7 +1030,7 @@ cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float 
     float *post_il = cv.take<float>(post_bytes);
     cudaStream_t s = ctx->stream;
     launch_to_interleaved(llr, ds.L, frames, cd.n, tiles, ds.subs, LOG2E, s);
-    launch_synd_transpose(synd, frames, cd.M, ds.subs, ds.st, tiles, s);
+    launch_synd_transpose(synd, frames, cd.M, ds.subs, ds.st, tiles, layered ? cd.layer_pos : nullptr, s);
     launch_init_tiles(ds, nullptr, s);
     launch_set_counts(ds, tiles, s);
     int launched = 4;
@@ -1137,7 +1157,8 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
             CK(cudaMemsetAsync(bits_dec[j], 0, (size_t)frames * Wn * 4, s));
             launch_init_tiles(ds, alive, s);
             launch_set_counts(ds, tiles_j[j], s);
-            launch_synd_transpose(synd[j], frames, cd.M, ds.subs, ds.st, tiles_j[j], s);
+            launch_synd_transpose(synd[j], frames, cd.M, ds.subs, ds.st, tiles_j[j], lay_j[j] ? cd.layer_pos : nullptr,
+                                  s);
             LlrParams p;
             fill_llr_params(p, q, j, known_mask, sigma_n, opts->msg_clamp);
             for (int jj = 0; jj < m; ++jj) p.known_bits[jj] = known_bits[jj];
@@ -1199,15 +1220,19 @@ cvsr_status cvsr_frame_hash(cvsr_ctx *ctx, const uint8_t *label, int32_t frames,
 }
 
 cvsr_status cvsr_verify(cvsr_ctx *ctx, const uint8_t *label_alice, const uint8_t *label_bob, const uint8_t *frame_ok,
-                        int32_t frames, int32_t n, uint64_t key, uint8_t *verified_out, uint64_t *hash_alice_out,
+                        int32_t frames, int32_t n, const uint64_t *keys, uint8_t *verified_out, uint64_t *hash_alice_out,
                         uint64_t *hash_bob_out) {
     if (cvsr_status st = check_ctx(ctx)) return st;
     if (frames < 0 || n <= 0) return fail(CVSR_ESHAPE, "frames=%d n=%d", frames, n);
-    if (key == 0 || key >= ((1ull << 61) - 1ull)) return fail(CVSR_EINVAL, "key must be in [1, 2^61 - 2]");
+    if (!keys) return fail(CVSR_EINVAL, "null keys");
+    for (int q = 0; q < CVSR_HASH_KEYS; ++q)
+        if (keys[q] == 0 || keys[q] >= ((1ull << 61) - 1ull)) return fail(CVSR_EINVAL, "key %d not in [1, 2^61 - 2]", q);
     if (frames == 0) return CVSR_OK;
     if (!label_alice || !label_bob || !frame_ok || !verified_out) return fail(CVSR_EINVAL, "null buffer");
     DeviceGuard g(ctx->device);
-    launch_verify(label_alice, label_bob, frame_ok, frames, n, key, verified_out,
+    unsigned long long k[CVSR_HASH_KEYS];
+    for (int q = 0; q < CVSR_HASH_KEYS; ++q) k[q] = keys[q];
+    launch_verify(label_alice, label_bob, frame_ok, frames, n, k, verified_out,
                   reinterpret_cast<unsigned long long *>(hash_alice_out),
                   reinterpret_cast<unsigned long long *>(hash_bob_out), ctx->stream);
     return check_launch(ctx, 1);

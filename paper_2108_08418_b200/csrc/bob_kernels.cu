@@ -374,11 +374,16 @@ __device__ __forceinline__ uint32_t label_word(const uint8_t *__restrict__ lab, 
 //   h = sum_t key^(t+1) * sum_k w_{t+kT} (key^T)^k,
 // each inner sum by Horner in K = key^T, then a block reduction.  Exact modular
 // arithmetic, so the result is independent of T and bit-identical to the definition.
-// NL = 2 hashes label_a and label_b together and writes ok[f] &= (h_a == h_b).
-template <int NL>
+// NL = 2 hashes label_a and label_b together; NK independent keys (hash h[f][k] per key);
+// ok[f] &= (h_a == h_b for every key).
+struct HashKeys {
+    unsigned long long k[CVSR_HASH_KEYS];
+};
+
+template <int NL, int NK>
 __global__ void __launch_bounds__(256) k_frame_hash(const uint8_t *__restrict__ label_a,
-                                                   const uint8_t *__restrict__ label_b, int32_t n,
-                                                   unsigned long long key, unsigned long long *__restrict__ out_a,
+                                                   const uint8_t *__restrict__ label_b, int32_t n, HashKeys keys,
+                                                   unsigned long long *__restrict__ out_a,
                                                    unsigned long long *__restrict__ out_b,
                                                    const uint8_t *__restrict__ ok_in, uint8_t *__restrict__ ok_out) {
     const int f = blockIdx.x, T = blockDim.x, t = threadIdx.x;
@@ -386,44 +391,66 @@ __global__ void __launch_bounds__(256) k_frame_hash(const uint8_t *__restrict__ 
     const bool aligned = (n & 3) == 0;
     const uint8_t *la = label_a + (size_t)f * n;
     const uint8_t *lb = NL == 2 ? label_b + (size_t)f * n : nullptr;
-    const unsigned long long K = powmod61(key, (unsigned long long)T);
-    unsigned long long ha = 0ull, hb = 0ull;
+    unsigned long long K[NK], h[NL][NK];
+#pragma unroll
+    for (int q = 0; q < NK; ++q) {
+        K[q] = powmod61(keys.k[q], (unsigned long long)T);
+        h[0][q] = 0ull;
+        if (NL == 2) h[NL - 1][q] = 0ull;
+    }
     const int kmax = t < W ? (W - 1 - t) / T : -1;
     for (int k = kmax; k >= 0; --k) {
         const int i = t + k * T;
-        ha = addmod61(mulmod61(ha, K), label_word(la, n, i, aligned));
-        if (NL == 2) hb = addmod61(mulmod61(hb, K), label_word(lb, n, i, aligned));
+        const uint32_t wa = label_word(la, n, i, aligned);
+        const uint32_t wb = NL == 2 ? label_word(lb, n, i, aligned) : 0u;
+#pragma unroll
+        for (int q = 0; q < NK; ++q) {
+            h[0][q] = addmod61(mulmod61(h[0][q], K[q]), wa);
+            if (NL == 2) h[NL - 1][q] = addmod61(mulmod61(h[NL - 1][q], K[q]), wb);
+        }
     }
-    const unsigned long long kt = powmod61(key, (unsigned long long)(t + 1));
-    __shared__ unsigned long long s[2][256];
-    s[0][t] = mulmod61(ha, kt);
-    if (NL == 2) s[1][t] = mulmod61(hb, kt);
+    __shared__ unsigned long long s[NL * NK][256];
+#pragma unroll
+    for (int q = 0; q < NK; ++q) {
+        const unsigned long long kt = powmod61(keys.k[q], (unsigned long long)(t + 1));
+#pragma unroll
+        for (int l = 0; l < NL; ++l) s[l * NK + q][t] = mulmod61(h[l][q], kt);
+    }
     __syncthreads();
     for (int o = T / 2; o > 0; o >>= 1) {
         if (t < o) {
-            s[0][t] = addmod61(s[0][t], s[0][t + o]);
-            if (NL == 2) s[1][t] = addmod61(s[1][t], s[1][t + o]);
+#pragma unroll
+            for (int r = 0; r < NL * NK; ++r) s[r][t] = addmod61(s[r][t], s[r][t + o]);
         }
         __syncthreads();
     }
     if (t == 0) {
-        if (out_a) out_a[f] = s[0][0];
-        if (NL == 2) {
-            if (out_b) out_b[f] = s[1][0];
-            ok_out[f] = (uint8_t)(ok_in[f] && s[0][0] == s[1][0]);
+        bool eq = true;
+#pragma unroll
+        for (int q = 0; q < NK; ++q) {
+            if (out_a) out_a[(size_t)f * NK + q] = s[q][0];
+            if (NL == 2) {
+                if (out_b) out_b[(size_t)f * NK + q] = s[NK + q][0];
+                eq = eq && s[q][0] == s[NK + q][0];
+            }
         }
+        if (NL == 2) ok_out[f] = (uint8_t)(ok_in[f] && eq);
     }
 }
 
 void launch_frame_hash(const uint8_t *label, int32_t F, int32_t n, unsigned long long key, unsigned long long *out,
                        cudaStream_t s) {
-    k_frame_hash<1><<<F, 256, 0, s>>>(label, nullptr, n, key, out, nullptr, nullptr, nullptr);
+    HashKeys k{};
+    k.k[0] = key;
+    k_frame_hash<1, 1><<<F, 256, 0, s>>>(label, nullptr, n, k, out, nullptr, nullptr, nullptr);
 }
 
 void launch_verify(const uint8_t *label_a, const uint8_t *label_b, const uint8_t *ok_in, int32_t F, int32_t n,
-                   unsigned long long key, uint8_t *ok_out, unsigned long long *ha, unsigned long long *hb,
+                   const unsigned long long *keys, uint8_t *ok_out, unsigned long long *ha, unsigned long long *hb,
                    cudaStream_t s) {
-    k_frame_hash<2><<<F, 256, 0, s>>>(label_a, label_b, n, key, ha, hb, ok_in, ok_out);
+    HashKeys k{};
+    for (int q = 0; q < CVSR_HASH_KEYS; ++q) k.k[q] = keys[q];
+    k_frame_hash<2, CVSR_HASH_KEYS><<<F, 256, 0, s>>>(label_a, label_b, n, k, ha, hb, ok_in, ok_out);
 }
 
 }  // namespace cvsr

@@ -132,6 +132,18 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
+// per-thread asynchronous global -> shared copy of 4 or 8 bytes (cp.async.ca, LDGSTS)
+template <int BYTES>
+__device__ __forceinline__ void cp_async_g2s(void *dst, const void *src) {
+    static_assert(BYTES == 4 || BYTES == 8 || BYTES == 16, "cp.async size");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES) : "memory");
+}
+// the mbarrier tracks this thread's prior cp.async copies: one pending arrival is added now and
+// arrives when they have landed
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // make this thread's mbarrier.init visible (to the async proxy) before any use
 __device__ __forceinline__ void mbar_init_fence() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");

@@ -871,7 +871,8 @@ __global__ void __launch_bounds__(256) k_from_interleaved(const float *__restric
 
 // public syndrome [F][Wm] -> per-tile lane-bit words st[t][c] (uint4 over sub-tiles)
 __global__ void __launch_bounds__(BLOCK) k_synd_transpose(const uint32_t *__restrict__ synd, int32_t F, int32_t M,
-                                                           int subs, uint4 *__restrict__ st) {
+                                                           int subs, uint4 *__restrict__ st,
+                                                           const int32_t *__restrict__ pos) {
     const int t = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Wm = words_of(M);
@@ -888,7 +889,7 @@ __global__ void __launch_bounds__(BLOCK) k_synd_transpose(const uint32_t *__rest
         }
     }
     const int c = w * 32 + lane;
-    if (c < M) st[(size_t)t * M + c] = make_uint4(mine[0], mine[1], mine[2], mine[3]);
+    if (c < M) st[(size_t)t * M + (pos ? pos[c] : c)] = make_uint4(mine[0], mine[1], mine[2], mine[3]);
 }
 
 // initial tile state: active frames = valid frames (& alive mask if given)
@@ -1414,9 +1415,9 @@ void launch_from_interleaved(const float *src, float *dst, int32_t F, int64_t ro
 }
 
 void launch_synd_transpose(const uint32_t *synd, int32_t F, int32_t M, int subs, uint4 *st, int tiles,
-                           cudaStream_t s) {
+                           const int32_t *pos, cudaStream_t s) {
     dim3 grid((words_of(M) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, tiles);
-    k_synd_transpose<<<grid, BLOCK, 0, s>>>(synd, F, M, subs, st);
+    k_synd_transpose<<<grid, BLOCK, 0, s>>>(synd, F, M, subs, st, pos);
 }
 
 void launch_init_tiles(const DecState &ds, const uint8_t *alive, cudaStream_t s) {

@@ -51,9 +51,19 @@ struct CodeDev {
     const int32_t *layer_chk;      // [M]
     int32_t n_layers;              // 0: more than MAX_LAYERS colours (layered schedule unavailable)
     int32_t layer_off[MAX_LAYERS + 1];
+    // the same checks in layer order as self-contained descriptors, so a warp's chunk of checks
+    // needs no dependent index loads: layer_desc[i] = {row_ptr[c], degree, c, 0} for
+    // c = layer_chk[i]; layer_col[i * layer_dc + k] = col_idx[row_ptr[c] + k] (0-padded to the
+    // layered kernels' compute width layer_dc); null when the layered kernels do not apply
+    const int4 *layer_desc;        // [M]
+    const int32_t *layer_pos;      // [M] position of check c in layer order (inverse of layer_chk)
+    const int32_t *layer_col;      // [M * layer_dc]
+    int32_t layer_dc;
 };
 
-// Per-decode device state (lives in the context's scratch arena).
+// Per-decode device state (lives in the context's scratch arena).  Syndrome rows st are in check
+// order for the flooding schedule and in layer order (row i = check layer_chk[i]) for the layered
+// schedule (launch_synd_transpose's pos argument).
 // Masks and bit words are uint4: component s holds the 32 lanes of sub-tile s.
 struct DecState {
     int32_t tiles;
@@ -113,6 +123,12 @@ constexpr float LLR_XMAX = 10.0f;
 constexpr float LLR_H = 2.0f * LLR_XMAX / 4096.0f;
 
 __host__ __device__ inline int32_t words_of(int64_t bits) { return (int32_t)((bits + 31) / 32); }
+
+// compute width of the layered kernels for a code's maximum check degree (the template DC of
+// k_layer / k_layer_tma): exact for 3..10, 2 for degrees <= 2, 12 for 11..12; 0 = unsupported
+inline int32_t layer_width(int32_t max_dc) {
+    return max_dc <= 2 ? 2 : (max_dc <= 10 ? max_dc : (max_dc <= 12 ? 12 : 0));
+}
 
 // frames per lane for a batch: the smallest S in {1, 2, 4} whose tiles are not
 // mostly empty (S = 4 once there are more than 64 frames)

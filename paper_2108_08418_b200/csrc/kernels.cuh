@@ -19,7 +19,7 @@ void launch_to_interleaved(const float *src, float *dst, int32_t F, int64_t rows
 void launch_from_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, int subs, float scale,
                              cudaStream_t s);
 void launch_synd_transpose(const uint32_t *synd, int32_t F, int32_t M, int subs, uint4 *st, int tiles,
-                           cudaStream_t s);
+                           const int32_t *pos /*nullable: row of check c = pos[c]*/, cudaStream_t s);
 void launch_init_tiles(const DecState &ds, const uint8_t *alive, cudaStream_t s);
 void launch_set_counts(const DecState &ds, int32_t n_active, cudaStream_t s);
 bool layered_supported(const CodeDev &cd);
@@ -41,8 +41,8 @@ void launch_syndrome_bits(const CodeDev &cd, const uint32_t *bits, int32_t F, ui
 void launch_frame_hash(const uint8_t *label, int32_t F, int32_t n, unsigned long long key, unsigned long long *out,
                        cudaStream_t s);
 void launch_verify(const uint8_t *label_a, const uint8_t *label_b, const uint8_t *ok_in, int32_t F, int32_t n,
-                   unsigned long long key, uint8_t *ok_out, unsigned long long *ha, unsigned long long *hb,
-                   cudaStream_t s);
+                   const unsigned long long *keys /*host [CVSR_HASH_KEYS]*/, uint8_t *ok_out, unsigned long long *ha,
+                   unsigned long long *hb, cudaStream_t s);
 void launch_count_errors(const uint8_t *a, const uint8_t *b, const uint8_t *ok, int32_t F, int32_t n,
                          unsigned long long *counts, cudaStream_t s);
 

@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(BLOCK, layer_minb(DC, S)) k_layer(CodeDev cd, 
         for (int i = 0; i < nc; ++i) {
             const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
             const int c = __shfl_sync(FULL, myc, i);
-            const uint32_t sb = lane_act<S>(stt[c], lane);
+            const uint32_t sb = lane_act<S>(stt[lbeg + i0 + i], lane);  // rows in layer order
             layer_check<DC, S>(cd, ds, t, act, lo, deg, sb,
                                [&](int k) { return __shfl_sync(FULL, myv, i * DC + k); }, lane, qmax2);
         }
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(BLOCK, layer_minb(DC, S)) k_layer(CodeDev cd, 
         for (int i = 0; i < nc; ++i) {
             const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
             const int c = __shfl_sync(FULL, myc, i);
-            const uint32_t sb = lane_act<S>(stt[c], lane);
+            const uint32_t sb = lane_act<S>(stt[lbeg + i0 + i], lane);  // rows in layer order
             const int myv = lane < deg ? cd.col_idx[lo + lane] : 0;
             layer_check<DC, S>(cd, ds, t, act, lo, deg, sb, [&](int k) { return __shfl_sync(FULL, myv, k); },
                                lane, qmax2);
@@ -156,9 +156,10 @@ __global__ void __launch_bounds__(BLOCK, layer_minb(DC, S)) k_layer(CodeDev cd, 
 // staged in shared memory by bulk asynchronous copies (cp.async.bulk, the TMA engine's
 // non-tensor path) instead of register loads, so the number of bytes in flight no longer
 // depends on registers.  Each warp owns P (2-3) stages and walks LT_CH checks of the layer:
-//   issue:   one elected lane arms the stage's mbarrier with the stage's byte count; lane k < deg
-//            copies the posterior line of the check's k-th variable (128 S bytes, gathered), lane 0
-//            copies the check's deg message lines (one contiguous span: CSR slots are contiguous);
+//   issue:   every lane copies its S frames of the posterior lines of the check's variables
+//            (cp.async, 4 S bytes per lane and line, gathered; the stage's mbarrier tracks them),
+//            lane 0 arms the mbarrier with the message bytes and copies the check's deg message
+//            lines with one bulk copy (one contiguous span: CSR slots are contiguous);
 //   compute: after the mbarrier phase completes, every lane reads its S frames of each line
 //            from shared memory, runs the sum/difference CN update (cn_update) per frame and
 //            writes r_e and post_v = q_e + r_e back into the stage, plus the hard decisions;
@@ -169,9 +170,12 @@ __global__ void __launch_bounds__(BLOCK, layer_minb(DC, S)) k_layer(CodeDev cd, 
 // Checks of one layer share no variable, so prefetching the next checks' posterior lines while
 // the current check is being written is exact.  The arithmetic is k_layer's operation for
 // operation (results are bit-identical).
-constexpr int LT_WARPS = 8;  // warps per block
+constexpr int LT_WARPS = 8;  // warps per block (k_layer_tmap, and k_layer_tma for S <= 2)
+// k_layer_tma: 4 warps per block at 4 frames per lane (512-byte lines: a warp's two stages take
+// 14 KB at check degree 7, so 8-warp blocks would leave one block per SM)
+__host__ __device__ constexpr int lt_warps(int S) { return S == 4 ? 4 : 8; }
 #ifndef CVSR_LT_CH
-#define CVSR_LT_CH 8
+#define CVSR_LT_CH 4
 #endif
 #ifndef CVSR_LT_STAGE_KB
 #define CVSR_LT_STAGE_KB 3
@@ -186,7 +190,7 @@ struct LtLayout {
     static constexpr int P = (STAGE * 4 <= CVSR_LT_STAGE_KB * 1024) ? 3 : 2;
     static constexpr size_t RAW = (size_t)P * STAGE * 4 + P * 8 + (size_t)LT_CH * DC * 4;
     static constexpr size_t WARP_BYTES = (RAW + 127) & ~(size_t)127;
-    static constexpr size_t BLOCK_BYTES = WARP_BYTES * LT_WARPS;
+    static constexpr size_t BLOCK_BYTES = WARP_BYTES * lt_warps(S);
     // blocks per SM the shared memory allows (228 KB per SM, 1 KB reserved per block), at most 4
     static constexpr int SMEM_BLOCKS = (int)((228 * 1024) / (BLOCK_BYTES + 1024));
     static constexpr int BLOCKS = SMEM_BLOCKS < 1 ? 1 : (SMEM_BLOCKS > 4 ? 4 : SMEM_BLOCKS);
@@ -195,33 +199,31 @@ struct LtLayout {
 // the check update of one check from its stage: DCT = compute width (>= deg; DCL = the stage
 // layout's DC).  Results overwrite the stage: posterior lines <- post_v, message lines <- r_e.
 template <int DCT, int DCL, int S>
-__device__ __forceinline__ void lt_compute(float *__restrict__ sp, int deg, uint32_t sb, const uint4 &act, int lane,
-                                           float qmax2, uint32_t *__restrict__ hbt, const int *__restrict__ vrow) {
+__device__ __forceinline__ void lt_compute(float *__restrict__ sp, int deg, uint32_t sb, int lane, float qmax2) {
     constexpr int LINE = LANES * S;
     float *pp = sp + lane * S;               // posterior lines
     float *rp = sp + DCL * LINE + lane * S;  // message lines
-#pragma unroll
+#pragma unroll(S == 4 ? 1 : S)
     for (int s = 0; s < S; ++s) {
-        float a[DCT];
+        float qu[DCT], a[DCT];
 #pragma unroll
-        for (int k = 0; k < DCT; ++k) a[k] = (k < deg) ? clampf(pp[k * LINE + s] - rp[k * LINE + s], qmax2) : DUMMY_Q;
+        for (int k = 0; k < DCT; ++k) {
+            qu[k] = (k < deg) ? pp[k * LINE + s] - rp[k * LINE + s] : DUMMY_Q;
+            a[k] = (k < deg) ? clampf(qu[k], qmax2) : DUMMY_Q;
+        }
         cn_update<DCT>(a, (sb >> s) & 1u, qmax2);
-        const uint32_t am = cmpu(act, s);
 #pragma unroll
         for (int k = 0; k < DCT; ++k) {
             if (k < deg) {
-                const float post = (pp[k * LINE + s] - rp[k * LINE + s]) + a[k];
                 rp[k * LINE + s] = a[k];
-                pp[k * LINE + s] = post;
-                const uint32_t w = __ballot_sync(FULL, post < 0.0f) & am;
-                if (lane == 0) hbt[(size_t)vrow[k] * 4 + s] = w;
+                pp[k * LINE + s] = qu[k] + a[k];
             }
         }
     }
 }
 
 template <int DC, int S>
-__global__ void __launch_bounds__(LT_WARPS * 32, LtLayout<DC, S>::BLOCKS)
+__global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
     k_layer_tma(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2) {
     using LY = LtLayout<DC, S>;
     constexpr int LINE = LY::LINE;
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtLayout<DC, S>::BLOCKS)
     const int t = ds.active_list[ti];
     const uint4 act = ds.tile_active[t];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i0 = (blockIdx.x * LT_WARPS + warp) * LT_CH;
+    const int i0 = (blockIdx.x * lt_warps(S) + warp) * LT_CH;
     const int nc = min(LT_CH, lcnt - i0);
     if (nc <= 0) return;
     unsigned char *wb = lt_smem + (size_t)warp * LY::WARP_BYTES;
@@ -244,26 +246,33 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtLayout<DC, S>::BLOCKS)
         for (int p = 0; p < P; ++p) mbar_init(&bar[p], 1);
         mbar_init_fence();
     }
-    // the chunk's check ids, row bounds, syndrome words and column indices, fetched up front
-    const int myc = lane < nc ? cd.layer_chk[lbeg + i0 + lane] : 0;
-    const int mylo = lane < nc ? cd.row_ptr[myc] : 0;
-    const int myhi = lane < nc ? cd.row_ptr[myc + 1] : 0;
-    const uint4 mys = lane < nc ? ds.st[(size_t)t * cd.M + myc] : make_uint4(0u, 0u, 0u, 0u);
-    for (int f0 = 0; f0 < LT_CH * DC; f0 += LANES) {
-        const int f = f0 + lane;
-        const int i = min(f / DC, LT_CH - 1), k = f - i * DC;
-        const int lo = __shfl_sync(FULL, mylo, i), hi = __shfl_sync(FULL, myhi, i);
-        if (f < LT_CH * DC) vidx[f] = (i < nc && k < hi - lo) ? cd.col_idx[lo + k] : 0;
-    }
+    // the chunk's descriptors {row start, degree, check id}, padded column indices and syndrome
+    // rows: independent coalesced loads (layer_desc / layer_col built in layer order at code load;
+    // st rows are in layer order for the layered schedule)
+    const int g0 = lbeg + i0;
+    const int4 dsc = lane < nc ? cd.layer_desc[g0 + lane] : make_int4(0, 0, 0, 0);
+    for (int f = lane; f < LT_CH * DC; f += LANES) vidx[f] = f < nc * DC ? cd.layer_col[(size_t)g0 * DC + f] : 0;
+    const int mylo = dsc.x, myhi = dsc.x + dsc.y;
+    const uint4 mys = lane < nc ? ds.st[(size_t)t * cd.M + g0 + lane] : make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     const float *Lt = ds.L + (size_t)t * cd.n * LINE;
     const float *mt = ds.msg + (size_t)t * cd.E * LINE;
+    // stage p of check i: every lane copies its S frames of the deg posterior lines (cp.async,
+    // tracked by the stage's mbarrier); lane 0 arms the barrier with the message bytes and copies
+    // the deg message lines, one contiguous CSR span, with one bulk copy
     auto issue = [&](int i, int p) {
         const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
         float *sp = stage + (size_t)p * LY::STAGE;
-        if (lane == 0) mbar_arrive_tx(&bar[p], 2u * (uint32_t)deg * LINE * 4u);
-        if (lane < deg) bulk_g2s(sp + lane * LINE, Lt + (size_t)vidx[i * DC + lane] * LINE, LINE * 4, &bar[p]);
-        if (lane == 0 && deg > 0) bulk_g2s(sp + DC * LINE, mt + (size_t)lo * LINE, (uint32_t)deg * LINE * 4, &bar[p]);
+        const int *vr = vidx + i * DC;
+#pragma unroll
+        for (int k = 0; k < DC; ++k)
+            if (k < deg) cp_async_g2s<4 * S>(sp + k * LINE + lane * S, Lt + (size_t)vr[k] * LINE + lane * S);
+        cp_async_mbar_arrive(&bar[p]);
+        __syncwarp();  // every lane's pending-count increment precedes lane 0's arrival
+        if (lane == 0) {
+            mbar_arrive_tx(&bar[p], (uint32_t)deg * LINE * 4u);
+            if (deg > 0) bulk_g2s(sp + DC * LINE, mt + (size_t)lo * LINE, (uint32_t)deg * LINE * 4, &bar[p]);
+        }
     };
     const int npre = min(P, nc);
     for (int i = 0; i < npre; ++i) issue(i, i);
@@ -287,24 +296,279 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtLayout<DC, S>::BLOCKS)
         const int *vrow = vidx + i * DC;
         if constexpr (DC >= 6) {
             // degree-2 checks of a code with a large maximum degree (MET type-A checks)
-            if (deg <= 2) lt_compute<2, DC, S>(sp, deg, sb, act, lane, qmax2, hbt, vrow);
-            else lt_compute<DC, DC, S>(sp, deg, sb, act, lane, qmax2, hbt, vrow);
+            if (deg <= 2) lt_compute<2, DC, S>(sp, deg, sb, lane, qmax2);
+            else lt_compute<DC, DC, S>(sp, deg, sb, lane, qmax2);
         } else {
-            lt_compute<DC, DC, S>(sp, deg, sb, act, lane, qmax2, hbt, vrow);
+            lt_compute<DC, DC, S>(sp, deg, sb, lane, qmax2);
         }
         __syncwarp();
-        if (al) {
+        // lane-vectorised stores of r_e and post_v, and the hard decisions [post_v < 0] of the
+        // tile's active frames (one word per sub-tile, stored together)
 #pragma unroll
-            for (int k = 0; k < DC; ++k) {
-                if (k < deg) {
+        for (int k = 0; k < DC; ++k) {
+            if (k < deg) {
+                const FV<S> post = ldv<S>(sp + k * LINE + lane * S);
+                if (al) {
                     stv<S>(mw + (size_t)(lo + k) * LINE, ldv<S>(sp + (DC + k) * LINE + lane * S));
-                    stv<S>(Lw + (size_t)vrow[k] * LINE, ldv<S>(sp + k * LINE + lane * S));
+                    stv<S>(Lw + (size_t)vrow[k] * LINE, post);
+                }
+                uint32_t w[S];
+#pragma unroll
+                for (int q = 0; q < S; ++q) w[q] = __ballot_sync(FULL, post.c[q] < 0.0f) & cmpu(act, q);
+                if (lane == 0) {
+                    uint32_t *h = hbt + (size_t)vrow[k] * 4;
+                    if constexpr (S == 1) h[0] = w[0];
+                    else if constexpr (S == 2) *reinterpret_cast<uint2 *>(h) = make_uint2(w[0], w[1]);
+                    else *reinterpret_cast<uint4 *>(h) = make_uint4(w[0], w[1], w[2], w[3]);
                 }
             }
         }
         fence_proxy_async_smem();
         __syncwarp();
         if (i + P < nc) issue(i + P, p);
+    }
+}
+
+// ------------------------------------------------------------------ persistent layer kernel
+//
+// k_layer_tmap<DC, S>: k_layer_tma's check update with a persistent grid.  The layer's work items
+// (tile, chunk of LT_CH checks) are spread over all resident warps (item = warp id + k x warps);
+// each warp runs ONE stage ring over the concatenated checks of its items, so the ring never
+// drains between items, and each item's metadata -- descriptors, syndrome rows, padded column
+// indices and the tile's active mask -- is copied into shared memory by cp.async one item ahead
+// (tracked by a per-buffer mbarrier), so no dependent index load stalls the warp.  Results are
+// bit-identical to k_layer_tma (same arithmetic per check; checks of a layer are independent).
+template <int DC, int S>
+struct LtpLayout {
+    using LY = LtLayout<DC, S>;
+    static constexpr int META = 16 * LT_CH * 2 + 16 + 4 * LT_CH * DC;  // desc, st rows, act, vidx
+    static constexpr int META_AL = (META + 15) & ~15;
+    static constexpr int BARS = ((LY::P + 2) * 8 + 15) & ~15;  // stage + metadata barriers, 16-B aligned
+    static constexpr size_t RAW = (size_t)LY::P * LY::STAGE * 4 + BARS + 2 * (size_t)META_AL;
+    static constexpr size_t WARP_BYTES = (RAW + 127) & ~(size_t)127;
+    static constexpr size_t BLOCK_BYTES = WARP_BYTES * LT_WARPS;
+    static constexpr int SMEM_BLOCKS = (int)((228 * 1024) / (BLOCK_BYTES + 1024));
+    static constexpr int BLOCKS = SMEM_BLOCKS < 1 ? 1 : (SMEM_BLOCKS > 4 ? 4 : SMEM_BLOCKS);
+};
+
+template <int DC, int S>
+__global__ void __launch_bounds__(LT_WARPS * 32, LtpLayout<DC, S>::BLOCKS)
+    k_layer_tmap(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2) {
+    using LY = LtLayout<DC, S>;
+    using LP = LtpLayout<DC, S>;
+    constexpr int LINE = LY::LINE;
+    constexpr int P = LY::P;
+    extern __shared__ __align__(128) unsigned char lt_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cpt = (lcnt + LT_CH - 1) / LT_CH;
+    const int n_items = ds.counts[0] * cpt;
+    const int W = gridDim.x * LT_WARPS;
+    int it_cur = blockIdx.x * LT_WARPS + warp;
+    if (it_cur >= n_items) return;
+    unsigned char *wb = lt_smem + (size_t)warp * LP::WARP_BYTES;
+    float *stage = reinterpret_cast<float *>(wb);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(wb + (size_t)P * LY::STAGE * 4);
+    uint64_t *mbar = bar + P;  // metadata barriers of the two item buffers
+    unsigned char *meta0 = wb + (size_t)P * LY::STAGE * 4 + LP::BARS;
+    if (lane == 0) {
+#pragma unroll
+        for (int p = 0; p < P + 2; ++p) mbar_init(&bar[p], 1);
+        mbar_init_fence();
+    }
+    __syncwarp();
+    // metadata buffer b: desc[LT_CH] int4 | strow[LT_CH] uint4 | act uint4 | vidx[LT_CH * DC] int
+    auto m_desc = [&](int b) { return reinterpret_cast<int4 *>(meta0 + (size_t)b * LP::META_AL); };
+    auto m_st = [&](int b) { return reinterpret_cast<uint4 *>(meta0 + (size_t)b * LP::META_AL + 16 * LT_CH); };
+    auto m_act = [&](int b) { return reinterpret_cast<uint4 *>(meta0 + (size_t)b * LP::META_AL + 32 * LT_CH); };
+    auto m_vidx = [&](int b) { return reinterpret_cast<int *>(meta0 + (size_t)b * LP::META_AL + 32 * LT_CH + 16); };
+    struct Item {
+        int t, nc, g0, b;
+        bool valid;
+    };
+    auto make = [&](int item, int t, int b) {
+        Item x;
+        x.valid = item < n_items;
+        x.b = b;
+        x.t = t;
+        x.nc = 0;
+        x.g0 = 0;
+        if (x.valid) {
+            const int ch = item % cpt;
+            x.g0 = lbeg + ch * LT_CH;
+            x.nc = min(LT_CH, lcnt - ch * LT_CH);
+        }
+        return x;
+    };
+    auto tile_of = [&](int item) { return item < n_items ? ds.active_list[item / cpt] : 0; };
+    // asynchronous metadata copy of an item into its buffer (every lane copies its part)
+    auto fetch = [&](const Item &x) {
+        if (!x.valid) return;
+        if (lane < x.nc) {
+            cp_async_g2s<16>(m_desc(x.b) + lane, cd.layer_desc + x.g0 + lane);
+            cp_async_g2s<16>(m_st(x.b) + lane, ds.st + (size_t)x.t * cd.M + x.g0 + lane);
+        }
+        if (lane == 31) cp_async_g2s<16>(m_act(x.b), ds.tile_active + x.t);
+        int *vx = m_vidx(x.b);
+        for (int f = lane; f < x.nc * DC; f += LANES) cp_async_g2s<4>(vx + f, cd.layer_col + (size_t)x.g0 * DC + f);
+        cp_async_mbar_arrive(&mbar[x.b]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&mbar[x.b]);
+    };
+    uint32_t mph = 0u;  // phase bit per metadata buffer
+    auto meta_wait = [&](const Item &x) {
+        mbar_wait(&mbar[x.b], (mph >> x.b) & 1u);
+        mph ^= 1u << x.b;
+    };
+    // stage p of check i of item x (see k_layer_tma)
+    auto issue = [&](const Item &x, int i, int p) {
+        const int4 d = m_desc(x.b)[i];
+        const int lo = d.x, deg = d.y;
+        float *sp = stage + (size_t)p * LY::STAGE;
+        const int *vr = m_vidx(x.b) + i * DC;
+        const float *Lt = ds.L + (size_t)x.t * cd.n * LINE;
+        const float *mt = ds.msg + (size_t)x.t * cd.E * LINE;
+#pragma unroll
+        for (int k = 0; k < DC; ++k)
+            if (k < deg) cp_async_g2s<4 * S>(sp + k * LINE + lane * S, Lt + (size_t)vr[k] * LINE + lane * S);
+        cp_async_mbar_arrive(&bar[p]);
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive_tx(&bar[p], (uint32_t)deg * LINE * 4u);
+            if (deg > 0) bulk_g2s(sp + DC * LINE, mt + (size_t)lo * LINE, (uint32_t)deg * LINE * 4, &bar[p]);
+        }
+    };
+    int it_nxt = it_cur + W, it_nn = it_nxt + W;
+    Item cur = make(it_cur, tile_of(it_cur), 0);
+    Item nxt = make(it_nxt, tile_of(it_nxt), 1);
+    int t_nn = tile_of(it_nn);
+    fetch(cur);
+    fetch(nxt);
+    meta_wait(cur);
+    bool nxt_active = false;
+    int iss_sel = 0, iss_i = 0;  // issue cursor: item (0 = cur, 1 = nxt) and check
+    int issued = 0, done = 0;
+    auto try_issue = [&]() -> bool {
+        if (iss_sel == 0 && iss_i >= cur.nc) {
+            iss_sel = 1;
+            iss_i = 0;
+        }
+        if (iss_sel == 1) {
+            if (!nxt.valid || iss_i >= nxt.nc) return false;
+            if (!nxt_active) {
+                meta_wait(nxt);
+                nxt_active = true;
+            }
+            issue(nxt, iss_i, issued % P);
+        } else {
+            issue(cur, iss_i, issued % P);
+        }
+        ++iss_i;
+        ++issued;
+        return true;
+    };
+    while (issued < P && try_issue()) {
+    }
+    int ci = 0;
+    for (;;) {
+        const int p = done % P;
+        mbar_wait(&bar[p], (uint32_t)(done / P) & 1u);
+        {
+            const int4 d = m_desc(cur.b)[ci];
+            const int lo = d.x, deg = d.y;
+            const uint4 act = *m_act(cur.b);
+            const uint32_t sb = lane_act<S>(m_st(cur.b)[ci], lane);
+            const uint32_t al = lane_act<S>(act, lane);
+            float *sp = stage + (size_t)p * LY::STAGE;
+            const int *vrow = m_vidx(cur.b) + ci * DC;
+            if constexpr (DC >= 6) {
+                if (deg <= 2) lt_compute<2, DC, S>(sp, deg, sb, lane, qmax2);
+                else lt_compute<DC, DC, S>(sp, deg, sb, lane, qmax2);
+            } else {
+                lt_compute<DC, DC, S>(sp, deg, sb, lane, qmax2);
+            }
+            __syncwarp();
+            uint32_t *hbt = reinterpret_cast<uint32_t *>(ds.hb + (size_t)cur.t * cd.n);
+            float *Lw = ds.L + (size_t)cur.t * cd.n * LINE + lane * S;
+            float *mw = ds.msg + (size_t)cur.t * cd.E * LINE + lane * S;
+#pragma unroll
+            for (int k = 0; k < DC; ++k) {
+                if (k < deg) {
+                    const FV<S> post = ldv<S>(sp + k * LINE + lane * S);
+                    if (al) {
+                        stv<S>(mw + (size_t)(lo + k) * LINE, ldv<S>(sp + (DC + k) * LINE + lane * S));
+                        stv<S>(Lw + (size_t)vrow[k] * LINE, post);
+                    }
+                    uint32_t w[S];
+#pragma unroll
+                    for (int q = 0; q < S; ++q) w[q] = __ballot_sync(FULL, post.c[q] < 0.0f) & cmpu(act, q);
+                    if (lane == 0) {
+                        uint32_t *h = hbt + (size_t)vrow[k] * 4;
+                        if constexpr (S == 1) h[0] = w[0];
+                        else if constexpr (S == 2) *reinterpret_cast<uint2 *>(h) = make_uint2(w[0], w[1]);
+                        else *reinterpret_cast<uint4 *>(h) = make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                }
+            }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        ++done;
+        ++ci;
+        if (ci == cur.nc) {
+            if (!nxt.valid) break;
+            // the next item becomes current; its successor's metadata goes to the freed buffer
+            const bool was_active = nxt_active;
+            cur = nxt;
+            ci = 0;
+            if (iss_sel == 0) iss_i = 0;
+            iss_sel = 0;
+            if (!was_active) meta_wait(cur);
+            nxt_active = false;
+            it_nxt = it_nn;
+            it_nn += W;
+            nxt = make(it_nxt, t_nn, 1 - cur.b);
+            t_nn = tile_of(it_nn);
+            fetch(nxt);
+        }
+        while (issued < done + P && try_issue()) {
+        }
+    }
+}
+
+template <int DC, int S>
+static void launch_layer_tmap_t(const CodeDev &cd, const DecState &ds, int grid_tiles, int lbeg, int lcnt, float q2,
+                                cudaStream_t s) {
+    static int max_blocks = 0;
+    constexpr size_t smem = LtpLayout<DC, S>::BLOCK_BYTES;
+    if (max_blocks == 0) {
+        cudaFuncSetAttribute(k_layer_tmap<DC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int dev = 0, n_sm = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_layer_tmap<DC, S>, LT_WARPS * 32, smem);
+        max_blocks = (per_sm > 0 ? per_sm : 1) * n_sm;
+    }
+    const long long items = (long long)grid_tiles * ((lcnt + LT_CH - 1) / LT_CH);
+    const long long want = (items + LT_WARPS - 1) / LT_WARPS;
+    const int grid = (int)(want < max_blocks ? want : max_blocks);
+    if (grid > 0) k_layer_tmap<DC, S><<<grid, LT_WARPS * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2);
+}
+
+template <int S>
+static bool launch_layer_tmap_s(const CodeDev &cd, const DecState &ds, int grid_tiles, int lbeg, int lcnt, float q2,
+                                cudaStream_t s) {
+    switch (cd.max_dc) {
+        case 1: case 2: launch_layer_tmap_t<2, S>(cd, ds, grid_tiles, lbeg, lcnt, q2, s); return true;
+        case 3: launch_layer_tmap_t<3, S>(cd, ds, grid_tiles, lbeg, lcnt, q2, s); return true;
+        case 4: launch_layer_tmap_t<4, S>(cd, ds, grid_tiles, lbeg, lcnt, q2, s); return true;
+        case 5: launch_layer_tmap_t<5, S>(cd, ds, grid_tiles, lbeg, lcnt, q2, s); return true;
+        case 6: launch_layer_tmap_t<6, S>(cd, ds, grid_tiles, lbeg, lcnt, q2, s); return true;
+        case 7: launch_layer_tmap_t<7, S>(cd, ds, grid_tiles, lbeg, lcnt, q2, s); return true;
+        case 8: launch_layer_tmap_t<8, S>(cd, ds, grid_tiles, lbeg, lcnt, q2, s); return true;
+        case 9: launch_layer_tmap_t<9, S>(cd, ds, grid_tiles, lbeg, lcnt, q2, s); return true;
+        case 10: launch_layer_tmap_t<10, S>(cd, ds, grid_tiles, lbeg, lcnt, q2, s); return true;
+        case 11: case 12: launch_layer_tmap_t<12, S>(cd, ds, grid_tiles, lbeg, lcnt, q2, s); return true;
+        default: return false;
     }
 }
 
@@ -324,18 +588,18 @@ __global__ void __launch_bounds__(256) k_synd_test(CodeDev cd, DecState ds) {
     __shared__ uint32_t s_unsat[SUBS];
     if (threadIdx.x < SUBS) s_unsat[threadIdx.x] = 0u;
     __syncthreads();
-    const int c = blockIdx.x * 256 + threadIdx.x;
+    const int i = blockIdx.x * 256 + threadIdx.x;  // layer-order position (st rows are in layer order)
     uint32_t u[SUBS] = {0u, 0u, 0u, 0u};
-    if (c < cd.M) {
-        const uint4 sw = ds.st[(size_t)t * cd.M + c];
+    if (i < cd.M) {
+        const uint4 sw = ds.st[(size_t)t * cd.M + i];
         u[0] = sw.x;
         u[1] = sw.y;
         u[2] = sw.z;
         u[3] = sw.w;
         const uint4 *hbt = ds.hb + (size_t)t * cd.n;
-        const int lo = cd.row_ptr[c], hi = cd.row_ptr[c + 1];
+        const int4 d = cd.layer_desc[i];
 #pragma unroll 4
-        for (int e = lo; e < hi; ++e) {
+        for (int e = d.x; e < d.x + d.y; ++e) {
             const uint4 h = hbt[cd.col_idx[e]];
             u[0] ^= h.x;
             if (S > 1) u[1] ^= h.y;
@@ -373,7 +637,7 @@ static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, dim3 grid,
         cudaFuncSetAttribute(k_layer_tma<DC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_layer_tma<DC, S><<<grid, LT_WARPS * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2);
+    k_layer_tma<DC, S><<<grid, lt_warps(S) * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2);
 }
 
 template <int S>
@@ -399,6 +663,17 @@ static bool layer_tma_enabled() {
     static const int v = [] {
         const char *e = getenv("CVSR_LAYER_TMA");
         return (e && *e) ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
+// persistent layer kernel (k_layer_tmap, CVSR_LAYER_PERSIST=1; default off): it removes the
+// index-load stalls but costs 14 % more instructions and the kernel is then issue-bound (full-tile
+// ncu: 4.38 vs 4.57 TB/s; C4 step 93.8 vs 85.8 ms, C2 50.4 vs 46.2 ms)
+static bool layer_persist_enabled() {
+    static const int v = [] {
+        const char *e = getenv("CVSR_LAYER_PERSIST");
+        return (e && *e) ? atoi(e) : 0;
     }();
     return v != 0;
 }
@@ -440,13 +715,19 @@ void launch_layer_init(const CodeDev &cd, const DecState &ds, int grid_tiles, cu
 int launch_layers(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, cudaStream_t s) {
     if (grid_tiles <= 0) return 0;
     const float q2 = qmax * LOG2E;
-    const bool tma = layer_tma_enabled() && ds.subs <= 2;
-    const int per_block = tma ? LT_WARPS * LT_CH : WARPS_PER_BLOCK * LCPW;
+    const bool tma = layer_tma_enabled();
+    const int per_block = tma ? lt_warps(ds.subs) * LT_CH : WARPS_PER_BLOCK * LCPW;
     for (int l = 0; l < cd.n_layers; ++l) {
         const int lbeg = cd.layer_off[l], lcnt = cd.layer_off[l + 1] - lbeg;
         dim3 grid((lcnt + per_block - 1) / per_block, grid_tiles);
+        if (tma && layer_persist_enabled() && ds.subs <= 2) {
+            if (ds.subs == 2) launch_layer_tmap_s<2>(cd, ds, grid_tiles, lbeg, lcnt, q2, s);
+            else launch_layer_tmap_s<1>(cd, ds, grid_tiles, lbeg, lcnt, q2, s);
+            continue;
+        }
         if (tma) {
-            if (ds.subs == 2) launch_layer_tma_s<2>(cd, ds, grid, lbeg, lcnt, q2, s);
+            if (ds.subs == 4) launch_layer_tma_s<4>(cd, ds, grid, lbeg, lcnt, q2, s);
+            else if (ds.subs == 2) launch_layer_tma_s<2>(cd, ds, grid, lbeg, lcnt, q2, s);
             else launch_layer_tma_s<1>(cd, ds, grid, lbeg, lcnt, q2, s);
             continue;
         }

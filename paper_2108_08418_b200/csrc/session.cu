@@ -17,7 +17,8 @@ struct cvsr_session {
     cvsr_quantiser q{};
     float sigma_n = 0.0f;
     cvsr_decode_opts opts{};
-    uint64_t verify_key = 0;           // != 0: frame_ok &= hash check (cvsr_session_set_verify)
+    bool verify = false;               // frame_ok &= hash check under verify_keys (cvsr_session_set_verify)
+    uint64_t verify_keys[CVSR_HASH_KEYS] = {};
     void *mem = nullptr;
     cudaStream_t copy = nullptr;       // H2D / D2H stream of run_host
     cudaEvent_t ev_in[8] = {}, ev_out[8] = {};
@@ -134,15 +135,22 @@ static cvsr_status run_range(cvsr_session *s, const float *x, const float *y, in
                                         &s->opts, label_alice + off, frame_ok + f0, iters + (size_t)f0 * s->m,
                                         stats_out))
         return st;
-    if (!s->verify_key) return CVSR_OK;
-    return cvsr_verify(s->ctx, label_alice + off, s->label_bob + off, frame_ok + f0, nf, s->n, s->verify_key,
+    if (!s->verify) return CVSR_OK;
+    return cvsr_verify(s->ctx, label_alice + off, s->label_bob + off, frame_ok + f0, nf, s->n, s->verify_keys,
                        frame_ok + f0, nullptr, nullptr);
 }
 
-cvsr_status cvsr_session_set_verify(cvsr_session *s, uint64_t key) {
+cvsr_status cvsr_session_set_verify(cvsr_session *s, const uint64_t *keys) {
     if (!s) return cvsr_internal_fail(CVSR_EINVAL, "null session");
-    if (key >= ((1ull << 61) - 1ull)) return cvsr_internal_fail(CVSR_EINVAL, "key must be 0 or in [1, 2^61 - 2]");
-    s->verify_key = key;
+    if (!keys) {
+        s->verify = false;
+        return CVSR_OK;
+    }
+    for (int q = 0; q < CVSR_HASH_KEYS; ++q)
+        if (keys[q] == 0 || keys[q] >= ((1ull << 61) - 1ull))
+            return cvsr_internal_fail(CVSR_EINVAL, "keys must be in [1, 2^61 - 2]");
+    for (int q = 0; q < CVSR_HASH_KEYS; ++q) s->verify_keys[q] = keys[q];
+    s->verify = true;
     return CVSR_OK;
 }
 

@@ -82,13 +82,13 @@ _SIGS = {
                         _P(cvsr_decode_opts), _vp, _vp, _vp, _P(cvsr_stats)], _i32),
     "cvsr_count_errors": ([_vp, _vp, _vp, _vp, _i32, _i32, _P(_i64)], _i32),
     "cvsr_frame_hash": ([_vp, _vp, _i32, _i32, ctypes.c_uint64, _vp], _i32),
-    "cvsr_session_set_verify": ([_vp, ctypes.c_uint64], _i32),
+    "cvsr_session_set_verify": ([_vp, _vp], _i32),
     "cvsr_session_run_host_stream": ([_vp, _i32, _vp, _vp, _vp, _vp], _i32),
     "cvsr_pa_plan_create": ([_vp, _i64, _i64, _vp, _P(_vp)], _i32),
     "cvsr_pa_plan_info": ([_vp, _P(_i64), _P(_i64), _P(_i64)], _i32),
     "cvsr_pa_hash": ([_vp, _vp, _i32, _vp, _vp], _i32),
     "cvsr_pa_plan_free": ([_vp], None),
-    "cvsr_verify": ([_vp, _vp, _vp, _vp, _i32, _i32, ctypes.c_uint64, _vp, _vp, _vp], _i32),
+    "cvsr_verify": ([_vp, _vp, _vp, _vp, _i32, _i32, _P(ctypes.c_uint64), _vp, _vp, _vp], _i32),
     "cvsr_session_create": ([_vp, _i32, _P(_vp), _P(_i32), _P(cvsr_quantiser), _f32, _i32, _i32,
                              _P(cvsr_decode_opts), _P(_vp)], _i32),
     "cvsr_session_run": ([_vp, _vp, _vp, _P(cvsr_stats)], _i32),
@@ -308,13 +308,25 @@ def cvsr_pa_plan_free(plan: int) -> None:
     _lib.cvsr_pa_plan_free(plan)
 
 
-def cvsr_session_set_verify(sess: int, key: int) -> None:
-    _call("cvsr_session_set_verify", sess, key)
+CVSR_HASH_KEYS = 3
 
 
-def cvsr_verify(ctx: int, label_alice, label_bob, frame_ok, frames: int, n: int, key: int, verified_out,
+def _keys(keys):
+    keys = list(keys)
+    if len(keys) != CVSR_HASH_KEYS:
+        raise ValueError(f"{CVSR_HASH_KEYS} keys expected")
+    return (ctypes.c_uint64 * CVSR_HASH_KEYS)(*keys)
+
+
+def cvsr_session_set_verify(sess: int, keys) -> None:
+    """keys: CVSR_HASH_KEYS ints in [1, 2^61 - 2], or None (off)."""
+    _call("cvsr_session_set_verify", sess, ctypes.cast(_keys(keys), _vp) if keys is not None else None)
+
+
+def cvsr_verify(ctx: int, label_alice, label_bob, frame_ok, frames: int, n: int, keys, verified_out,
                 hash_alice_out=None, hash_bob_out=None) -> None:
-    _call("cvsr_verify", ctx, _ptr(label_alice), _ptr(label_bob), _ptr(frame_ok), frames, n, key,
+    """keys: CVSR_HASH_KEYS ints; hash outputs uint64[frames][CVSR_HASH_KEYS] (optional)."""
+    _call("cvsr_verify", ctx, _ptr(label_alice), _ptr(label_bob), _ptr(frame_ok), frames, n, _keys(keys),
           _ptr(verified_out), _ptr(hash_alice_out) if hash_alice_out is not None else None,
           _ptr(hash_bob_out) if hash_bob_out is not None else None)
 

@@ -49,8 +49,8 @@ class SRPipeline:
         self.label_alice = torch.empty((frames, n), dtype=torch.uint8, **kw)
         self.frame_ok = torch.empty((frames,), dtype=torch.uint8, **kw)
         self.verified = torch.empty((frames,), dtype=torch.uint8, **kw)
-        self.hash_alice = torch.empty((frames,), dtype=torch.int64, **kw)
-        self.hash_bob = torch.empty((frames,), dtype=torch.int64, **kw)
+        self.hash_alice = torch.empty((frames, cvsr.CVSR_HASH_KEYS), dtype=torch.int64, **kw)
+        self.hash_bob = torch.empty((frames, cvsr.CVSR_HASH_KEYS), dtype=torch.int64, **kw)
         self.iters = torch.empty((frames, m), dtype=torch.int32, **kw)
         self.codes = list(codes)
 
@@ -67,14 +67,16 @@ class SRPipeline:
                                    self.frames, self.n, self.opts, self.label_alice, self.frame_ok, self.iters,
                                    want_stats=want_stats)
 
-    def verify(self, key: int) -> None:
-        """PAPER.md:90 hash check: verified = frame_ok AND hash(Alice) == hash(Bob) (keyed per call)."""
-        cvsr.cvsr_verify(self.ctx, self.label_alice, self.label_bob, self.frame_ok, self.frames, self.n, key,
+    def verify(self, keys) -> None:
+        """PAPER.md:90 hash check: verified = frame_ok AND hash(Alice) == hash(Bob) under each of the
+        cvsr.CVSR_HASH_KEYS independent keys (fresh per call)."""
+        cvsr.cvsr_verify(self.ctx, self.label_alice, self.label_bob, self.frame_ok, self.frames, self.n, keys,
                          self.verified, self.hash_alice, self.hash_bob)
 
     def step(self, x: torch.Tensor, y: torch.Tensor, want_stats: bool = False,
-             key: Optional[int] = None) -> Optional[dict]:
-        """Bob, Alice and (key given) the hash verification of one batch."""
+             key=None) -> Optional[dict]:
+        """Bob, Alice and (keys given: a sequence of cvsr.CVSR_HASH_KEYS ints) the hash verification
+        of one batch."""
         self.bob(y)
         st = self.alice(x, want_stats)
         if key is not None:

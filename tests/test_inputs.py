@@ -88,3 +88,25 @@ def test_peg_construction_girth_and_degrees():
     dc = np.diff(np.asarray(peg.row_ptr))
     assert set(dc.tolist()) <= {4, 5} and peg.n_edges == cfg.n_edges
     assert four_cycles(peg) == 0 and four_cycles(cfg) > 0
+
+
+def test_codebook_recipes_reproduce_c4_codes():
+    """The code database stores recipes + SHA digests (PAPER.md:392 database; tools/backoff.py):
+    the C4 config's coded slices are exactly the codes the back-off marked good, rebuilt bit for
+    bit from their recipes, and every stored trial respects the Delta R = 0.05 ladder from the
+    rate closest to capacity."""
+    from cvsr_inputs import codebook, configs
+    entries = codebook.load()
+    assert entries, "cvsr_inputs/codebook.json missing"
+    cl = configs.C4.build_codes()
+    for j, c in enumerate(cl):
+        if c is None:
+            continue
+        e = codebook.good("C4", j, configs.C4.n)
+        assert e is not None and e["digest"] == c.digest()
+        assert e["test"]["failed"] == 0 and e["test"]["undetected"] == 0
+        ladder = sorted({x["params"]["rate"] for x in entries if x["config"] == "C4" and x["slice"] == j},
+                        reverse=True)
+        assert abs(ladder[0] - int(1000 * e["cap"]) / 1000) < 1e-9
+        assert all(abs((a - b) - 0.05) < 1e-9 for a, b in zip(ladder, ladder[1:]))
+        assert e["params"]["rate"] == ladder[-1]
