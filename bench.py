@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--splits", type=int, default=1, help="concurrent frame ranges per GPU (streams)")
     ap.add_argument("--schedule", default="layered", choices=["layered", "flooding"],
                     help="BP schedule of the CUDA path (DESIGN.md R-9 layered, A-8 flooding)")
+    ap.add_argument("--no-other-schedule", action="store_true",
+                    help="skip the secondary line of the other BP schedule (same workload, K steps)")
     return ap.parse_args()
 
 
@@ -165,9 +167,10 @@ def oracle_sample(cfg, codes_l, frames: int, first_frame: int = 0, schedule: str
 
 def run_reference(args):
     """The reference arm: the fp64 oracle on the box's host cores, same config, metric and BP
-    schedule.  One frame takes a single core tens of seconds at N_R = 1e6, so the K timed steps are
-    K frames reconciled concurrently (OpenMP over frames) and ms_per_step = wall time / K; the W
-    warm-up steps are W frames, untimed."""
+    schedule.  One frame takes a single core tens of seconds at N_R = 1e6, so the K timed steps
+    share one sample of whole waves of frames (one per core, at least K frames) reconciled
+    concurrently (OpenMP over frames) and ms_per_step = wall time / K; the W warm-up steps are W
+    frames, untimed."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -176,7 +179,8 @@ def run_reference(args):
     cores = oracle.num_threads()
     if args.warmup:
         oracle_sample(cfg, codes_l, min(args.warmup, cores), first_frame=10_000, schedule=args.schedule)
-    frames = max(1, args.steps)
+    # whole waves of one frame per core, at least one frame per step
+    frames = cores * ((max(1, args.steps) + cores - 1) // cores)
     bits, t_total, okf = oracle_sample(cfg, codes_l, frames, schedule=args.schedule)
     v = bits / t_total
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
@@ -185,9 +189,9 @@ def run_reference(args):
             "config": {"workload": f"{cfg.name}: m={cfg.m} slices, N_R={cfg.n}, gamma={cfg.gamma}",
                        "frames_timed": frames, "sample": True, "bp_schedule": args.schedule},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"{frames} frames x N_R={cfg.n} of {cfg.name} (one per step, reconciled "
-                                       f"concurrently on {cores} cores; {args.schedule} BP), {t_total:.1f} s wall, "
-                                       f"{okf} ok"},
+                             "sample": f"{frames} frames x N_R={cfg.n} of {cfg.name} (whole waves of one frame per "
+                                       f"core for the {args.steps} steps, reconciled concurrently on {cores} cores; "
+                                       f"{args.schedule} BP), {t_total:.1f} s wall, {okf} ok"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -259,7 +263,7 @@ def main():
     # per-step hash keys (a fresh public key for every verification)
     key_rng = np.random.default_rng(1000 + rank)
     keys = [[int(k) for k in key_rng.integers(1, (1 << 61) - 2, size=cvsr.CVSR_HASH_KEYS)]
-            for _ in range(args.warmup + 4 * args.steps + 1)]
+            for _ in range(args.warmup + 4 * args.steps + 8)]
     # untimed reference run for statistics (the batch is identical every step)
     st = pipe.step(x, y, want_stats=True, key=keys.pop())
     undetected = pipe.count_errors()[1]
@@ -382,10 +386,32 @@ def main():
         cvsr.cvsr_session_destroy(sess)
         cvsr.cvsr_ctx_destroy(ectx)
 
+    # secondary measurement: the same workload with the other BP schedule (SURVEY reading A-8 is
+    # flooding; the headline runs the layered reading R-9), device-resident, K timed steps
+    other = None
+    if not args.no_other_schedule and args.splits == 1:
+        osch = "flooding" if args.schedule == "layered" else "layered"
+        op = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, device, cfg.max_iter, cfg.q_max,
+                        stream, schedule=osch)
+        ost = op.step(x, y, want_stats=True, key=keys.pop())
+        overified = int(op.verified.sum().item())
+        op.step(x, y, key=keys.pop())
+        barrier()
+        o0, o1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        o0.record(stream)
+        for _ in range(args.steps):
+            op.step(x, y, key=keys[-1])
+        o1.record(stream)
+        barrier()
+        other = {"schedule": osch, "ms": o0.elapsed_time(o1), "bits": overified * cfg.m * n,
+                 "mean_iters": [float(ost["iters_sum"][j] / max(F, 1)) for j in range(cfg.m)],
+                 "frames_ok": ost["frames_ok"]}
+        op.close()
+
     # ---- reduce over ranks (the only collective: statistics + max time)
     red, iters_sum, edge_iters, tmax = cdist.reduce_stats(
         {"bits": bits_per_step, "frames": st["frames"], "frames_ok": st["frames_ok"], "undetected": undetected},
-        st["iters_sum"], st["edge_iters"], [t_ms, e2e["ms"] if e2e else 0.0], device)
+        st["iters_sum"], st["edge_iters"], [t_ms, e2e["ms"] if e2e else 0.0, other["ms"] if other else 0.0], device)
     if rank != 0:
         if distributed:
             dist.destroy_process_group()
@@ -520,6 +546,13 @@ def main():
                  "api": "cvsr_session_run_host_stream (C ABI, pinned host buffers, K batches double-buffered)"} if e2e else None),
         **extra,
     }
+    if other:
+        # rank 0's schedule comparison (the bits of rank 0 over the max-over-ranks time)
+        line["other_schedule"] = {"schedule": other["schedule"],
+                                  "value_rank0_x_ranks": other["bits"] * world / (tmax[2] / args.steps * 1e-3),
+                                  "ms_per_step": tmax[2] / args.steps, "mean_iters_rank0": other["mean_iters"],
+                                  "frames_ok_rank0": other["frames_ok"],
+                                  "note": "same workload, device-resident, K steps, no profiling pass"}
     print(json.dumps(line), flush=True)
     pipe.close()
     if distributed:

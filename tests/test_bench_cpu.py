@@ -27,7 +27,7 @@ def test_reference_arm_json_line():
     assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle"
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["higher_is_better"] is True
     assert line["metric"].startswith("reconciled bits/sec")
-    assert line["config"]["bp_schedule"] == "layered" and line["config"]["frames_timed"] == 2
+    assert line["config"]["bp_schedule"] == "layered" and line["config"]["frames_timed"] >= 2
 
 
 def test_launch_plan():
