@@ -349,7 +349,7 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
     prof_begin(ctx, KC_INIT);
     int launched = 0;
     if (layered) {  // r = 0, post = L (ds.L), decision 0 = [L < 0]
-        CK(cudaMemsetAsync(ds.msg, 0, (size_t)ds.tiles * cd.E * T * sizeof(float), s));
+        if (!layers_zero_first()) CK(cudaMemsetAsync(ds.msg, 0, (size_t)ds.tiles * cd.E * T * sizeof(float), s));
         launch_layer_init(cd, ds, ds.tiles, s);
         launched = 1;
     } else {
@@ -414,7 +414,7 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
             }
             if (!check_and_compact(k, true)) break;
             prof_begin(ctx, KC_VN);
-            launched += launch_layers(cd, ds, bound, qmax, s);
+            launched += launch_layers(cd, ds, bound, qmax, k == 1, s);
             prof_end(ctx);
             CK(cudaEventRecord(ctx->ring[k % RING], s));
         }
@@ -1036,10 +1036,10 @@ cvsr_status cvsr_decode_trace(cvsr_ctx *ctx, const cvsr_code *code, const float 
     int launched = 4;
     if (layered) {
         // r = 0, post = L; k sweeps over the layers; r_e is in ds.msg (CSR slots), post_v in ds.L
-        CK(cudaMemsetAsync(ds.msg, 0, (size_t)tiles * cd.E * LANES * subs * sizeof(float), s));
+        if (!layers_zero_first()) CK(cudaMemsetAsync(ds.msg, 0, (size_t)tiles * cd.E * LANES * subs * sizeof(float), s));
         launch_layer_init(cd, ds, tiles, s);
         ++launched;
-        for (int k = 1; k <= k_iters; ++k) launched += launch_layers(cd, ds, tiles, msg_clamp, s);
+        for (int k = 1; k <= k_iters; ++k) launched += launch_layers(cd, ds, tiles, msg_clamp, k == 1, s);
         if (c2v_out) {
             launch_from_interleaved(ds.msg, c2v_out, frames, cd.E, tiles, ds.subs, LN2, s);
             ++launched;

@@ -24,7 +24,8 @@ void launch_init_tiles(const DecState &ds, const uint8_t *alive, cudaStream_t s)
 void launch_set_counts(const DecState &ds, int32_t n_active, cudaStream_t s);
 bool layered_supported(const CodeDev &cd);
 void launch_layer_init(const CodeDev &cd, const DecState &ds, int grid_tiles, cudaStream_t s);
-int launch_layers(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, cudaStream_t s);
+int launch_layers(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, cudaStream_t s);
+bool layers_zero_first();
 int layer_subs(int32_t max_dc);
 void launch_synd_test(const CodeDev &cd, const DecState &ds, int grid_tiles, cudaStream_t s);
 size_t decode_smem_bytes(const CodeDev &cd);

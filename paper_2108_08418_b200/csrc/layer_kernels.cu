@@ -198,17 +198,40 @@ struct LtLayout {
 
 // the check update of one check from its stage: DCT = compute width (>= deg; DCL = the stage
 // layout's DC).  Results overwrite the stage: posterior lines <- post_v, message lines <- r_e.
+#ifndef CVSR_LT_VLOAD
+#define CVSR_LT_VLOAD 0
+#endif
 template <int DCT, int DCL, int S>
-__device__ __forceinline__ void lt_compute(float *__restrict__ sp, int deg, uint32_t sb, int lane, float qmax2) {
+__device__ __forceinline__ void lt_compute(float *__restrict__ sp, int deg, uint32_t sb, int lane, float qmax2,
+                                           bool first = false) {
     constexpr int LINE = LANES * S;
     float *pp = sp + lane * S;               // posterior lines
     float *rp = sp + DCL * LINE + lane * S;  // message lines
+#if CVSR_LT_VLOAD
+    // all S frames of each line with one vector shared-memory load (no 2-way bank conflicts)
+    float qv[S][DCT];
+#pragma unroll
+    for (int k = 0; k < DCT; ++k) {
+        if (k < deg) {
+            const FV<S> p = ldv<S>(pp + k * LINE), r = first ? splat<S>(0.0f) : ldv<S>(rp + k * LINE);
+#pragma unroll
+            for (int s = 0; s < S; ++s) qv[s][k] = p.c[s] - r.c[s];
+        } else {
+#pragma unroll
+            for (int s = 0; s < S; ++s) qv[s][k] = DUMMY_Q;
+        }
+    }
+#endif
 #pragma unroll(S == 4 ? 1 : S)
     for (int s = 0; s < S; ++s) {
         float qu[DCT], a[DCT];
 #pragma unroll
         for (int k = 0; k < DCT; ++k) {
-            qu[k] = (k < deg) ? pp[k * LINE + s] - rp[k * LINE + s] : DUMMY_Q;
+#if CVSR_LT_VLOAD
+            qu[k] = qv[s][k];
+#else
+            qu[k] = (k < deg) ? pp[k * LINE + s] - (first ? 0.0f : rp[k * LINE + s]) : DUMMY_Q;
+#endif
             a[k] = (k < deg) ? clampf(qu[k], qmax2) : DUMMY_Q;
         }
         cn_update<DCT>(a, (sb >> s) & 1u, qmax2);
@@ -224,7 +247,7 @@ __device__ __forceinline__ void lt_compute(float *__restrict__ sp, int deg, uint
 
 template <int DC, int S>
 __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
-    k_layer_tma(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2) {
+    k_layer_tma(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2, int first) {
     using LY = LtLayout<DC, S>;
     constexpr int LINE = LY::LINE;
     constexpr int P = LY::P;
@@ -270,8 +293,9 @@ __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
         cp_async_mbar_arrive(&bar[p]);
         __syncwarp();  // every lane's pending-count increment precedes lane 0's arrival
         if (lane == 0) {
-            mbar_arrive_tx(&bar[p], (uint32_t)deg * LINE * 4u);
-            if (deg > 0) bulk_g2s(sp + DC * LINE, mt + (size_t)lo * LINE, (uint32_t)deg * LINE * 4, &bar[p]);
+            // first iteration: r = 0 (reading R-9 init), no message lines to load
+            mbar_arrive_tx(&bar[p], first ? 0u : (uint32_t)deg * LINE * 4u);
+            if (deg > 0 && !first) bulk_g2s(sp + DC * LINE, mt + (size_t)lo * LINE, (uint32_t)deg * LINE * 4, &bar[p]);
         }
     };
     const int npre = min(P, nc);
@@ -296,10 +320,10 @@ __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
         const int *vrow = vidx + i * DC;
         if constexpr (DC >= 6) {
             // degree-2 checks of a code with a large maximum degree (MET type-A checks)
-            if (deg <= 2) lt_compute<2, DC, S>(sp, deg, sb, lane, qmax2);
-            else lt_compute<DC, DC, S>(sp, deg, sb, lane, qmax2);
+            if (deg <= 2) lt_compute<2, DC, S>(sp, deg, sb, lane, qmax2, first != 0);
+            else lt_compute<DC, DC, S>(sp, deg, sb, lane, qmax2, first != 0);
         } else {
-            lt_compute<DC, DC, S>(sp, deg, sb, lane, qmax2);
+            lt_compute<DC, DC, S>(sp, deg, sb, lane, qmax2, first != 0);
         }
         __syncwarp();
         // lane-vectorised stores of r_e and post_v, and the hard decisions [post_v < 0] of the
@@ -630,30 +654,30 @@ void launch_synd_test(const CodeDev &cd, const DecState &ds, int grid_tiles, cud
 
 template <int DC, int S>
 static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,
-                               cudaStream_t s) {
+                               int first, cudaStream_t s) {
     static bool attr = false;
     constexpr size_t smem = LtLayout<DC, S>::BLOCK_BYTES;
     if (!attr) {
         cudaFuncSetAttribute(k_layer_tma<DC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_layer_tma<DC, S><<<grid, lt_warps(S) * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2);
+    k_layer_tma<DC, S><<<grid, lt_warps(S) * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2, first);
 }
 
 template <int S>
 static bool launch_layer_tma_s(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,
-                               cudaStream_t s) {
+                               int first, cudaStream_t s) {
     switch (cd.max_dc) {
-        case 1: case 2: launch_layer_tma_t<2, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
-        case 3: launch_layer_tma_t<3, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
-        case 4: launch_layer_tma_t<4, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
-        case 5: launch_layer_tma_t<5, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
-        case 6: launch_layer_tma_t<6, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
-        case 7: launch_layer_tma_t<7, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
-        case 8: launch_layer_tma_t<8, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
-        case 9: launch_layer_tma_t<9, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
-        case 10: launch_layer_tma_t<10, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
-        case 11: case 12: launch_layer_tma_t<12, S>(cd, ds, grid, lbeg, lcnt, q2, s); return true;
+        case 1: case 2: launch_layer_tma_t<2, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
+        case 3: launch_layer_tma_t<3, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
+        case 4: launch_layer_tma_t<4, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
+        case 5: launch_layer_tma_t<5, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
+        case 6: launch_layer_tma_t<6, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
+        case 7: launch_layer_tma_t<7, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
+        case 8: launch_layer_tma_t<8, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
+        case 9: launch_layer_tma_t<9, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
+        case 10: launch_layer_tma_t<10, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
+        case 11: case 12: launch_layer_tma_t<12, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
         default: return false;
     }
 }
@@ -712,7 +736,11 @@ void launch_layer_init(const CodeDev &cd, const DecState &ds, int grid_tiles, cu
 }
 
 // all layers of one iteration (returns the number of launches)
-int launch_layers(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, cudaStream_t s) {
+// whether launch_layers(first = true) itself treats r as 0 (k_layer_tma); otherwise the caller
+// zeroes the message arena before the first iteration
+bool layers_zero_first() { return layer_tma_enabled() && !layer_persist_enabled(); }
+
+int launch_layers(const CodeDev &cd, const DecState &ds, int grid_tiles, float qmax, bool first, cudaStream_t s) {
     if (grid_tiles <= 0) return 0;
     const float q2 = qmax * LOG2E;
     const bool tma = layer_tma_enabled();
@@ -726,9 +754,10 @@ int launch_layers(const CodeDev &cd, const DecState &ds, int grid_tiles, float q
             continue;
         }
         if (tma) {
-            if (ds.subs == 4) launch_layer_tma_s<4>(cd, ds, grid, lbeg, lcnt, q2, s);
-            else if (ds.subs == 2) launch_layer_tma_s<2>(cd, ds, grid, lbeg, lcnt, q2, s);
-            else launch_layer_tma_s<1>(cd, ds, grid, lbeg, lcnt, q2, s);
+            const int f = first ? 1 : 0;
+            if (ds.subs == 4) launch_layer_tma_s<4>(cd, ds, grid, lbeg, lcnt, q2, f, s);
+            else if (ds.subs == 2) launch_layer_tma_s<2>(cd, ds, grid, lbeg, lcnt, q2, f, s);
+            else launch_layer_tma_s<1>(cd, ds, grid, lbeg, lcnt, q2, f, s);
             continue;
         }
         if (ds.subs == 4) launch_layer_s<4>(cd, ds, grid, lbeg, lcnt, q2, s);

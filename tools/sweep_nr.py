@@ -27,13 +27,15 @@ def main():
     ap.add_argument("--symbols", type=int, default=configs.C5_SYMBOLS_PER_GPU)
     ap.add_argument("--nr", default=",".join(str(x) for x in configs.C5_NR))
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--schedule", default="layered", choices=["layered", "flooding"])
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     for n_r in [int(v) for v in args.nr.split(",")]:
         cfg = configs.c5(n_r)
         frames = max(1, args.symbols // n_r)
         codes_l = cfg.build_codes()
-        pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n_r, frames, dev, cfg.max_iter)
+        pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n_r, frames, dev, cfg.max_iter,
+                          schedule=args.schedule)
         x, y = torch_quadratures(frames, n_r, cfg.gamma, dev)
         st = pipe.step(x, y, want_stats=True)
         und = pipe.count_errors()[1]
@@ -48,7 +50,7 @@ def main():
         rates = [c.rate if c is not None else 0.0 for c in codes_l]
         pi_my, _ = analysis.entropies(cfg.gamma, cfg.m, cfg.delta)
         ok = st["frames_ok"] - und
-        print(json.dumps({"n_r": n_r, "frames": frames, "ms_per_step": ms,
+        print(json.dumps({"n_r": n_r, "frames": frames, "ms_per_step": ms, "schedule": args.schedule,
                           "reconciled_bits_per_s": ok * cfg.m * n_r / (ms * 1e-3),
                           "fer": 1 - st["frames_ok"] / frames, "undetected": und,
                           "mean_iters": [s / max(a, 1) for s, a in zip(st["iters_sum"], st["attempted"])],
