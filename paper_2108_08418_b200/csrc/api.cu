@@ -327,7 +327,7 @@ DecState carve_decstate(Carve &cv, int tiles, int frames, int subs, int64_t n, i
 // are launched LOOKAHEAD ahead of a mapped-memory progress counter written by
 // the status kernel; the counter also bounds the grid's tile dimension.
 cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0, int max_iter, float qmax,
-                       uint32_t *bits_out, const CompactArena *ca, bool layered) {
+                       uint32_t *bits_out, const CompactArena *ca, bool layered, bool hb_ready = false) {
     cudaStream_t s = ctx->stream;
     const CodeDev &cd = code->d;
     volatile int32_t *hc = ctx->host_counts;
@@ -350,8 +350,10 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
     int launched = 0;
     if (layered) {  // r = 0, post = L (ds.L), decision 0 = [L < 0]
         if (!layers_zero_first()) CK(cudaMemsetAsync(ds.msg, 0, (size_t)ds.tiles * cd.E * T * sizeof(float), s));
-        launch_layer_init(cd, ds, ds.tiles, s);
-        launched = 1;
+        if (!hb_ready) {  // (the reconcile LLR kernel writes the initial decisions itself)
+            launch_layer_init(cd, ds, ds.tiles, s);
+            launched = 1;
+        }
     } else {
         launched = launch_vn(cd, ds, ds.tiles, qmax, true, nullptr, s);  // decision 0 -> hbuf[0]
     }
@@ -723,6 +725,14 @@ cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, cons
         layer_chk.resize((size_t)n_checks);
         std::vector<int32_t> at(layer_off.begin(), layer_off.end() - 1);
         for (int32_t c = 0; c < n_checks; ++c) layer_chk[at[colour[c]]++] = c;
+        // within a layer, checks by degree (descending, then index): the checks of a layer share no
+        // variable, so their order is free; grouping equal degrees keeps a warp's consecutive checks
+        // on one exact-degree body of k_layer_tma
+        for (int l = 0; l < n_layers; ++l)
+            std::stable_sort(layer_chk.begin() + layer_off[l], layer_chk.begin() + layer_off[l + 1],
+                             [&](int32_t a, int32_t b) {
+                                 return row_ptr[a + 1] - row_ptr[a] > row_ptr[b + 1] - row_ptr[b];
+                             });
     }
 
     // layer-ordered check descriptors + padded column table (layered kernels; CodeDev comment)
@@ -1164,12 +1174,13 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
             for (int jj = 0; jj < m; ++jj) p.known_bits[jj] = known_bits[jj];
             prof_begin(ctx, KC_INIT);
             if (cvsr_status st = prepare_llr_table(ctx, p, &launched)) return st;
-            launch_llr_interleaved(p, x, frames, n, tiles_j[j], ds.subs, ds.L, s);
+            launch_llr_interleaved(p, x, frames, n, tiles_j[j], ds.subs, ds.L, lay_j[j] ? ds.hb : nullptr,
+                                   ds.tile_active, s);
             prof_end(ctx);
             launched += 4;
             if (cvsr_status st = check_launch(ctx, 0)) return st;
             if (cvsr_status st = run_decode(ctx, codes[j], ds, opts->max_iter, opts->msg_clamp, bits_dec[j],
-                                            comp_j[j] ? &ca : nullptr, lay_j[j]))
+                                            comp_j[j] ? &ca : nullptr, lay_j[j], lay_j[j]))
                 return st;
             launch_slice_done(ds, m, j, 0, alive, attempt, iters, s);
             ++launched;

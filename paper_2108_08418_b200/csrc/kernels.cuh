@@ -53,6 +53,7 @@ void launch_llr_slice(const LlrParams &p, const float *x, const uint8_t *known_l
                       float *out, cudaStream_t s);
 void launch_llr_biawgn(const float *y, int64_t count, float sigma2, float llr_max, float *out, cudaStream_t s);
 void launch_llr_interleaved(const LlrParams &p, const float *x, int32_t F, int32_t n, int tiles, int subs, float *L,
+                            uint4 *hb /*nullable: also write [L < 0] of active frames*/, const uint4 *tile_active,
                             cudaStream_t s);
 
 // reconcile bookkeeping (bob_kernels.cu)

@@ -245,9 +245,58 @@ __device__ __forceinline__ void lt_compute(float *__restrict__ sp, int deg, uint
     }
 }
 
+// lane-vectorised stores of r_e and post_v of one check from its stage, and the hard decisions
+// [post_v < 0] of the tile's active frames (one word per sub-tile, stored together).  DCT = the
+// compile-time bound of the loop (the check's exact degree when EXACT, else >= deg).
+template <int DCT, int DCL, int S, bool EXACT>
+__device__ __forceinline__ void lt_store(const float *__restrict__ sp, int deg, int lo, const int *__restrict__ vrow,
+                                         uint32_t al, const uint4 &act, int lane, float *__restrict__ mw,
+                                         float *__restrict__ Lw, uint32_t *__restrict__ hbt) {
+    constexpr int LINE = LANES * S;
+#pragma unroll
+    for (int k = 0; k < DCT; ++k) {
+        if (EXACT || k < deg) {
+            const FV<S> post = ldv<S>(sp + k * LINE + lane * S);
+            if (al) {
+                stv<S>(mw + (size_t)(lo + k) * LINE, ldv<S>(sp + (DCL + k) * LINE + lane * S));
+                stv<S>(Lw + (size_t)vrow[k] * LINE, post);
+            }
+            uint32_t w[S];
+#pragma unroll
+            for (int q = 0; q < S; ++q) w[q] = __ballot_sync(FULL, post.c[q] < 0.0f) & cmpu(act, q);
+            if (lane == 0) {
+                uint32_t *h = hbt + (size_t)vrow[k] * 4;
+                if constexpr (S == 1) h[0] = w[0];
+                else if constexpr (S == 2) *reinterpret_cast<uint2 *>(h) = make_uint2(w[0], w[1]);
+                else *reinterpret_cast<uint4 *>(h) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+    }
+}
+
+// one check: compute (lt_compute; deg passed as DCT when exact, so no edge is a padded dummy and
+// no degree predicate remains) and store
+template <int DCT, int DCL, int S, bool EXACT>
+__device__ __forceinline__ void lt_check(float *__restrict__ sp, int deg, uint32_t sb, int lane, float qmax2,
+                                         bool first, int lo, const int *__restrict__ vrow, uint32_t al,
+                                         const uint4 &act, float *__restrict__ mw, float *__restrict__ Lw,
+                                         uint32_t *__restrict__ hbt) {
+    lt_compute<DCT, DCL, S>(sp, EXACT ? DCT : deg, sb, lane, qmax2, first);
+    __syncwarp();
+    lt_store<DCT, DCL, S, EXACT>(sp, EXACT ? DCT : deg, lo, vrow, al, act, lane, mw, Lw, hbt);
+}
+
+#ifndef CVSR_LT_EXACT
+#define CVSR_LT_EXACT 1
+#endif
+// exact-degree bodies are used up to this maximum check degree: measured faster on C2 (degrees 4/5:
+// 43.8 vs 46.6 ms per step) and slower on C4 (6/7, 8/9: 86.0 vs 84.3 ms; more i-cache misses)
+#ifndef CVSR_LT_EXACT_MAXDC
+#define CVSR_LT_EXACT_MAXDC 5
+#endif
 template <int DC, int S>
 __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
-    k_layer_tma(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2, int first) {
+    k_layer_tma(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2, int first, int exact) {
     using LY = LtLayout<DC, S>;
     constexpr int LINE = LY::LINE;
     constexpr int P = LY::P;
@@ -318,34 +367,18 @@ __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
         const uint32_t sb = lane_act<S>(sw, lane);
         float *sp = stage + (size_t)p * LY::STAGE;
         const int *vrow = vidx + i * DC;
-        if constexpr (DC >= 6) {
-            // degree-2 checks of a code with a large maximum degree (MET type-A checks)
-            if (deg <= 2) lt_compute<2, DC, S>(sp, deg, sb, lane, qmax2, first != 0);
-            else lt_compute<DC, DC, S>(sp, deg, sb, lane, qmax2, first != 0);
+        const bool f1 = first != 0;
+        // exact-degree bodies for the two largest degrees (the irregular codes' checks take two
+        // consecutive degrees; no padded dummy edges, no degree predicates), the 2-edge body for
+        // MET type-A checks, and the padded body otherwise
+        if (CVSR_LT_EXACT && exact && deg == DC) {
+            lt_check<DC, DC, S, true>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
+        } else if (CVSR_LT_EXACT && exact && DC > 3 && deg == DC - 1) {
+            lt_check<(DC > 3 ? DC - 1 : DC), DC, S, true>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
+        } else if (DC >= 6 && deg <= 2) {
+            lt_check<2, DC, S, false>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
         } else {
-            lt_compute<DC, DC, S>(sp, deg, sb, lane, qmax2, first != 0);
-        }
-        __syncwarp();
-        // lane-vectorised stores of r_e and post_v, and the hard decisions [post_v < 0] of the
-        // tile's active frames (one word per sub-tile, stored together)
-#pragma unroll
-        for (int k = 0; k < DC; ++k) {
-            if (k < deg) {
-                const FV<S> post = ldv<S>(sp + k * LINE + lane * S);
-                if (al) {
-                    stv<S>(mw + (size_t)(lo + k) * LINE, ldv<S>(sp + (DC + k) * LINE + lane * S));
-                    stv<S>(Lw + (size_t)vrow[k] * LINE, post);
-                }
-                uint32_t w[S];
-#pragma unroll
-                for (int q = 0; q < S; ++q) w[q] = __ballot_sync(FULL, post.c[q] < 0.0f) & cmpu(act, q);
-                if (lane == 0) {
-                    uint32_t *h = hbt + (size_t)vrow[k] * 4;
-                    if constexpr (S == 1) h[0] = w[0];
-                    else if constexpr (S == 2) *reinterpret_cast<uint2 *>(h) = make_uint2(w[0], w[1]);
-                    else *reinterpret_cast<uint4 *>(h) = make_uint4(w[0], w[1], w[2], w[3]);
-                }
-            }
+            lt_check<DC, DC, S, false>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -504,34 +537,18 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtpLayout<DC, S>::BLOCKS)
             const uint32_t al = lane_act<S>(act, lane);
             float *sp = stage + (size_t)p * LY::STAGE;
             const int *vrow = m_vidx(cur.b) + ci * DC;
-            if constexpr (DC >= 6) {
-                if (deg <= 2) lt_compute<2, DC, S>(sp, deg, sb, lane, qmax2);
-                else lt_compute<DC, DC, S>(sp, deg, sb, lane, qmax2);
-            } else {
-                lt_compute<DC, DC, S>(sp, deg, sb, lane, qmax2);
-            }
-            __syncwarp();
             uint32_t *hbt = reinterpret_cast<uint32_t *>(ds.hb + (size_t)cur.t * cd.n);
             float *Lw = ds.L + (size_t)cur.t * cd.n * LINE + lane * S;
             float *mw = ds.msg + (size_t)cur.t * cd.E * LINE + lane * S;
-#pragma unroll
-            for (int k = 0; k < DC; ++k) {
-                if (k < deg) {
-                    const FV<S> post = ldv<S>(sp + k * LINE + lane * S);
-                    if (al) {
-                        stv<S>(mw + (size_t)(lo + k) * LINE, ldv<S>(sp + (DC + k) * LINE + lane * S));
-                        stv<S>(Lw + (size_t)vrow[k] * LINE, post);
-                    }
-                    uint32_t w[S];
-#pragma unroll
-                    for (int q = 0; q < S; ++q) w[q] = __ballot_sync(FULL, post.c[q] < 0.0f) & cmpu(act, q);
-                    if (lane == 0) {
-                        uint32_t *h = hbt + (size_t)vrow[k] * 4;
-                        if constexpr (S == 1) h[0] = w[0];
-                        else if constexpr (S == 2) *reinterpret_cast<uint2 *>(h) = make_uint2(w[0], w[1]);
-                        else *reinterpret_cast<uint4 *>(h) = make_uint4(w[0], w[1], w[2], w[3]);
-                    }
-                }
+            if (CVSR_LT_EXACT && deg == DC) {
+                lt_check<DC, DC, S, true>(sp, deg, sb, lane, qmax2, false, lo, vrow, al, act, mw, Lw, hbt);
+            } else if (CVSR_LT_EXACT && DC > 3 && deg == DC - 1) {
+                lt_check<(DC > 3 ? DC - 1 : DC), DC, S, true>(sp, deg, sb, lane, qmax2, false, lo, vrow, al, act, mw,
+                                                            Lw, hbt);
+            } else if (DC >= 6 && deg <= 2) {
+                lt_check<2, DC, S, false>(sp, deg, sb, lane, qmax2, false, lo, vrow, al, act, mw, Lw, hbt);
+            } else {
+                lt_check<DC, DC, S, false>(sp, deg, sb, lane, qmax2, false, lo, vrow, al, act, mw, Lw, hbt);
             }
         }
         fence_proxy_async_smem();
@@ -661,7 +678,8 @@ static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, dim3 grid,
         cudaFuncSetAttribute(k_layer_tma<DC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_layer_tma<DC, S><<<grid, lt_warps(S) * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2, first);
+    k_layer_tma<DC, S><<<grid, lt_warps(S) * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2, first,
+                                                            DC <= CVSR_LT_EXACT_MAXDC ? 1 : 0);
 }
 
 template <int S>

@@ -164,41 +164,56 @@ __device__ __forceinline__ float llr_eval_combo(const LlrParams &p, const float 
 // decoder feed: conditional LLR written straight into the interleaved arena
 // L[t][v][lane][S] (fused transpose, log2 units); known bits read from the
 // packed slices.  NK = number of known slices (compile time: the table index is
-// assembled with NK unrolled bit extractions, no per-symbol mask walking).
+// assembled with NK unrolled bit extractions, no per-symbol mask walking).  A block
+// covers LLR_VB groups of 32 variables of one tile (the edge table is staged once per
+// block).  hb != nullptr (layered schedule): the initial hard decisions hb[t][v] =
+// [L < 0] of the tile's active frames are written as well (k_layer_init's job).
+constexpr int LLR_VB = 4;
 template <int S, int NK>
 __global__ void __launch_bounds__(256) k_llr_interleaved(LlrParams p, const float *__restrict__ x, int32_t F,
-                                                         int32_t n, float *__restrict__ L) {
+                                                         int32_t n, float *__restrict__ L, uint4 *__restrict__ hb,
+                                                         const uint4 *__restrict__ tile_active) {
     __shared__ float se[256];
     __shared__ float sm[LANES * S][33];
     for (int i = threadIdx.x; i < 255; i += blockDim.x) se[i] = p.edges[i];
-    __syncthreads();
     const int t = blockIdx.y;
-    const int v0 = blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int Wn = words_of(n);
-    const int v = v0 + tx;
-    const uint32_t *kb[NK > 0 ? NK : 1];
+    const uint4 act = hb ? tile_active[t] : make_uint4(0u, 0u, 0u, 0u);
+    for (int g = 0; g < LLR_VB; ++g) {
+        const int v0 = (blockIdx.x * LLR_VB + g) * 32;
+        if (v0 >= n) break;  // block-uniform
+        __syncthreads();     // se staged / sm free again
+        const int v = v0 + tx;
+        const uint32_t *kb[NK > 0 ? NK : 1];
 #pragma unroll
-    for (int k = 0; k < NK; ++k) kb[k] = p.known_bits[p.kj[k]] + (v0 >> 5);
-    for (int fl = ty; fl < LANES * S; fl += 8) {
-        const int f = t * LANES * S + fl;
-        float val = 0.0f;
-        if (f < F && v < n) {
-            uint32_t combo = 0u;
+        for (int k = 0; k < NK; ++k) kb[k] = p.known_bits[p.kj[k]] + (v0 >> 5);
+        for (int fl = ty; fl < LANES * S; fl += 8) {
+            const int f = t * LANES * S + fl;
+            float val = 0.0f;
+            if (f < F && v < n) {
+                uint32_t combo = 0u;
 #pragma unroll
-            for (int k = 0; k < NK; ++k) combo |= ((__ldg(kb[k] + (size_t)f * Wn) >> tx) & 1u) << k;
-            val = llr_eval_combo(p, se, combo, x[(size_t)f * n + v]);
+                for (int k = 0; k < NK; ++k) combo |= ((__ldg(kb[k] + (size_t)f * Wn) >> tx) & 1u) << k;
+                val = llr_eval_combo(p, se, combo, x[(size_t)f * n + v]);
+            }
+            sm[fl][tx] = val * LOG2E;  // arena: log2 units
         }
-        sm[fl][tx] = val * LOG2E;  // arena: log2 units
-    }
-    __syncthreads();
-    for (int vl = ty; vl < 32; vl += 8) {
-        const int vv = v0 + vl;
-        if (vv < n) {
-            FV<S> o;
+        __syncthreads();
+        for (int vl = ty; vl < 32; vl += 8) {
+            const int vv = v0 + vl;
+            if (vv < n) {  // warp-uniform
+                FV<S> o;
 #pragma unroll
-            for (int s = 0; s < S; ++s) o.c[s] = sm[s * LANES + tx][vl];
-            stv<S>(L + (((size_t)t * n + vv) * LANES + tx) * S, o);
+                for (int s = 0; s < S; ++s) o.c[s] = sm[s * LANES + tx][vl];
+                stv<S>(L + (((size_t)t * n + vv) * LANES + tx) * S, o);
+                if (hb) {
+                    uint32_t w[SUBS] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                    for (int s = 0; s < S; ++s) w[s] = __ballot_sync(0xffffffffu, o.c[s] < 0.0f) & cmpu(act, s);
+                    if (tx == 0) hb[(size_t)t * n + vv] = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            }
         }
     }
 }
@@ -235,26 +250,26 @@ void launch_llr_biawgn(const float *y, int64_t count, float sigma2, float llr_ma
 }
 
 template <int S>
-static void launch_llr_il_s(const LlrParams &p, const float *x, int32_t F, int32_t n, dim3 grid, float *L,
-                            cudaStream_t s) {
+static void launch_llr_il_s(const LlrParams &p, const float *x, int32_t F, int32_t n, dim3 grid, float *L, uint4 *hb,
+                            const uint4 *act, cudaStream_t s) {
     switch (p.nk) {
-        case 0: k_llr_interleaved<S, 0><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
-        case 1: k_llr_interleaved<S, 1><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
-        case 2: k_llr_interleaved<S, 2><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
-        case 3: k_llr_interleaved<S, 3><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
-        case 4: k_llr_interleaved<S, 4><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
-        case 5: k_llr_interleaved<S, 5><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
-        case 6: k_llr_interleaved<S, 6><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
-        default: k_llr_interleaved<S, 7><<<grid, 256, 0, s>>>(p, x, F, n, L); break;
+        case 0: k_llr_interleaved<S, 0><<<grid, 256, 0, s>>>(p, x, F, n, L, hb, act); break;
+        case 1: k_llr_interleaved<S, 1><<<grid, 256, 0, s>>>(p, x, F, n, L, hb, act); break;
+        case 2: k_llr_interleaved<S, 2><<<grid, 256, 0, s>>>(p, x, F, n, L, hb, act); break;
+        case 3: k_llr_interleaved<S, 3><<<grid, 256, 0, s>>>(p, x, F, n, L, hb, act); break;
+        case 4: k_llr_interleaved<S, 4><<<grid, 256, 0, s>>>(p, x, F, n, L, hb, act); break;
+        case 5: k_llr_interleaved<S, 5><<<grid, 256, 0, s>>>(p, x, F, n, L, hb, act); break;
+        case 6: k_llr_interleaved<S, 6><<<grid, 256, 0, s>>>(p, x, F, n, L, hb, act); break;
+        default: k_llr_interleaved<S, 7><<<grid, 256, 0, s>>>(p, x, F, n, L, hb, act); break;
     }
 }
 
 void launch_llr_interleaved(const LlrParams &p, const float *x, int32_t F, int32_t n, int tiles, int subs, float *L,
-                            cudaStream_t s) {
-    dim3 grid((n + 31) / 32, tiles);
-    if (subs == 4) launch_llr_il_s<4>(p, x, F, n, grid, L, s);
-    else if (subs == 2) launch_llr_il_s<2>(p, x, F, n, grid, L, s);
-    else launch_llr_il_s<1>(p, x, F, n, grid, L, s);
+                            uint4 *hb, const uint4 *tile_active, cudaStream_t s) {
+    dim3 grid((n + 32 * LLR_VB - 1) / (32 * LLR_VB), tiles);
+    if (subs == 4) launch_llr_il_s<4>(p, x, F, n, grid, L, hb, tile_active, s);
+    else if (subs == 2) launch_llr_il_s<2>(p, x, F, n, grid, L, hb, tile_active, s);
+    else launch_llr_il_s<1>(p, x, F, n, grid, L, hb, tile_active, s);
 }
 
 }  // namespace cvsr
