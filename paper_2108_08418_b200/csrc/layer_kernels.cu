@@ -173,7 +173,10 @@ __global__ void __launch_bounds__(BLOCK, layer_minb(DC, S)) k_layer(CodeDev cd, 
 constexpr int LT_WARPS = 8;  // warps per block (k_layer_tmap, and k_layer_tma for S <= 2)
 // k_layer_tma: 4 warps per block at 4 frames per lane (512-byte lines: a warp's two stages take
 // 14 KB at check degree 7, so 8-warp blocks would leave one block per SM)
-__host__ __device__ constexpr int lt_warps(int S) { return S == 4 ? 4 : 8; }
+#ifndef CVSR_LT_WARPS2
+#define CVSR_LT_WARPS2 8
+#endif
+__host__ __device__ constexpr int lt_warps(int S) { return S == 4 ? 4 : (S == 2 ? CVSR_LT_WARPS2 : 8); }
 #ifndef CVSR_LT_CH
 #define CVSR_LT_CH 4
 #endif
@@ -193,7 +196,11 @@ struct LtLayout {
     static constexpr size_t BLOCK_BYTES = WARP_BYTES * lt_warps(S);
     // blocks per SM the shared memory allows (228 KB per SM, 1 KB reserved per block), at most 4
     static constexpr int SMEM_BLOCKS = (int)((228 * 1024) / (BLOCK_BYTES + 1024));
+#ifdef CVSR_LT_MINB
+    static constexpr int BLOCKS = CVSR_LT_MINB;
+#else
     static constexpr int BLOCKS = SMEM_BLOCKS < 1 ? 1 : (SMEM_BLOCKS > 4 ? 4 : SMEM_BLOCKS);
+#endif
 };
 
 // the check update of one check from its stage: DCT = compute width (>= deg; DCL = the stage
@@ -371,14 +378,20 @@ __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
         // exact-degree bodies for the two largest degrees (the irregular codes' checks take two
         // consecutive degrees; no padded dummy edges, no degree predicates), the 2-edge body for
         // MET type-A checks, and the padded body otherwise
-        if (CVSR_LT_EXACT && exact && deg == DC) {
-            lt_check<DC, DC, S, true>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
-        } else if (CVSR_LT_EXACT && exact && DC > 3 && deg == DC - 1) {
-            lt_check<(DC > 3 ? DC - 1 : DC), DC, S, true>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
-        } else if (DC >= 6 && deg <= 2) {
-            lt_check<2, DC, S, false>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
+        (void)exact;
+        if constexpr (CVSR_LT_EXACT && DC <= CVSR_LT_EXACT_MAXDC) {
+            if (deg == DC)
+                lt_check<DC, DC, S, true>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
+            else if (DC > 3 && deg == DC - 1)
+                lt_check<(DC > 3 ? DC - 1 : DC), DC, S, true>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw,
+                                                            hbt);
+            else
+                lt_check<DC, DC, S, false>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
         } else {
-            lt_check<DC, DC, S, false>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
+            if (DC >= 6 && deg <= 2)
+                lt_check<2, DC, S, false>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
+            else
+                lt_check<DC, DC, S, false>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
         }
         fence_proxy_async_smem();
         __syncwarp();
