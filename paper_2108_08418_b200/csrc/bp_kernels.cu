@@ -919,6 +919,8 @@ __global__ void k_set_counts(DecState ds, int32_t n_active) {
         ds.counts[0] = n_active;
         ds.counts[1] = 0;
         ds.counts[2] = 0;
+        ds.counts[8] = 0;  // work-item counter of the persistent layer kernel (k_layer_tmap)
+        ds.counts[9] = 0;  // its exit counter
     }
 }
 

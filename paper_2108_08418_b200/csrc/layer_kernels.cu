@@ -432,9 +432,29 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtpLayout<DC, S>::BLOCKS)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cpt = (lcnt + LT_CH - 1) / LT_CH;
     const int n_items = ds.counts[0] * cpt;
-    const int W = gridDim.x * LT_WARPS;
-    int it_cur = blockIdx.x * LT_WARPS + warp;
-    if (it_cur >= n_items) return;
+    // dynamic work distribution: items are grabbed from ds.counts[8]; the last warp to run out
+    // resets the counters for the next launch (ds.counts[9] counts exited warps)
+    const int total_warps = gridDim.x * LT_WARPS;
+    auto grab = [&]() {
+        int v = 0;
+        if (lane == 0) v = atomicAdd(&ds.counts[8], 1);
+        return __shfl_sync(FULL, v, 0);
+    };
+    auto leave = [&]() {
+        if (lane == 0) {
+            __threadfence();
+            if (atomicAdd(&ds.counts[9], 1) == total_warps - 1) {
+                ds.counts[8] = 0;
+                ds.counts[9] = 0;
+                __threadfence();
+            }
+        }
+    };
+    int it_cur = grab();
+    if (it_cur >= n_items) {
+        leave();
+        return;
+    }
     unsigned char *wb = lt_smem + (size_t)warp * LP::WARP_BYTES;
     float *stage = reinterpret_cast<float *>(wb);
     uint64_t *bar = reinterpret_cast<uint64_t *>(wb + (size_t)P * LY::STAGE * 4);
@@ -507,7 +527,7 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtpLayout<DC, S>::BLOCKS)
             if (deg > 0) bulk_g2s(sp + DC * LINE, mt + (size_t)lo * LINE, (uint32_t)deg * LINE * 4, &bar[p]);
         }
     };
-    int it_nxt = it_cur + W, it_nn = it_nxt + W;
+    int it_nxt = grab(), it_nn = grab();
     Item cur = make(it_cur, tile_of(it_cur), 0);
     Item nxt = make(it_nxt, tile_of(it_nxt), 1);
     int t_nn = tile_of(it_nn);
@@ -569,7 +589,10 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtpLayout<DC, S>::BLOCKS)
         ++done;
         ++ci;
         if (ci == cur.nc) {
-            if (!nxt.valid) break;
+            if (!nxt.valid) {
+                leave();
+                break;
+            }
             // the next item becomes current; its successor's metadata goes to the freed buffer
             const bool was_active = nxt_active;
             cur = nxt;
@@ -579,7 +602,7 @@ __global__ void __launch_bounds__(LT_WARPS * 32, LtpLayout<DC, S>::BLOCKS)
             if (!was_active) meta_wait(cur);
             nxt_active = false;
             it_nxt = it_nn;
-            it_nn += W;
+            it_nn = (it_nn < n_items) ? grab() : n_items;
             nxt = make(it_nxt, t_nn, 1 - cur.b);
             t_nn = tile_of(it_nn);
             fetch(nxt);
