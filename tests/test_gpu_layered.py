@@ -281,3 +281,45 @@ def test_reconcile_layered_c4_full_size_sampled(cv, ctx):
     both = ok_ref.astype(bool) & ok[sample]
     assert both.sum() >= 1 and np.array_equal(lab_g[both], lab_ref[both])
     pipe.close()
+
+
+def test_layered_variants_bit_identical(tmp_path):
+    """Every layered kernel variant performs the same arithmetic in the same layer order, so the
+    frames-per-lane choice (CVSR_SUBS = 1, 2, 4), the register-staged k_layer (CVSR_LAYER_TMA=0),
+    the persistent k_layer_tmap (CVSR_LAYER_PERSIST=1) and frame compaction off (CVSR_COMPACT=0)
+    give bit-identical labels, flags and iteration counts on a multi-tile C4-structure and C2
+    reconcile."""
+    prog = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from cvsr_inputs import awgn, configs
+from paper_2108_08418_b200.pipeline import SRPipeline
+out = {}
+for name, n, F in (("C4", 20000, 150), ("C2", 8192, 200)):
+    cfg = configs.scaled(configs.CONFIGS[name], n, F)
+    codes_l = cfg.build_codes()
+    x, y = awgn.quadratures(F, n, cfg.gamma, seed=44)
+    p = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, torch.device("cuda:0"),
+                   max_iter=cfg.max_iter, schedule="layered")
+    p.step(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+    torch.cuda.synchronize()
+    out[name + "_lab"] = p.label_alice.cpu().numpy()
+    out[name + "_ok"] = p.frame_ok.cpu().numpy()
+    out[name + "_it"] = p.iters.cpu().numpy()
+    p.close()
+np.savez(sys.argv[1], **out)
+'''
+    outs = []
+    for tag, env in (("default", {}), ("s1", {"CVSR_SUBS": "1"}), ("s4", {"CVSR_SUBS": "4"}),
+                     ("reg", {"CVSR_LAYER_TMA": "0"}), ("persist", {"CVSR_LAYER_PERSIST": "1"}),
+                     ("nocompact", {"CVSR_COMPACT": "0"})):
+        path = str(tmp_path / f"{tag}.npz")
+        res = subprocess.run([sys.executable, "-c", prog, path], cwd=ROOT, env=dict(os.environ, **env),
+                             capture_output=True, text=True, timeout=900)
+        assert res.returncode == 0, (tag, res.stderr[-2000:])
+        outs.append((tag, np.load(path)))
+    ref = outs[0][1]
+    assert ref["C4_ok"].sum() >= 100 and ref["C2_ok"].sum() >= 100
+    for tag, o in outs[1:]:
+        for k in ref.files:
+            assert np.array_equal(ref[k], o[k]), (tag, k)
