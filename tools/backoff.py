@@ -32,12 +32,8 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import torch  # noqa: E402
-
 from cvsr_inputs import codebook, configs  # noqa: E402
-from cvsr_inputs.awgn import torch_quadratures  # noqa: E402
-from paper_2108_08418_b200 import keyrate  # noqa: E402
-from paper_2108_08418_b200.pipeline import SRPipeline  # noqa: E402
+from paper_2108_08418_b200 import keyrate  # noqa: E402  (host fp64 formulas)
 
 DELTA_R = 0.05
 FLOOR = 0.01
@@ -53,6 +49,9 @@ def entry_for(cfg, j, family, rate, seed):
 
 def test(cfg, codes_l, j, frames, batch):
     """FER of slice j over `frames` frames (batches of the config's frames per GPU)."""
+    import torch
+    from cvsr_inputs.awgn import torch_quadratures
+    from paper_2108_08418_b200.pipeline import SRPipeline
     dev = torch.device("cuda:0")
     pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, cfg.n, batch, dev, cfg.max_iter,
                       schedule="layered")
@@ -72,6 +71,33 @@ def test(cfg, codes_l, j, frames, batch):
             "mean_iters": it / max(att, 1), "undetected": und, "seconds": round(time.time() - t0, 1)}
 
 
+def ladder(order, caps, trial):
+    """The back-off of PAPER.md:394 for the slices in decode `order` with capacities `caps`:
+    trial(j, family, rate, chosen) -> bool runs the failure test of slice j's candidate code given
+    the good codes `chosen` of the earlier slices.  Returns (chosen, trials): chosen[j] = (family,
+    rate) or None (disclosed), trials = [(j, family, rate, passed)] in order."""
+    chosen, trials = {}, []
+    for j in order:
+        r = math.floor(1000 * caps[j]) / 1000
+        while True:
+            if r < FLOOR:
+                chosen[j] = None
+                break
+            fams = ["met"] if r < 0.1 else (["irregular", "met"] if r <= 0.25 else ["irregular"])
+            passed = False
+            for fam in fams:
+                ok = trial(j, fam, r, dict(chosen))
+                trials.append((j, fam, r, ok))
+                if ok:
+                    chosen[j] = (fam, r)
+                    passed = True
+                    break
+            if passed:
+                break
+            r = round(r - DELTA_R, 3)
+    return chosen, trials
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C4")
@@ -81,45 +107,35 @@ def main():
     args = ap.parse_args()
     base = configs.CONFIGS[args.config]
     caps = keyrate.slice_capacities(base.gamma, base.m, base.delta, base.order)
-    chosen = {}   # slice -> (family, rate) of the good code; None = disclosed
-    trials = []
+    entries = []
+
+    def trial(j, fam, r, chosen):
+        slices = []
+        for s in base.slices:
+            if s.j == j:
+                slices.append(_spec(s.j, fam, r))
+            elif s.j in chosen:
+                slices.append(_spec(s.j, *chosen[s.j]) if chosen[s.j] else dataclasses.replace(s, kind="disclosed"))
+            else:
+                slices.append(s)
+        cfg = dataclasses.replace(base, slices=tuple(slices))
+        codes_l = cfg.build_codes(seed=args.seed)
+        res = test(cfg, codes_l, j, args.frames, base.frames)
+        ok = res["failed"] == 0 and res["undetected"] == 0
+        e = entry_for(cfg, j, fam, r, args.seed + 17 * j)
+        e["digest"] = codes_l[j].digest()
+        e["realised_rate"] = codes_l[j].rate
+        e["test"] = res
+        e["status"] = "good" if ok else "failed"
+        e["cap"] = float(caps[j])
+        entries.append(e)
+        print(json.dumps(e), flush=True)
+        return ok
+
+    chosen, _ = ladder(base.order, caps, trial)
     for j in base.order:
-        r = math.floor(1000 * caps[j]) / 1000
-        while True:
-            if r < FLOOR:
-                chosen[j] = None
-                print(json.dumps({"slice": j, "cap": caps[j], "disclosed": True}), flush=True)
-                break
-            fams = ["met"] if r < 0.1 else (["irregular", "met"] if r <= 0.25 else ["irregular"])
-            passed = False
-            for fam in fams:
-                slices = []
-                for s in base.slices:
-                    if s.j == j:
-                        slices.append(_spec(s.j, fam, r))
-                    elif s.j in chosen:
-                        slices.append(_spec(s.j, *chosen[s.j]) if chosen[s.j] else dataclasses.replace(s, kind="disclosed"))
-                    else:
-                        slices.append(s)
-                cfg = dataclasses.replace(base, slices=tuple(slices))
-                codes_l = cfg.build_codes(seed=args.seed)
-                res = test(cfg, codes_l, j, args.frames, base.frames)
-                ok = res["failed"] == 0 and res["undetected"] == 0
-                e = entry_for(cfg, j, fam, r, args.seed + 17 * j)
-                e["digest"] = codes_l[j].digest()
-                e["realised_rate"] = codes_l[j].rate
-                e["test"] = res
-                e["status"] = "good" if ok else "failed"
-                e["cap"] = float(caps[j])
-                trials.append(e)
-                print(json.dumps(e), flush=True)
-                if ok:
-                    chosen[j] = (fam, r)
-                    passed = True
-                    break
-            if passed:
-                break
-            r = round(r - DELTA_R, 3)
+        if chosen.get(j) is None:
+            print(json.dumps({"slice": j, "cap": caps[j], "disclosed": True}), flush=True)
     rates = [0.0 if chosen.get(j) is None else chosen[j][1] for j in range(base.m)]
     pi_my, _ = keyrate.entropies(base.gamma, base.m, base.delta)
     beta = keyrate.beta(pi_my, base.m, rates, base.gamma)
@@ -128,8 +144,8 @@ def main():
     print(json.dumps(summary), flush=True)
     if args.write:
         old = [e for e in codebook.load() if e["config"] != base.name]
-        codebook.save(old + trials, meta={"procedure": "tools/backoff.py (PAPER.md:394, DESIGN.md R-2')",
-                                          "last_summary": summary})
+        codebook.save(old + entries, meta={"procedure": "tools/backoff.py (PAPER.md:394, DESIGN.md R-2')",
+                                           "last_summary": summary})
 
 
 def _spec(j, family, rate):
