@@ -323,3 +323,35 @@ np.savez(sys.argv[1], **out)
     for tag, o in outs[1:]:
         for k in ref.files:
             assert np.array_equal(ref[k], o[k]), (tag, k)
+
+
+def test_reconcile_layered_c4b_full_size_properties(cv, ctx):
+    """C4b at full size (N_R = 5e6, 25 frames: one 32-frame tile at one frame per lane, the
+    paper's experimental optimum P:408) in the bench's launch configuration: properties that hold
+    at any size -- every reconciled frame reproduces Bob's syndromes of every coded slice, no frame
+    is an undetected error, flags and counts agree with cvsr_stats, iterations stay in range."""
+    cfg = configs.C4b
+    codes_l = cfg.build_codes()
+    F, n = cfg.frames, cfg.n
+    from cvsr_inputs.awgn import torch_quadratures
+    from paper_2108_08418_b200.pipeline import SRPipeline
+    xd, yd = torch_quadratures(F, n, cfg.gamma, torch.device("cuda:0"))
+    pipe = SRPipeline(cfg.m, cfg.edges(), codes_l, cfg.order, cfg.sigma_n, n, F, torch.device("cuda:0"),
+                      max_iter=cfg.max_iter, schedule="layered")
+    st = pipe.step(xd, yd, want_stats=True)
+    torch.cuda.synchronize()
+    ok = pipe.frame_ok.cpu().numpy().astype(bool)
+    it = pipe.iters.cpu().numpy()
+    assert st["frames"] == F and st["frames_ok"] == int(ok.sum()) and ok.all()
+    assert st["schedule"] == [0 if c is None else LAYERED for c in codes_l]
+    for j, c in enumerate(codes_l):
+        if c is None:
+            assert (it[:, j] == 0).all()
+            continue
+        assert ((it[:, j] >= 0) & (it[:, j] <= cfg.max_iter)).all()
+        s_a = torch.empty_like(pipe.synd[j])
+        cv.cvsr_syndrome(pipe.ctx, pipe.code_h[j], pipe.label_alice, F, j, s_a)
+        torch.cuda.synchronize()
+        assert (s_a == pipe.synd[j]).all(dim=1).cpu().numpy()[ok].all()
+    assert pipe.count_errors()[1] == 0
+    pipe.close()
