@@ -22,7 +22,7 @@ PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "codebook.json")
 
 
 def build(entry: Dict) -> _codes.Code:
-    """The code of a database entry (family "irregular" | "met")."""
+    """The code of a database entry (family "irregular" | "met" | "met_irr")."""
     p = entry["params"]
     if entry["family"] == "irregular":
         kw = {}
@@ -32,6 +32,8 @@ def build(entry: Dict) -> _codes.Code:
     if entry["family"] == "met":
         return _codes.met_low_rate(entry["n"], p["alpha"], p["beta"], p.get("dv_core", 3), p.get("dc_core", 6),
                                    seed=entry["seed"])
+    if entry["family"] == "met_irr":
+        return _codes.met_irregular_core(entry["n"], p["alpha"], p["core_rate"], seed=entry["seed"])
     raise ValueError(f"unknown family {entry['family']!r}")
 
 

@@ -236,6 +236,30 @@ def met_low_rate(n: int, alpha: float, beta: float, dv_core: int = 3, dc_core: i
                 name=f"MET alpha={alpha} beta={beta} core({dv_core},{dc_core}) n={n}")
 
 
+def met_irregular_core(n: int, alpha: float, core_rate: float, seed: int = 1,
+                       lam: Dict[int, float] = LAMBDA_IRREGULAR) -> Code:
+    """MET-style low-rate code with an IRREGULAR core (PROPOSED, R-2'): rate
+    alpha * core_rate.  Variables: n_c = alpha*n core nodes (indices 0..n_c-1) + n - n_c
+    degree-1 nodes; checks: the core code irregular_rate(n_c, core_rate, lam) over the core
+    nodes, then n - n_c type-A degree-2 checks {degree-1 node, core node}, the core nodes taking
+    the degree-1 nodes round-robin (~(1-alpha)/alpha each).  The type-A checks repeat every core
+    bit over several channel uses; the core code then works at a rate suited to its ensemble."""
+    n_c = int(round(alpha * n))
+    n_1 = n - n_c
+    core = irregular_rate(n_c, core_rate, seed=seed, lam=lam)
+    M_B = core.m_checks
+    core_of = (permutation(n_1, seed ^ 0xA11A) % n_c).astype(np.int32)
+    lens = np.concatenate([np.diff(core.row_ptr), np.full(n_1, 2, np.int32)])
+    row_ptr = np.zeros(M_B + n_1 + 1, dtype=np.int32)
+    row_ptr[1:] = np.cumsum(lens)
+    col_idx = np.empty(int(row_ptr[-1]), dtype=np.int32)
+    col_idx[:core.n_edges] = core.col_idx
+    b = np.arange(n_c, n, dtype=np.int32)
+    col_idx[core.n_edges:] = np.stack([np.minimum(core_of, b), np.maximum(core_of, b)], axis=1).reshape(-1)
+    return Code(n, M_B + n_1, row_ptr, col_idx,
+                name=f"MET alpha={alpha} irregular core R={core_rate} n={n}")
+
+
 def csc(code: Code) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
     """(col_ptr[n+1], row_of_edge[E] in CSC order, csr_pos[E] in CSC order)."""
     E = code.n_edges

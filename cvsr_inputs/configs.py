@@ -20,7 +20,7 @@ CODE_SEED = 1  # SURVEY.md §8(d) "Seeds"
 class SliceSpec:
     """One slice j: None code => disclosed (Bob's bits sent in the clear)."""
     j: int
-    kind: str            # "disclosed" | "irregular" | "met" | "regular"
+    kind: str            # "disclosed" | "irregular" | "met" | "met_irr" | "regular"
     rate: float = 0.0    # target rate (realised rate is 1 - M/n)
     met: Optional[Tuple[float, float, int, int]] = None  # (alpha, beta, dv_core, dc_core)
     lam: Optional[Tuple[Tuple[int, float], ...]] = None  # irregular: edge-perspective lambda (default LAMBDA_IRREGULAR)
@@ -61,6 +61,9 @@ class SRConfig:
             elif s.kind == "met":
                 a, b, dv, dc = s.met
                 out[s.j] = _codes.met_low_rate(self.n, a, b, dv, dc, seed=seed + 17 * s.j)
+            elif s.kind == "met_irr":  # met = (alpha, core_rate, 0, 0): MET-style with an irregular core
+                a, rc = s.met[0], s.met[1]
+                out[s.j] = _codes.met_irregular_core(self.n, a, rc, seed=seed + 17 * s.j)
             elif s.kind == "regular":
                 raise ValueError("regular slices are configured explicitly")
         return out
@@ -102,15 +105,16 @@ C3 = SRConfig(
 # C4: standard settings: gamma = 2.21468, m = 5, delta* = 0.21359, LSB-first
 # capacities (0.0006, 0.0022, 0.1670, 0.6485, 0.4918).  Rates from the code database's back-off
 # (cvsr_inputs/codebook.json, tools/backoff.py on B200; PAPER.md:394 with reading R-2': start at
-# the database rate closest to capacity, Delta R = 0.05 until 1000 frames decode with no failure
-# and no undetected error): S0, S1 disclosed (below the floor 0.01); S2 0.166 and
-# 0.116 fail (irregular and MET-style), 0.066 MET-style good (5.8 iterations); S3 0.648 fails,
-# 0.598 good (16.5); S4 0.491 fails, 0.441 good (22.6).  beta = 0.7505 (round 1: 0.715).
+# the database rate closest to capacity, Delta R = 0.05 until 2000 frames decode with no failure
+# and no undetected error): S0, S1 disclosed (below the floor 0.01); S2 0.166
+# fails with every family, 0.116 fails as irregular and passes as the MET-style code with an
+# irregular rate-0.4 core (alpha = 0.29; 27.3 iterations); S3 0.648 fails, 0.598 good (16.5);
+# S4 0.491 fails, 0.441 good (22.6).  beta = 0.8099 (round 1: 0.715).
 # N_R = 1e6 (the "~1e6" sub-block of Fig. 5), 125 frames per GPU of N = 1e9 on 8 GPUs.
 C4 = SRConfig(
     name="C4", m=5, gamma=2.214676, delta=0.21359, n=1_000_000, frames=125,
     slices=(SliceSpec(0, "disclosed"), SliceSpec(1, "disclosed"),
-            SliceSpec(2, "met", 0.066, (0.132, 0.066, 3, 6)), SliceSpec(3, "irregular", 0.598),
+            SliceSpec(2, "met_irr", 0.116, (0.29, 0.4, 0, 0)), SliceSpec(3, "irregular", 0.598),
             SliceSpec(4, "irregular", 0.441)),
     order=(0, 1, 2, 3, 4),
 )

@@ -14,8 +14,8 @@ For each slice S_j in decode order (PAPER.md:394 steps 1-3):
 Families (PAPER.md:392 uses MET codes below R = 0.1 and irregular codes above; our PROPOSED
 substitutes, reading A-7): for R < 0.1 the MET-style code (degree-1 variables, degree-2
 type-A checks, (3,6) core: alpha = 2R, beta = R); for R >= 0.1 the irregular code first and, if
-it fails (up to R = 0.25, where alpha = 2R stays <= 0.5), the MET-style code of the same rate
-before backing off.
+it fails (up to R = 0.25), the MET-style codes of the same rate -- with an irregular core of rate
+0.4 and 0.5 ("met_irr", alpha = R / core rate), then with the (3,6) core -- before backing off.
 
     python tools/backoff.py --config C4 --frames 2000 [--write]
 
@@ -39,9 +39,25 @@ DELTA_R = 0.05
 FLOOR = 0.01
 
 
+MET_IRR_CORE_RATES = (0.4, 0.5)
+
+
+def families(r):
+    """Families tried at rate r, in order (PAPER.md:392 reading)."""
+    if r < 0.1:
+        return ["met"]
+    if r <= 0.25:
+        return ["irregular"] + [f"met_irr{rc}" for rc in MET_IRR_CORE_RATES] + ["met"]
+    return ["irregular"]
+
+
 def entry_for(cfg, j, family, rate, seed):
     if family == "met":
         params = {"rate": rate, "alpha": round(2 * rate, 6), "beta": round(rate, 6), "dv_core": 3, "dc_core": 6}
+    elif family.startswith("met_irr"):
+        rc = float(family[len("met_irr"):])
+        params = {"rate": rate, "alpha": round(rate / rc, 6), "core_rate": rc}
+        family = "met_irr"
     else:
         params = {"rate": rate}
     return {"config": cfg.name, "slice": j, "n": cfg.n, "family": family, "params": params, "seed": seed}
@@ -83,7 +99,7 @@ def ladder(order, caps, trial):
             if r < FLOOR:
                 chosen[j] = None
                 break
-            fams = ["met"] if r < 0.1 else (["irregular", "met"] if r <= 0.25 else ["irregular"])
+            fams = families(r)
             passed = False
             for fam in fams:
                 ok = trial(j, fam, r, dict(chosen))
@@ -151,6 +167,9 @@ def main():
 def _spec(j, family, rate):
     if family == "met":
         return configs.SliceSpec(j, "met", rate, (round(2 * rate, 6), round(rate, 6), 3, 6))
+    if family.startswith("met_irr"):
+        rc = float(family[len("met_irr"):])
+        return configs.SliceSpec(j, "met_irr", rate, (round(rate / rc, 6), rc, 0, 0))
     return configs.SliceSpec(j, "irregular", rate)
 
 
