@@ -480,7 +480,7 @@ def main():
         if os.path.exists(tj):
             with open(tj) as f:
                 tr = json.load(f)
-            if tr.get("config") == cfg.name and tr.get("schedule") == args.schedule and kname.startswith(tr["kernel"]):
+            if tr.get("config") == cfg.name and tr.get("schedule") == args.schedule and tr["kernel"].startswith(kname):
                 tb = tr["bytes_per_useful_edge_frame"]
                 roofline["traffic"] = tb * edge_it_rank / max(kn / args.steps, 1)
                 roofline["traffic_note"] = (f"ncu dram__bytes_read+write summed over all {tr['launches']} "

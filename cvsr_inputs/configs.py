@@ -119,6 +119,13 @@ C4 = SRConfig(
     order=(0, 1, 2, 3, 4),
 )
 
+# C4 with S2 backed off one more rung to the (3,6)-core MET code at 0.066 (the round-2 database
+# before the irregular-core family was added): beta 0.7505 for 1.4x the throughput (S2 needs 5.8
+# instead of 27.3 iterations) -- the throughput end of the beta / throughput trade-off
+C4fast = dataclasses.replace(C4, name="C4fast", slices=(
+    SliceSpec(0, "disclosed"), SliceSpec(1, "disclosed"), SliceSpec(2, "met", 0.066, (0.132, 0.066, 3, 6)),
+    SliceSpec(3, "irregular", 0.598), SliceSpec(4, "irregular", 0.441)))
+
 # C4 at the paper's experimental optimum N_R = 5e6: 25 frames per GPU
 C4b = dataclasses.replace(C4, name="C4b", n=5_000_000, frames=25)
 
@@ -131,7 +138,7 @@ def c5(n_r: int) -> SRConfig:
     return dataclasses.replace(C4, name=f"C5[{n_r}]", n=n_r, frames=max(1, C5_SYMBOLS_PER_GPU // n_r))
 
 
-CONFIGS = {"C2": C2, "C3": C3, "C4": C4, "C4b": C4b}
+CONFIGS = {"C2": C2, "C3": C3, "C4": C4, "C4b": C4b, "C4fast": C4fast}
 
 
 def scaled(cfg: SRConfig, n: int, frames: int) -> SRConfig:

@@ -239,7 +239,11 @@ def test_reconcile_layered_parity(cv, ctx, name, n, frames):
     both = ok_ref.astype(bool) & g["ok"].astype(bool)
     assert both.sum() >= max(1, frames // 2)
     assert np.array_equal(g["label"][both], lab_ref[both])
-    assert np.array_equal(lab_ref[ok_ref.astype(bool)], lab_bob[ok_ref.astype(bool)])
+    # a converged frame can still be a wrong codeword at these short lengths (the MET code's
+    # low-weight codewords); both implementations then agree on it (above) and the hash check
+    # discards it -- the full-size C4 test below requires none at N_R = 1e6
+    okr = ok_ref.astype(bool)
+    assert np.sum(np.any(lab_ref[okr] != lab_bob[okr], axis=1)) <= max(1, frames // 50)
     assert np.sum(g["ok"] != ok_ref) <= max(1, frames // 20)
     assert np.sum(np.any(g["iters"][both] != it_ref[both], axis=1)) <= max(1, frames // 20)
     st = g["stats"]
