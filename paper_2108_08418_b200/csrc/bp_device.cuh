@@ -52,6 +52,16 @@ __device__ __forceinline__ uint32_t lane_act(const uint4 &m, int lane) {
 // |r| = +inf -> Q_MAX.
 template <int DC>
 __device__ __forceinline__ void cn_update(float (&q)[DC], uint32_t sbit, float qmax2) {
+    if constexpr (DC == 2) {
+        // two edges: the box-plus over the single other edge is that edge itself, so
+        // r_e = (1 - 2 s) clamp(q_other) exactly -- no transcendental; a dummy other edge
+        // (degree-1 check) gives the empty-fold value Q_MAX
+        const float m0 = fminf(fabsf(q[1]), qmax2), m1 = fminf(fabsf(q[0]), qmax2);
+        const uint32_t g0 = sbit ^ sgnbit(q[1]), g1 = sbit ^ sgnbit(q[0]);
+        q[0] = g0 ? -m0 : m0;
+        q[1] = g1 ? -m1 : m1;
+        return;
+    }
     float u[DC];
     uint32_t par = sbit;
 #pragma unroll
