@@ -118,7 +118,8 @@ def test_backoff_ladder_follows_paper_procedure():
     first above (MET retried up to 0.25), disclose below the floor 0.01; earlier
     slices' good codes are passed to later trials.  Checked with a stand-in failure test that
     passes when R <= 0.5 cap (MET with the (3,6) core), R <= 0.7 cap with an irregular core of
-    rate 0.4 only, or 0.25 < R <= 0.93 cap (irregular): the pattern measured on B200 for C4."""
+    rate <= 0.4, or 0.25 < R <= 0.93 cap (irregular): the pattern measured on B200 for C4; among
+    the codes passing at a rung the least decoding work wins."""
     import importlib.util
     import os
     spec = importlib.util.spec_from_file_location("backoff", os.path.join(os.path.dirname(__file__), "..",
@@ -131,16 +132,21 @@ def test_backoff_ladder_follows_paper_procedure():
     def trial(j, fam, r, chosen):
         seen.append((j, dict(chosen)))
         if fam == "met":
-            return r <= 0.5 * caps[j]
-        if fam.startswith("met_irr"):
-            return fam == "met_irr0.4" and r <= 0.7 * caps[j]
-        return 0.25 < r <= 0.93 * caps[j]
+            return r <= 0.5 * caps[j], 3.0
+        if fam.startswith("met_irr"):  # 0.3 / 0.35 / 0.4 pass, 0.35 with the least work
+            rc = float(fam[7:])
+            return rc <= 0.4 and r <= 0.7 * caps[j], {0.3: 2.0, 0.35: 1.0, 0.4: 1.5}.get(rc, 9.0)
+        return 0.25 < r <= 0.93 * caps[j], 1.0
 
     chosen, trials = bo.ladder([0, 1, 2, 3, 4], caps, trial)
     assert chosen[0] is None and chosen[1] is None
-    assert [(t[1], t[2], t[3]) for t in trials if t[0] == 2] == [
-        ("irregular", 0.166, False), ("met_irr0.4", 0.166, False), ("met_irr0.5", 0.166, False),
-        ("met", 0.166, False), ("irregular", 0.116, False), ("met_irr0.4", 0.116, True)]
+    t2 = [(t[1], t[2], t[3]) for t in trials if t[0] == 2]
+    assert [t for t in t2 if t[1] == 0.166] == [("irregular", 0.166, False), ("met_irr0.3", 0.166, False),
+                                                 ("met_irr0.35", 0.166, False), ("met_irr0.4", 0.166, False),
+                                                 ("met_irr0.5", 0.166, False), ("met", 0.166, False)]
+    assert [t for t in t2 if t[1] == 0.116 and t[2]] == [("met_irr0.3", 0.116, True), ("met_irr0.35", 0.116, True),
+                                                         ("met_irr0.4", 0.116, True)]
+    assert chosen[2] == ("met_irr0.35", 0.116) and min(t[1] for t in t2) == 0.116
     assert [(t[2], t[3]) for t in trials if t[0] == 3] == [(0.648, False), (0.598, True)]
     assert chosen[4] == ("irregular", 0.441)
-    assert seen[-1][1][3] == ("irregular", 0.598) and seen[-1][1][2] == ("met_irr0.4", 0.116)
+    assert seen[-1][1][3] == ("irregular", 0.598) and seen[-1][1][2] == ("met_irr0.35", 0.116)

@@ -15,7 +15,9 @@ Families (PAPER.md:392 uses MET codes below R = 0.1 and irregular codes above; o
 substitutes, reading A-7): for R < 0.1 the MET-style code (degree-1 variables, degree-2
 type-A checks, (3,6) core: alpha = 2R, beta = R); for R >= 0.1 the irregular code first and, if
 it fails (up to R = 0.25), the MET-style codes of the same rate -- with an irregular core of rate
-0.4 and 0.5 ("met_irr", alpha = R / core rate), then with the (3,6) core -- before backing off.
+0.3, 0.35, 0.4 and 0.5 ("met_irr", alpha = R / core rate), then with the (3,6) core -- before
+backing off.  When several families pass at a rate the one with the least decoding work (edges x
+mean iterations) is marked good.
 
     python tools/backoff.py --config C4 --frames 2000 [--write]
 
@@ -39,7 +41,7 @@ DELTA_R = 0.05
 FLOOR = 0.01
 
 
-MET_IRR_CORE_RATES = (0.4, 0.5)
+MET_IRR_CORE_RATES = (0.3, 0.35, 0.4, 0.5)
 
 
 def families(r):
@@ -89,9 +91,11 @@ def test(cfg, codes_l, j, frames, batch):
 
 def ladder(order, caps, trial):
     """The back-off of PAPER.md:394 for the slices in decode `order` with capacities `caps`:
-    trial(j, family, rate, chosen) -> bool runs the failure test of slice j's candidate code given
-    the good codes `chosen` of the earlier slices.  Returns (chosen, trials): chosen[j] = (family,
-    rate) or None (disclosed), trials = [(j, family, rate, passed)] in order."""
+    trial(j, family, rate, chosen) -> (passed, work) runs the failure test of slice j's candidate
+    code given the good codes `chosen` of the earlier slices (work = edges x mean iterations).  At
+    the highest rate where any family passes, the passing family with the least work is chosen.
+    Returns (chosen, trials): chosen[j] = (family, rate) or None (disclosed), trials = [(j, family,
+    rate, passed)] in order."""
     chosen, trials = {}, []
     for j in order:
         r = math.floor(1000 * caps[j]) / 1000
@@ -99,16 +103,14 @@ def ladder(order, caps, trial):
             if r < FLOOR:
                 chosen[j] = None
                 break
-            fams = families(r)
-            passed = False
-            for fam in fams:
-                ok = trial(j, fam, r, dict(chosen))
+            best = None
+            for fam in families(r):
+                ok, work = trial(j, fam, r, dict(chosen))
                 trials.append((j, fam, r, ok))
-                if ok:
-                    chosen[j] = (fam, r)
-                    passed = True
-                    break
-            if passed:
+                if ok and (best is None or work < best[1]):
+                    best = (fam, work)
+            if best is not None:
+                chosen[j] = (best[0], r)
                 break
             r = round(r - DELTA_R, 3)
     return chosen, trials
@@ -144,11 +146,19 @@ def main():
         e["test"] = res
         e["status"] = "good" if ok else "failed"
         e["cap"] = float(caps[j])
+        e["work"] = codes_l[j].n_edges * res["mean_iters"]
         entries.append(e)
         print(json.dumps(e), flush=True)
-        return ok
+        return ok, e["work"]
 
     chosen, _ = ladder(base.order, caps, trial)
+    for e in entries:  # only the chosen code of each slice is "good"; other passing ones "passed"
+        c = chosen.get(e["slice"])
+        picked = c is not None and e["params"]["rate"] == c[1] and (
+            e["family"] == c[0] or (c[0].startswith("met_irr") and e["family"] == "met_irr"
+                                    and abs(e["params"].get("core_rate", -1) - float(c[0][7:])) < 1e-9))
+        if e["status"] == "good" and not picked:
+            e["status"] = "passed"
     for j in base.order:
         if chosen.get(j) is None:
             print(json.dumps({"slice": j, "cap": caps[j], "disclosed": True}), flush=True)

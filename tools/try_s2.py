@@ -24,13 +24,17 @@ spec.loader.exec_module(bo)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=1000)
+    ap.add_argument("--rates", default="0.116,0.166")
+    ap.add_argument("--core-rates", default="0.4,0.5,0.6")
+    ap.add_argument("--no-met", action="store_true")
     args = ap.parse_args()
     base = configs.C4
     cands = []
-    for r in (0.116, 0.166):
-        for rc in (0.4, 0.5, 0.6):
+    for r in (float(v) for v in args.rates.split(",")):
+        for rc in (float(v) for v in args.core_rates.split(",")):
             cands.append(("met_irr", r, (round(r / rc, 6), rc, 0, 0)))
-        cands.append(("met", r, (round(2 * r, 6), r, 3, 6)))
+        if not args.no_met:
+            cands.append(("met", r, (round(2 * r, 6), r, 3, 6)))
     for kind, r, met in cands:
         sl = tuple(configs.SliceSpec(2, kind, r, met) if s.j == 2 else s for s in base.slices)
         cfg = dataclasses.replace(base, slices=sl)
