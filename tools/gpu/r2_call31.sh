@@ -1,0 +1,11 @@
+cd $GRAFT_REPO_ROOT
+one() { timeout 300 env $1 python bench.py --no-e2e --no-cpu-baseline --no-other-schedule --steps 5 --warmup 3 ${@:2} 2>gpurun_out/ab_err.txt | python -c "
+import json,sys
+d=json.loads(sys.stdin.readlines()[-1]); r=d['roofline']; b=d['roofline_bp_iteration']
+print('$*'.replace('build/variants/',''),'val %.4g'%d['value'],'ms %.2f'%d['ms_per_step'],'layer_frac %.3f'%r['frac'],'iter_frac %.3f'%b['frac'],'fer',d['fer'],'beta %.4f'%d['beta'],[round(x,2) for x in d['mean_iters']],{k:round(v,2) for k,v in b['kernel_ms_per_step'].items()})" || tail -3 gpurun_out/ab_err.txt; }
+one CVSR_X=0
+one CVSR_LAYER_PAIR=0
+one CVSR_X=0 --config C3
+one CVSR_LAYER_PAIR=0 --config C3
+one CVSR_X=0 --config C4fast
+timeout 900 python -m pytest tests -m gpu -x -q -k "layered or reconcile" > gpurun_out/t31_layered.log 2>&1; echo "layered rc $?"; tail -2 gpurun_out/t31_layered.log
