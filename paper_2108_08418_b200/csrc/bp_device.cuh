@@ -164,4 +164,12 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// programmatic dependent launch: wait until the preceding grid of the stream has completed and
+// its memory operations are visible (a no-op when the kernel was not launched as a dependent)
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the next (dependent) grid of the stream launch once every CTA of this grid has called it
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace cvsr

@@ -309,29 +309,35 @@ __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
     constexpr int P = LY::P;
     extern __shared__ __align__(128) unsigned char lt_smem[];
     const int ti = blockIdx.y;
-    if (ti >= ds.counts[0]) return;
-    const int t = ds.active_list[ti];
-    const uint4 act = ds.tile_active[t];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i0 = (blockIdx.x * lt_warps(S) + warp) * LT_CH;
     const int nc = min(LT_CH, lcnt - i0);
-    if (nc <= 0) return;
     unsigned char *wb = lt_smem + (size_t)warp * LY::WARP_BYTES;
     float *stage = reinterpret_cast<float *>(wb);
     uint64_t *bar = reinterpret_cast<uint64_t *>(wb + (size_t)P * LY::STAGE * 4);
     int *vidx = reinterpret_cast<int *>(bar + P);
-    if (lane == 0) {
-#pragma unroll
-        for (int p = 0; p < P; ++p) mbar_init(&bar[p], 1);
-        mbar_init_fence();
-    }
-    // the chunk's descriptors {row start, degree, check id}, padded column indices and syndrome
-    // rows: independent coalesced loads (layer_desc / layer_col built in layer order at code load;
-    // st rows are in layer order for the layered schedule)
+    // prologue on code-constant data only (it may overlap the previous layer's grid when launched
+    // as a programmatic dependent): the chunk's descriptors {row start, degree, check id} and
+    // padded column indices, independent coalesced loads (layer_desc / layer_col in layer order)
     const int g0 = lbeg + i0;
-    const int4 dsc = lane < nc ? cd.layer_desc[g0 + lane] : make_int4(0, 0, 0, 0);
-    for (int f = lane; f < LT_CH * DC; f += LANES) vidx[f] = f < nc * DC ? cd.layer_col[(size_t)g0 * DC + f] : 0;
+    int4 dsc = make_int4(0, 0, 0, 0);
+    if (nc > 0) {
+        if (lane == 0) {
+#pragma unroll
+            for (int p = 0; p < P; ++p) mbar_init(&bar[p], 1);
+            mbar_init_fence();
+        }
+        if (lane < nc) dsc = cd.layer_desc[g0 + lane];
+        for (int f = lane; f < LT_CH * DC; f += LANES) vidx[f] = f < nc * DC ? cd.layer_col[(size_t)g0 * DC + f] : 0;
+    }
+    // everything below reads state the previous kernels wrote (tile lists, syndrome rows, r, post)
+    griddep_wait();
+    griddep_launch_dependents();
+    if (ti >= ds.counts[0] || nc <= 0) return;
+    const int t = ds.active_list[ti];
+    const uint4 act = ds.tile_active[t];
     const int mylo = dsc.x, myhi = dsc.x + dsc.y;
+    // syndrome rows (in layer order for the layered schedule)
     const uint4 mys = lane < nc ? ds.st[(size_t)t * cd.M + g0 + lane] : make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     const float *Lt = ds.L + (size_t)t * cd.n * LINE;
@@ -705,6 +711,15 @@ void launch_synd_test(const CodeDev &cd, const DecState &ds, int grid_tiles, cud
     else k_synd_test<1><<<grid, 256, 0, s>>>(cd, ds);
 }
 
+// programmatic dependent launch of the layer kernels (CVSR_LAYER_PDL=0: plain stream order)
+static bool layer_pdl_enabled() {
+    static const int v = [] {
+        const char *e = getenv("CVSR_LAYER_PDL");
+        return (e && *e) ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 template <int DC, int S>
 static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,
                                int first, cudaStream_t s) {
@@ -714,8 +729,24 @@ static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, dim3 grid,
         cudaFuncSetAttribute(k_layer_tma<DC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_layer_tma<DC, S><<<grid, lt_warps(S) * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2, first,
-                                                            DC <= CVSR_LT_EXACT_MAXDC ? 1 : 0);
+    const int exact = DC <= CVSR_LT_EXACT_MAXDC ? 1 : 0;
+    if (!layer_pdl_enabled()) {
+        k_layer_tma<DC, S><<<grid, lt_warps(S) * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2, first, exact);
+        return;
+    }
+    // programmatic dependent launch: the grid is launched while the previous layer's last wave
+    // runs, its CTAs do the code-constant prologue and wait (griddep_wait) for that grid to finish
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = dim3(lt_warps(S) * 32);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaLaunchKernelEx(&lc, k_layer_tma<DC, S>, cd, ds, lbeg, lcnt, q2, first, exact);
 }
 
 template <int S>
