@@ -303,7 +303,7 @@ __device__ __forceinline__ void lt_check(float *__restrict__ sp, int deg, uint32
 #endif
 template <int DC, int S>
 __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
-    k_layer_tma(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2, int first, int exact) {
+    k_layer_tma(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2, int first, int exact, int early) {
     using LY = LtLayout<DC, S>;
     constexpr int LINE = LY::LINE;
     constexpr int P = LY::P;
@@ -316,9 +316,14 @@ __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
     float *stage = reinterpret_cast<float *>(wb);
     uint64_t *bar = reinterpret_cast<uint64_t *>(wb + (size_t)P * LY::STAGE * 4);
     int *vidx = reinterpret_cast<int *>(bar + P);
-    // prologue on code-constant data only (it may overlap the previous layer's grid when launched
-    // as a programmatic dependent): the chunk's descriptors {row start, degree, check id} and
-    // padded column indices, independent coalesced loads (layer_desc / layer_col in layer order)
+    // Prologue (it may overlap the previous layer's grid when launched as a programmatic
+    // dependent): the chunk's descriptors {row start, degree, check id} and padded column indices,
+    // independent coalesced loads (layer_desc / layer_col in layer order).  When `early` (the
+    // previous kernel of the stream is a layer kernel of the same iteration, so the tile lists,
+    // syndrome rows and compaction of this iteration are complete -- every CTA of that kernel
+    // passed its griddep_wait before this grid launched) the tile, its syndrome rows and the
+    // message lines of the first P checks (written by this layer's own kernel one iteration ago)
+    // are fetched here too; only the posterior lines wait for the previous layer.
     const int g0 = lbeg + i0;
     int4 dsc = make_int4(0, 0, 0, 0);
     if (nc > 0) {
@@ -329,23 +334,26 @@ __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
         }
         if (lane < nc) dsc = cd.layer_desc[g0 + lane];
         for (int f = lane; f < LT_CH * DC; f += LANES) vidx[f] = f < nc * DC ? cd.layer_col[(size_t)g0 * DC + f] : 0;
+        __syncwarp();  // barrier init and vidx visible to the whole warp
     }
-    // everything below reads state the previous kernels wrote (tile lists, syndrome rows, r, post)
-    griddep_wait();
-    griddep_launch_dependents();
-    if (ti >= ds.counts[0] || nc <= 0) return;
-    const int t = ds.active_list[ti];
-    const uint4 act = ds.tile_active[t];
     const int mylo = dsc.x, myhi = dsc.x + dsc.y;
-    // syndrome rows (in layer order for the layered schedule)
-    const uint4 mys = lane < nc ? ds.st[(size_t)t * cd.M + g0 + lane] : make_uint4(0u, 0u, 0u, 0u);
-    __syncwarp();
-    const float *Lt = ds.L + (size_t)t * cd.n * LINE;
-    const float *mt = ds.msg + (size_t)t * cd.E * LINE;
-    // stage p of check i: every lane copies its S frames of the deg posterior lines (cp.async,
-    // tracked by the stage's mbarrier); lane 0 arms the barrier with the message bytes and copies
-    // the deg message lines, one contiguous CSR span, with one bulk copy
-    auto issue = [&](int i, int p) {
+    const int npre = min(P, nc);
+    int t = 0;
+    uint4 act = make_uint4(0u, 0u, 0u, 0u), mys = make_uint4(0u, 0u, 0u, 0u);
+    const float *Lt = nullptr, *mt = nullptr;
+    // stage p of check i: lane 0 arms the stage's mbarrier with the message bytes and copies the
+    // deg message lines, one contiguous CSR span, with one bulk copy (first iteration: r = 0,
+    // reading R-9 init, nothing to load); every lane copies its S frames of the deg posterior
+    // lines (cp.async tracked by the same mbarrier) and lane 0 arrives once they are registered
+    auto issue_msg = [&](int i, int p) {
+        const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
+        if (lane == 0 && deg > 0 && !first) {
+            mbar_expect_tx(&bar[p], (uint32_t)deg * LINE * 4u);
+            bulk_g2s(stage + (size_t)p * LY::STAGE + DC * LINE, mt + (size_t)lo * LINE, (uint32_t)deg * LINE * 4,
+                     &bar[p]);
+        }
+    };
+    auto issue_post = [&](int i, int p) {
         const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
         float *sp = stage + (size_t)p * LY::STAGE;
         const int *vr = vidx + i * DC;
@@ -354,14 +362,33 @@ __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
             if (k < deg) cp_async_g2s<4 * S>(sp + k * LINE + lane * S, Lt + (size_t)vr[k] * LINE + lane * S);
         cp_async_mbar_arrive(&bar[p]);
         __syncwarp();  // every lane's pending-count increment precedes lane 0's arrival
-        if (lane == 0) {
-            // first iteration: r = 0 (reading R-9 init), no message lines to load
-            mbar_arrive_tx(&bar[p], first ? 0u : (uint32_t)deg * LINE * 4u);
-            if (deg > 0 && !first) bulk_g2s(sp + DC * LINE, mt + (size_t)lo * LINE, (uint32_t)deg * LINE * 4, &bar[p]);
-        }
+        if (lane == 0) mbar_arrive(&bar[p]);
     };
-    const int npre = min(P, nc);
-    for (int i = 0; i < npre; ++i) issue(i, i);
+    auto tile_meta = [&]() -> bool {
+        if (ti >= ds.counts[0] || nc <= 0) return false;
+        t = ds.active_list[ti];
+        act = ds.tile_active[t];
+        // syndrome rows (in layer order for the layered schedule)
+        if (lane < nc) mys = ds.st[(size_t)t * cd.M + g0 + lane];
+        Lt = ds.L + (size_t)t * cd.n * LINE;
+        mt = ds.msg + (size_t)t * cd.E * LINE;
+        return true;
+    };
+    bool live = true;
+    if (early) {
+        live = tile_meta();
+        if (live)
+            for (int i = 0; i < npre; ++i) issue_msg(i, i);
+    }
+    griddep_wait();  // the previous layer's posteriors (and, if !early, this iteration's lists)
+    griddep_launch_dependents();
+    if (!early) {
+        live = tile_meta();
+        if (live)
+            for (int i = 0; i < npre; ++i) issue_msg(i, i);
+    }
+    if (!live) return;
+    for (int i = 0; i < npre; ++i) issue_post(i, i);
     const uint32_t al = lane_act<S>(act, lane);
     uint32_t *hbt = reinterpret_cast<uint32_t *>(ds.hb + (size_t)t * cd.n);
     float *Lw = ds.L + (size_t)t * cd.n * LINE + lane * S;
@@ -401,7 +428,10 @@ __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (i + P < nc) issue(i + P, p);
+        if (i + P < nc) {
+            issue_msg(i + P, p);
+            issue_post(i + P, p);
+        }
     }
 }
 
@@ -720,9 +750,18 @@ static bool layer_pdl_enabled() {
     return v != 0;
 }
 
+// message lines of the first stages fetched before the dependency wait (CVSR_LAYER_EARLY=0: after)
+static bool layer_early_enabled() {
+    static const int v = [] {
+        const char *e = getenv("CVSR_LAYER_EARLY");
+        return (e && *e) ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 template <int DC, int S>
 static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,
-                               int first, cudaStream_t s) {
+                               int first, int early, cudaStream_t s) {
     static bool attr = false;
     constexpr size_t smem = LtLayout<DC, S>::BLOCK_BYTES;
     if (!attr) {
@@ -731,7 +770,7 @@ static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, dim3 grid,
     }
     const int exact = DC <= CVSR_LT_EXACT_MAXDC ? 1 : 0;
     if (!layer_pdl_enabled()) {
-        k_layer_tma<DC, S><<<grid, lt_warps(S) * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2, first, exact);
+        k_layer_tma<DC, S><<<grid, lt_warps(S) * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2, first, exact, 0);
         return;
     }
     // programmatic dependent launch: the grid is launched while the previous layer's last wave
@@ -746,23 +785,23 @@ static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, dim3 grid,
     lc.stream = s;
     lc.attrs = at;
     lc.numAttrs = 1;
-    cudaLaunchKernelEx(&lc, k_layer_tma<DC, S>, cd, ds, lbeg, lcnt, q2, first, exact);
+    cudaLaunchKernelEx(&lc, k_layer_tma<DC, S>, cd, ds, lbeg, lcnt, q2, first, exact, early);
 }
 
 template <int S>
 static bool launch_layer_tma_s(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,
-                               int first, cudaStream_t s) {
+                               int first, int early, cudaStream_t s) {
     switch (cd.max_dc) {
-        case 1: case 2: launch_layer_tma_t<2, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
-        case 3: launch_layer_tma_t<3, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
-        case 4: launch_layer_tma_t<4, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
-        case 5: launch_layer_tma_t<5, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
-        case 6: launch_layer_tma_t<6, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
-        case 7: launch_layer_tma_t<7, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
-        case 8: launch_layer_tma_t<8, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
-        case 9: launch_layer_tma_t<9, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
-        case 10: launch_layer_tma_t<10, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
-        case 11: case 12: launch_layer_tma_t<12, S>(cd, ds, grid, lbeg, lcnt, q2, first, s); return true;
+        case 1: case 2: launch_layer_tma_t<2, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
+        case 3: launch_layer_tma_t<3, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
+        case 4: launch_layer_tma_t<4, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
+        case 5: launch_layer_tma_t<5, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
+        case 6: launch_layer_tma_t<6, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
+        case 7: launch_layer_tma_t<7, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
+        case 8: launch_layer_tma_t<8, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
+        case 9: launch_layer_tma_t<9, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
+        case 10: launch_layer_tma_t<10, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
+        case 11: case 12: launch_layer_tma_t<12, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
         default: return false;
     }
 }
@@ -840,9 +879,12 @@ int launch_layers(const CodeDev &cd, const DecState &ds, int grid_tiles, float q
         }
         if (tma) {
             const int f = first ? 1 : 0;
-            if (ds.subs == 4) launch_layer_tma_s<4>(cd, ds, grid, lbeg, lcnt, q2, f, s);
-            else if (ds.subs == 2) launch_layer_tma_s<2>(cd, ds, grid, lbeg, lcnt, q2, f, s);
-            else launch_layer_tma_s<1>(cd, ds, grid, lbeg, lcnt, q2, f, s);
+            // the tile lists / messages may be read before the dependency wait only when the
+            // previous kernel of the stream is the layer kernel launched just above
+            const int early = (l > 0 && layer_pdl_enabled() && layer_early_enabled()) ? 1 : 0;
+            if (ds.subs == 4) launch_layer_tma_s<4>(cd, ds, grid, lbeg, lcnt, q2, f, early, s);
+            else if (ds.subs == 2) launch_layer_tma_s<2>(cd, ds, grid, lbeg, lcnt, q2, f, early, s);
+            else launch_layer_tma_s<1>(cd, ds, grid, lbeg, lcnt, q2, f, early, s);
             continue;
         }
         if (ds.subs == 4) launch_layer_s<4>(cd, ds, grid, lbeg, lcnt, q2, s);
