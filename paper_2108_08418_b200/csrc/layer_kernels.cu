@@ -170,11 +170,13 @@ __global__ void __launch_bounds__(BLOCK, layer_minb(DC, S)) k_layer(CodeDev cd, 
 // Checks of one layer share no variable, so prefetching the next checks' posterior lines while
 // the current check is being written is exact.  The arithmetic is k_layer's operation for
 // operation (results are bit-identical).
-constexpr int LT_WARPS = 8;  // warps per block (k_layer_tmap, and k_layer_tma for S <= 2)
+constexpr int LT_WARPS = 8;  // warps per block (k_layer_tmap, and k_layer_tma for S = 1)
 // k_layer_tma: 4 warps per block at 4 frames per lane (512-byte lines: a warp's two stages take
-// 14 KB at check degree 7, so 8-warp blocks would leave one block per SM)
+// 14 KB at check degree 7, so 8-warp blocks would leave one block per SM) and at 2 frames per
+// lane (CVSR_LT_WARPS2; the same warps per SM in smaller blocks shorten each layer's tail: C4
+// 104.4 -> 102.9 ms, C2 42.7 -> 42.0 ms with 8 / 4 warps; 2 and 6 warps measured in between)
 #ifndef CVSR_LT_WARPS2
-#define CVSR_LT_WARPS2 8
+#define CVSR_LT_WARPS2 4
 #endif
 __host__ __device__ constexpr int lt_warps(int S) { return S == 4 ? 4 : (S == 2 ? CVSR_LT_WARPS2 : 8); }
 #ifndef CVSR_LT_CH
