@@ -877,8 +877,10 @@ cvsr_status cvsr_syndrome(cvsr_ctx *ctx, const cvsr_code *code, const uint8_t *l
     if (frames == 0) return CVSR_OK;
     if (!label || !synd_out) return fail(CVSR_EINVAL, "null buffer");
     DeviceGuard g(ctx->device);
-    // pack S_j first (coalesced), then gather bits from the small packed rows
-    const size_t need = (size_t)frames * words_of(code->d.n) * sizeof(uint32_t);
+    // pack S_j first (coalesced), then the bit-sliced transpose of the packed rows and one 16-byte
+    // gather per edge for 128 frames (launch_syndrome_bits)
+    const size_t bits_bytes = (((size_t)frames * words_of(code->d.n) * sizeof(uint32_t)) + 255) & ~(size_t)255;
+    const size_t need = bits_bytes + (size_t)code->d.n * syndrome_sliced_groups(frames) * sizeof(uint32_t);
     if (need > ctx->bob_bits_cap) {
         CK(cudaStreamSynchronize(ctx->stream));
         if (ctx->bob_bits) CK(cudaFree(ctx->bob_bits));
@@ -892,8 +894,9 @@ cvsr_status cvsr_syndrome(cvsr_ctx *ctx, const cvsr_code *code, const uint8_t *l
         ctx->bob_bits_cap = need;
     }
     launch_slice_bits(label, frames, code->d.n, slice_j, ctx->bob_bits, ctx->stream);
-    launch_syndrome_bits(code->d, ctx->bob_bits, frames, synd_out, ctx->stream);
-    return check_launch(ctx, 2);
+    uint32_t *sliced = reinterpret_cast<uint32_t *>(reinterpret_cast<unsigned char *>(ctx->bob_bits) + bits_bytes);
+    const int k = launch_syndrome_bits(code->d, ctx->bob_bits, frames, synd_out, sliced, ctx->stream);
+    return check_launch(ctx, 1 + k);
 }
 
 // builds the LLR table for p on the context stream (p.table stays null when the grid

@@ -1,4 +1,6 @@
 // Bob-side kernels (quantise, slice bits, syndrome) and reconcile bookkeeping.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -157,6 +159,61 @@ __global__ void __launch_bounds__(BLOCK) k_syndrome_bits_smem(CodeDev cd, const 
     }
 }
 
+// Bit-sliced syndrome (default for cvsr_syndrome): the packed rows [F][Wn] are transposed to
+// sl[v][g] = bits of variable v for frames 32 g .. 32 g + 31 (G4 words per variable, a multiple of
+// 4), then a warp takes 32 consecutive checks (lane = check) and 4 frame groups: per edge one
+// 16-byte gather of the variable's 128 frames' bits instead of one 32-byte sector per frame, and
+// the column indices are read once per 128 frames.  A 32 x 32 bit transpose turns the checks'
+// parity words back into the frames' syndrome words.  Same XOR as k_syndrome_bits: bit-exact.
+__global__ void __launch_bounds__(256) k_bits_to_sliced(const uint32_t *__restrict__ bits, int32_t F, int32_t n,
+                                                        int32_t G4, uint32_t *__restrict__ sl) {
+    __shared__ uint32_t sm[32][33];
+    const int Wn = words_of(n);
+    const int w0 = blockIdx.x * 32, g = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = warp; r < 32; r += 8) {
+        const int f = g * 32 + r, w = w0 + lane;
+        sm[r][lane] = (f < F && w < Wn) ? bits[(size_t)f * Wn + w] : 0u;
+    }
+    __syncthreads();
+    for (int c = warp; c < 32; c += 8) {
+        const int w = w0 + c;
+        if (w >= Wn) break;  // warp-uniform
+        const uint32_t y = transpose32(sm[lane][c], lane);  // lane i: variable 32 w + i, bit r = frame 32 g + r
+        const int v = w * 32 + lane;
+        if (v < n) sl[(size_t)v * G4 + g] = y;
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK) k_syndrome_sliced(CodeDev cd, const uint32_t *__restrict__ sl, int32_t G4,
+                                                           int32_t F, uint32_t *__restrict__ synd) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int Wm = words_of(cd.M);
+    const int w = blockIdx.x * WARPS_PER_BLOCK + warp;
+    if (w >= Wm) return;  // warp-uniform
+    const int q = blockIdx.y;  // frame groups 4 q .. 4 q + 3
+    const int c = w * 32 + lane;
+    uint4 par = make_uint4(0u, 0u, 0u, 0u);
+    if (c < cd.M) {
+        const int beg = cd.row_ptr[c], end = cd.row_ptr[c + 1];
+#pragma unroll 4
+        for (int e = beg; e < end; ++e) {
+            const uint4 b = __ldg(reinterpret_cast<const uint4 *>(sl + (size_t)cd.col_idx[e] * G4) + q);
+            par.x ^= b.x;
+            par.y ^= b.y;
+            par.z ^= b.z;
+            par.w ^= b.w;
+        }
+    }
+    const uint32_t pw[4] = {par.x, par.y, par.z, par.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t y = transpose32(pw[k], lane);  // lane f: bit i = parity of check 32 w + i, frame 32 g + f
+        const int f = (4 * q + k) * 32 + lane;
+        if (f < F) synd[(size_t)f * Wm + w] = y;
+    }
+}
+
 // simulation check: counts {ok frames, ok frames with any label mismatch, mismatching bytes}
 __global__ void k_count_errors(const uint8_t *__restrict__ a, const uint8_t *__restrict__ b,
                                const uint8_t *__restrict__ ok, int32_t n, unsigned long long *counts) {
@@ -281,7 +338,26 @@ void launch_syndrome(const CodeDev &cd, const uint8_t *label, int32_t F, int32_t
     k_syndrome<<<grid, BLOCK, 0, s>>>(cd, label, j, synd);
 }
 
-void launch_syndrome_bits(const CodeDev &cd, const uint32_t *bits, int32_t F, uint32_t *synd, cudaStream_t s) {
+int32_t syndrome_sliced_groups(int32_t F) { return ((words_of(F) + 3) / 4) * 4; }
+
+static bool syndrome_sliced_enabled() {
+    static const int v = [] {
+        const char *e = getenv("CVSR_SYND_SLICED");
+        return (e && *e) ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
+int launch_syndrome_bits(const CodeDev &cd, const uint32_t *bits, int32_t F, uint32_t *synd, uint32_t *sliced,
+                         cudaStream_t s) {
+    if (sliced && syndrome_sliced_enabled()) {
+        const int32_t G4 = syndrome_sliced_groups(F);
+        // every group including the padding ones (frames >= F are written as zeros)
+        k_bits_to_sliced<<<dim3((words_of(cd.n) + 31) / 32, G4), 256, 0, s>>>(bits, F, cd.n, G4, sliced);
+        k_syndrome_sliced<<<dim3((words_of(cd.M) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, G4 / 4), BLOCK, 0, s>>>(
+            cd, sliced, G4, F, synd);
+        return 2;
+    }
     // stage FB frames' rows in shared memory when they fit (<= 96 KB per block) and the
     // batch still fills the GPU with blocks; otherwise the per-frame kernel
     const size_t row = (size_t)words_of(cd.n) * 4;
@@ -297,6 +373,7 @@ void launch_syndrome_bits(const CodeDev &cd, const uint32_t *bits, int32_t F, ui
         dim3 grid((words_of(cd.M) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, F);
         k_syndrome_bits<<<grid, BLOCK, 0, s>>>(cd, bits, synd);
     }
+    return 1;
 }
 
 void launch_count_errors(const uint8_t *a, const uint8_t *b, const uint8_t *ok, int32_t F, int32_t n,

@@ -784,20 +784,6 @@ __global__ void __launch_bounds__(1024) k_list(DecState ds, int32_t *host_counts
 }
 
 // Write the hard decisions of retired frames as packed bits (32x32 bit transposes by ballots).
-// Bit-matrix transpose across a warp: lane r holds row r (bit c = element [r][c]); returns
-// column `lane` (bit r = element [r][lane]).  Round j swaps the j x j off-diagonal blocks
-// between lane r and lane r ^ j.
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-    constexpr uint32_t M[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-        const int j = 16 >> k;
-        const uint32_t y = __shfl_xor_sync(FULL, x, j);
-        x = (lane & j) ? ((x & ~M[k]) | ((y & ~M[k]) >> j)) : ((x & M[k]) | ((y & M[k]) << j));
-    }
-    return x;
-}
-
 __global__ void __launch_bounds__(BLOCK) k_retire(DecState ds, int32_t n, uint32_t *bits_out) {
     const int ti = blockIdx.y;
     if (ti >= ds.counts[1]) return;

@@ -124,6 +124,22 @@ constexpr float LLR_H = 2.0f * LLR_XMAX / 4096.0f;
 
 __host__ __device__ inline int32_t words_of(int64_t bits) { return (int32_t)((bits + 31) / 32); }
 
+#ifdef __CUDACC__
+// Bit-matrix transpose across a warp (all 32 lanes): lane r holds row r (bit c = element [r][c]);
+// returns column `lane` (bit r = element [r][lane]).  Round j swaps the j x j off-diagonal blocks
+// between lane r and lane r ^ j.
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+    constexpr uint32_t M[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int j = 16 >> k;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+        x = (lane & j) ? ((x & ~M[k]) | ((y & ~M[k]) >> j)) : ((x & M[k]) | ((y & M[k]) << j));
+    }
+    return x;
+}
+#endif
+
 // compute width of the layered kernels for a code's maximum check degree (the template DC of
 // k_layer / k_layer_tma): exact for 3..10, 2 for degrees <= 2, 12 for 11..12; 0 = unsupported
 inline int32_t layer_width(int32_t max_dc) {

@@ -38,7 +38,11 @@ int launch_compact(const CodeDev &cd, const DecState &src, const DecState &dst, 
 void launch_quantise(const float *edges_host, int m, const float *y, int64_t count, uint8_t *label, cudaStream_t s);
 void launch_slice_bits(const uint8_t *label, int32_t F, int32_t n, int32_t j, uint32_t *bits, cudaStream_t s);
 void launch_syndrome(const CodeDev &cd, const uint8_t *label, int32_t F, int32_t j, uint32_t *synd, cudaStream_t s);
-void launch_syndrome_bits(const CodeDev &cd, const uint32_t *bits, int32_t F, uint32_t *synd, cudaStream_t s);
+// sliced: scratch of n x syndrome_sliced_groups(F) words (16-byte aligned) for the bit-sliced
+// kernels, or null for the per-frame kernels; returns the number of launches
+int launch_syndrome_bits(const CodeDev &cd, const uint32_t *bits, int32_t F, uint32_t *synd, uint32_t *sliced,
+                         cudaStream_t s);
+int32_t syndrome_sliced_groups(int32_t F);
 void launch_frame_hash(const uint8_t *label, int32_t F, int32_t n, unsigned long long key, unsigned long long *out,
                        cudaStream_t s);
 void launch_verify(const uint8_t *label_a, const uint8_t *label_b, const uint8_t *ok_in, int32_t F, int32_t n,
