@@ -735,8 +735,105 @@ __global__ void __launch_bounds__(256) k_synd_test(CodeDev cd, DecState ds) {
         atomicOr(reinterpret_cast<uint32_t *>(&ds.tile_unsat[t]) + threadIdx.x, s_unsat[threadIdx.x]);
 }
 
+// Same test with the check's padded column indices from layer_col (DC = layer_dc, one row of
+// consecutive words per check) and TT tiles per thread: every index load and then every
+// hard-decision gather of the TT tiles is issued before the first XOR, so a thread has up to
+// TT x DC independent gathers in flight instead of a dependent index -> gather chain per edge.
+constexpr int ST_TT = 2;
+template <int S, int DC>
+__global__ void __launch_bounds__(256) k_synd_test_w(CodeDev cd, DecState ds) {
+    __shared__ uint32_t s_unsat[ST_TT][SUBS];
+    if (threadIdx.x < ST_TT * SUBS) s_unsat[threadIdx.x / SUBS][threadIdx.x % SUBS] = 0u;
+    __syncthreads();
+    const int i = blockIdx.x * 256 + threadIdx.x;  // layer-order position (st rows are in layer order)
+    const int nt = min(ST_TT, ds.counts[0] - (int)blockIdx.y * ST_TT);
+    if (nt <= 0) return;  // block-uniform
+    int tt[ST_TT];
+    uint4 act[ST_TT];
+#pragma unroll
+    for (int k = 0; k < ST_TT; ++k) {
+        tt[k] = k < nt ? ds.active_list[blockIdx.y * ST_TT + k] : 0;
+        act[k] = k < nt ? ds.tile_active[tt[k]] : make_uint4(0u, 0u, 0u, 0u);
+    }
+    uint4 u[ST_TT];
+#pragma unroll
+    for (int k = 0; k < ST_TT; ++k) u[k] = make_uint4(0u, 0u, 0u, 0u);
+    if (i < cd.M) {
+        const int deg = cd.layer_desc[i].y;
+        int col[DC];
+#pragma unroll
+        for (int e = 0; e < DC; ++e) col[e] = cd.layer_col[(size_t)i * DC + e];
+#pragma unroll
+        for (int k = 0; k < ST_TT; ++k) {
+            if (k < nt) {
+                const uint4 *hbt = ds.hb + (size_t)tt[k] * cd.n;
+                uint4 a = ds.st[(size_t)tt[k] * cd.M + i];
+#pragma unroll
+                for (int e = 0; e < DC; ++e) {
+                    if (e < deg) {
+                        const uint4 h = hbt[col[e]];
+                        a.x ^= h.x;
+                        if (S > 1) a.y ^= h.y;
+                        if (S > 2) {
+                            a.z ^= h.z;
+                            a.w ^= h.w;
+                        }
+                    }
+                }
+                u[k] = a;
+            }
+        }
+    }
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < ST_TT; ++k) {
+        const uint32_t w4[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+            const uint32_t v = __reduce_or_sync(FULL, w4[q]) & cmpu(act[k], q);
+            if (lane == 0 && v) atomicOr(&s_unsat[k][q], v);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < ST_TT * S) {
+        const int k = threadIdx.x / S, q = threadIdx.x % S;
+        if (k < nt && s_unsat[k][q])
+            atomicOr(reinterpret_cast<uint32_t *>(&ds.tile_unsat[tt[k]]) + q, s_unsat[k][q]);
+    }
+}
+
+static bool synd_test_w_enabled() {
+    static const int v = [] {
+        const char *e = getenv("CVSR_SYND_TEST_W");
+        return (e && *e) ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
+template <int S>
+static bool launch_synd_test_w(const CodeDev &cd, const DecState &ds, int grid_tiles, cudaStream_t s) {
+    dim3 grid((cd.M + 255) / 256, (grid_tiles + ST_TT - 1) / ST_TT);
+    switch (cd.layer_dc) {
+        case 2: k_synd_test_w<S, 2><<<grid, 256, 0, s>>>(cd, ds); return true;
+        case 3: k_synd_test_w<S, 3><<<grid, 256, 0, s>>>(cd, ds); return true;
+        case 4: k_synd_test_w<S, 4><<<grid, 256, 0, s>>>(cd, ds); return true;
+        case 5: k_synd_test_w<S, 5><<<grid, 256, 0, s>>>(cd, ds); return true;
+        case 6: k_synd_test_w<S, 6><<<grid, 256, 0, s>>>(cd, ds); return true;
+        case 7: k_synd_test_w<S, 7><<<grid, 256, 0, s>>>(cd, ds); return true;
+        case 8: k_synd_test_w<S, 8><<<grid, 256, 0, s>>>(cd, ds); return true;
+        case 9: k_synd_test_w<S, 9><<<grid, 256, 0, s>>>(cd, ds); return true;
+        case 10: k_synd_test_w<S, 10><<<grid, 256, 0, s>>>(cd, ds); return true;
+        default: return false;
+    }
+}
+
 void launch_synd_test(const CodeDev &cd, const DecState &ds, int grid_tiles, cudaStream_t s) {
     if (grid_tiles <= 0) return;
+    if (synd_test_w_enabled() && cd.layer_col) {
+        if (ds.subs == 4 && launch_synd_test_w<4>(cd, ds, grid_tiles, s)) return;
+        if (ds.subs == 2 && launch_synd_test_w<2>(cd, ds, grid_tiles, s)) return;
+        if (ds.subs == 1 && launch_synd_test_w<1>(cd, ds, grid_tiles, s)) return;
+    }
     dim3 grid((cd.M + 255) / 256, grid_tiles);
     if (ds.subs == 4) k_synd_test<4><<<grid, 256, 0, s>>>(cd, ds);
     else if (ds.subs == 2) k_synd_test<2><<<grid, 256, 0, s>>>(cd, ds);
