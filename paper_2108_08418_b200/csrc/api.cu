@@ -903,7 +903,10 @@ cvsr_status cvsr_syndrome(cvsr_ctx *ctx, const cvsr_code *code, const uint8_t *l
 // would be too coarse for sigma_n; the kernels then evaluate exactly)
 static cvsr_status prepare_llr_table(cvsr_ctx *ctx, LlrParams &p, int *launched) {
     p.table = nullptr;
-    const size_t need = ((size_t)1 << __builtin_popcount(p.known_mask)) * LLR_NTAB * sizeof(float);
+    p.table4 = nullptr;
+    const size_t combos = (size_t)1 << __builtin_popcount(p.known_mask);
+    const size_t scalar_bytes = (combos * LLR_NTAB * sizeof(float) + 255) & ~(size_t)255;
+    const size_t need = scalar_bytes + combos * LLR_NWIN * sizeof(float4);
     if (need > ctx->llr_tab_cap) {
         CK(cudaStreamSynchronize(ctx->stream));
         if (ctx->llr_tab) CK(cudaFree(ctx->llr_tab));
@@ -916,9 +919,11 @@ static cvsr_status prepare_llr_table(cvsr_ctx *ctx, LlrParams &p, int *launched)
         }
         ctx->llr_tab_cap = need;
     }
-    if (launch_llr_table(p, ctx->llr_tab, ctx->stream)) {
+    float4 *win = reinterpret_cast<float4 *>(reinterpret_cast<unsigned char *>(ctx->llr_tab) + scalar_bytes);
+    if (launch_llr_table(p, ctx->llr_tab, win, ctx->stream)) {
         p.table = ctx->llr_tab;
-        ++*launched;
+        p.table4 = win;
+        *launched += 2;
     }
     return CVSR_OK;
 }

@@ -111,6 +111,7 @@ struct LlrParams {
     int32_t nk;                     // number of known slices
     int32_t kj[8];                  // their indices, ascending (bit t of a table combo = slice kj[t])
     const float *table;             // [2^|K|][LLR_NTAB] unclamped L on the x grid (nullptr: exact only)
+    const float4 *table4;           // [2^|K|][LLR_NWIN] windows (table[i .. i+3]) of the same values
     float edges[255];
 };
 
@@ -121,6 +122,8 @@ struct LlrParams {
 constexpr int LLR_NTAB = 4096 + 3;
 constexpr float LLR_XMAX = 10.0f;
 constexpr float LLR_H = 2.0f * LLR_XMAX / 4096.0f;
+// interpolation windows: window i = the 4 grid values of interval i's cubic (one 16-byte load)
+constexpr int LLR_NWIN = 4095;
 
 __host__ __device__ inline int32_t words_of(int64_t bits) { return (int32_t)((bits + 31) / 32); }
 

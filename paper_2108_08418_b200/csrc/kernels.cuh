@@ -52,7 +52,8 @@ void launch_count_errors(const uint8_t *a, const uint8_t *b, const uint8_t *ok, 
                          unsigned long long *counts, cudaStream_t s);
 
 // llr_kernels.cu
-bool launch_llr_table(const LlrParams &p, float *table, cudaStream_t s);
+// scalar table and its 16-byte interpolation windows (2 launches); false: grid too coarse, none
+bool launch_llr_table(const LlrParams &p, float *table, float4 *table4, cudaStream_t s);
 void launch_llr_slice(const LlrParams &p, const float *x, const uint8_t *known_label, int32_t F, int32_t n,
                       float *out, cudaStream_t s);
 void launch_llr_biawgn(const float *y, int64_t count, float sigma2, float llr_max, float *out, cudaStream_t s);

@@ -118,16 +118,27 @@ __global__ void k_llr_table(LlrParams p, float *__restrict__ table, int combos) 
     table[idx] = llr_raw(se, p.m, p.j, p.known_mask, kappa_of(p.known_mask, combo), x, p.inv_sigma);
 }
 
+// window table: table4[combo][i] = (table[i], table[i+1], table[i+2], table[i+3]) -- the 4 values
+// one interpolation reads, as one aligned 16-byte load (the 4 scalar loads per symbol were the
+// L1 wavefront bound of the LLR kernels: 82 % of the global-load wavefront peak)
+__global__ void k_llr_window(const float *__restrict__ table, float4 *__restrict__ table4, int combos) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= combos * LLR_NWIN) return;
+    const int combo = idx / LLR_NWIN, i = idx % LLR_NWIN;
+    const float *f = table + (size_t)combo * LLR_NTAB + i;
+    table4[idx] = make_float4(f[0], f[1], f[2], f[3]);
+}
+
 // L(x) from the table (cubic Lagrange through grid points i-1..i+2) or exactly
 __device__ __forceinline__ float llr_eval(const LlrParams &p, const float *se, uint32_t kappa, float x) {
     const float u = (x + LLR_XMAX) * (1.0f / LLR_H);
-    if (p.table && u >= 0.0f && u < 4095.0f) {
+    if (p.table4 && u >= 0.0f && u < 4095.0f) {
         const int i = (int)u;
         const float t = u - (float)i;
-        const float *f = p.table + (size_t)combo_of(p.known_mask, kappa) * LLR_NTAB + i;  // f[0] = grid point i-1
+        const float4 f = __ldg(p.table4 + (size_t)combo_of(p.known_mask, kappa) * LLR_NWIN + i);  // .x: point i-1
         const float tm1 = t - 1.0f, tm2 = t - 2.0f, tp1 = t + 1.0f;
-        const float L = (-t * tm1 * tm2 * (1.0f / 6.0f)) * f[0] + (tp1 * tm1 * tm2 * 0.5f) * f[1] +
-                        (-tp1 * t * tm2 * 0.5f) * f[2] + (tp1 * t * tm1 * (1.0f / 6.0f)) * f[3];
+        const float L = (-t * tm1 * tm2 * (1.0f / 6.0f)) * f.x + (tp1 * tm1 * tm2 * 0.5f) * f.y +
+                        (-tp1 * t * tm2 * 0.5f) * f.z + (tp1 * t * tm1 * (1.0f / 6.0f)) * f.w;
         return llr_clamp(L, p.llr_max);
     }
     return llr_cond(se, p.m, p.j, p.known_mask, kappa, x, p.inv_sigma, p.llr_max);
@@ -149,13 +160,13 @@ __global__ void k_llr_slice(LlrParams p, const float *__restrict__ x, const uint
 // slice kj[t]); exact evaluation off the grid
 __device__ __forceinline__ float llr_eval_combo(const LlrParams &p, const float *se, uint32_t combo, float x) {
     const float u = (x + LLR_XMAX) * (1.0f / LLR_H);
-    if (p.table && u >= 0.0f && u < 4095.0f) {
+    if (p.table4 && u >= 0.0f && u < 4095.0f) {
         const int i = (int)u;
         const float t = u - (float)i;
-        const float *f = p.table + (size_t)combo * LLR_NTAB + i;  // f[0] = grid point i-1
+        const float4 f = __ldg(p.table4 + (size_t)combo * LLR_NWIN + i);  // .x: grid point i-1
         const float tm1 = t - 1.0f, tm2 = t - 2.0f, tp1 = t + 1.0f;
-        const float L = (-t * tm1 * tm2 * (1.0f / 6.0f)) * f[0] + (tp1 * tm1 * tm2 * 0.5f) * f[1] +
-                        (-tp1 * t * tm2 * 0.5f) * f[2] + (tp1 * t * tm1 * (1.0f / 6.0f)) * f[3];
+        const float L = (-t * tm1 * tm2 * (1.0f / 6.0f)) * f.x + (tp1 * tm1 * tm2 * 0.5f) * f.y +
+                        (-tp1 * t * tm2 * 0.5f) * f.z + (tp1 * t * tm1 * (1.0f / 6.0f)) * f.w;
         return llr_clamp(L, p.llr_max);
     }
     return llr_cond(se, p.m, p.j, p.known_mask, kappa_of(p.known_mask, (int)combo), x, p.inv_sigma, p.llr_max);
@@ -231,11 +242,12 @@ static int grid_for(int64_t work, int block) {
 }
 
 // table for p (p.table is the destination); returns false when the grid is too coarse for sigma_n
-bool launch_llr_table(const LlrParams &p, float *table, cudaStream_t s) {
+bool launch_llr_table(const LlrParams &p, float *table, float4 *table4, cudaStream_t s) {
     if (LLR_H * p.inv_sigma > 0.02f) return false;
     const int combos = 1 << __builtin_popcount(p.known_mask);
     const int total = combos * LLR_NTAB;
     k_llr_table<<<(total + 255) / 256, 256, 0, s>>>(p, table, combos);
+    k_llr_window<<<(combos * LLR_NWIN + 255) / 256, 256, 0, s>>>(table, table4, combos);
     return true;
 }
 
