@@ -46,6 +46,13 @@
  *    path.  CVSR_SCHEDULE [flooding]: "layered" makes the row-layered
  *    schedule the default of calls whose cvsr_decode_opts.flags leave the
  *    schedule unset (CVSR_SCHED_DEFAULT); the flags select it per call.
+ *    Layered-path variants, all tested bit-identical to the default:
+ *    CVSR_LAYER_TMA [1] (0: register-staged k_layer), CVSR_LAYER_PERSIST [0]
+ *    (persistent k_layer_tmap), CVSR_LAYER_PDL [1] (layer kernels launched as
+ *    programmatic dependents), CVSR_LAYER_EARLY [1] (tile lists and first
+ *    message lines read before the dependency wait), CVSR_SYND_TEST_W [1]
+ *    (syndrome test from the padded layer rows, two tiles per thread);
+ *    CVSR_SYND_SLICED [1]: cvsr_syndrome through bit-sliced 32-frame words.
  *  - Layouts.  "frame-major" arrays are [frames][n] row-major.  Packed bit
  *    vectors put bit i at bit (i mod 32) of 32-bit word floor(i/32); a
  *    vector of B bits occupies ceil(B/32) words per frame; padding bits are

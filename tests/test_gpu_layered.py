@@ -290,8 +290,10 @@ def test_reconcile_layered_c4_full_size_sampled(cv, ctx):
 def test_layered_variants_bit_identical(tmp_path):
     """Every layered kernel variant performs the same arithmetic in the same layer order, so the
     frames-per-lane choice (CVSR_SUBS = 1, 2, 4), the register-staged k_layer (CVSR_LAYER_TMA=0),
-    the persistent k_layer_tmap (CVSR_LAYER_PERSIST=1) and frame compaction off (CVSR_COMPACT=0)
-    give bit-identical labels, flags and iteration counts on a multi-tile C4-structure and C2
+    the persistent k_layer_tmap (CVSR_LAYER_PERSIST=1), frame compaction off (CVSR_COMPACT=0),
+    plain stream-ordered layer launches (CVSR_LAYER_PDL=0), no reads before the dependency wait
+    (CVSR_LAYER_EARLY=0), the thread-per-(check, tile) syndrome test (CVSR_SYND_TEST_W=0) and
+    Bob's per-frame syndrome kernels (CVSR_SYND_SLICED=0) give bit-identical labels, flags and iteration counts on a multi-tile C4-structure and C2
     reconcile."""
     prog = r'''
 import sys, numpy as np, torch
@@ -316,7 +318,9 @@ np.savez(sys.argv[1], **out)
     outs = []
     for tag, env in (("default", {}), ("s1", {"CVSR_SUBS": "1"}), ("s4", {"CVSR_SUBS": "4"}),
                      ("reg", {"CVSR_LAYER_TMA": "0"}), ("persist", {"CVSR_LAYER_PERSIST": "1"}),
-                     ("nocompact", {"CVSR_COMPACT": "0"})):
+                     ("nocompact", {"CVSR_COMPACT": "0"}), ("nopdl", {"CVSR_LAYER_PDL": "0"}),
+                     ("noearly", {"CVSR_LAYER_EARLY": "0"}), ("synd_test_thread", {"CVSR_SYND_TEST_W": "0"}),
+                     ("bob_synd_per_frame", {"CVSR_SYND_SLICED": "0"})):
         path = str(tmp_path / f"{tag}.npz")
         res = subprocess.run([sys.executable, "-c", prog, path], cwd=ROOT, env=dict(os.environ, **env),
                              capture_output=True, text=True, timeout=900)
