@@ -823,6 +823,13 @@ cvsr_status cvsr_code_load(cvsr_ctx *ctx, int32_t n_vars, int32_t n_checks, cons
     d.layer_pos = ldc > 0 ? d_lp : nullptr;
     d.layer_dc = ldc;
     for (int l = 0; l <= MAX_LAYERS; ++l) d.layer_off[l] = layer_off[l];
+    for (int l = 0; l < MAX_LAYERS; ++l) {
+        int32_t nb = 0;
+        if (l < n_layers)
+            for (int32_t i = layer_off[l]; i < layer_off[l + 1]; ++i)
+                nb += (row_ptr[layer_chk[i] + 1] - row_ptr[layer_chk[i]]) > 2;
+        d.layer_nbig[l] = nb;
+    }
     code->d = d;
     *out = code;
     return CVSR_OK;

@@ -59,6 +59,9 @@ struct CodeDev {
     const int32_t *layer_pos;      // [M] position of check c in layer order (inverse of layer_chk)
     const int32_t *layer_col;      // [M * layer_dc]
     int32_t layer_dc;
+    // checks of layer l with degree > 2 (a layer is sorted by degree, so they come first; the
+    // degree <= 2 tail is taken in longer chunks by k_layer_tma, host copy)
+    int32_t layer_nbig[MAX_LAYERS];
 };
 
 // Per-decode device state (lives in the context's scratch arena).  Syndrome rows st are in check

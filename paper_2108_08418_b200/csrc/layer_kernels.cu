@@ -1,6 +1,8 @@
 // Row-layered BP schedule (reading R-9) for sm_100a.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "bp_device.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
@@ -186,6 +188,11 @@ __host__ __device__ constexpr int lt_warps(int S) { return S == 4 ? 4 : (S == 2 
 #define CVSR_LT_STAGE_KB 3
 #endif
 constexpr int LT_CH = CVSR_LT_CH;  // checks per warp
+#ifndef CVSR_LT_CH2
+#define CVSR_LT_CH2 12
+#endif
+constexpr int LT_CH2 = CVSR_LT_CH2;  // degree <= 2 checks per warp (codes with DC >= 6)
+static_assert(LT_CH <= 32 && LT_CH2 <= 32, "a chunk's descriptors are held one per lane");
 
 template <int DC, int S>
 struct LtLayout {
@@ -193,7 +200,14 @@ struct LtLayout {
     static constexpr int STAGE = 2 * DC * LINE;            // floats: DC posterior lines, then DC message lines
     // stages per warp: 3 while a stage is at most CVSR_LT_STAGE_KB, else 2 (shared memory per SM)
     static constexpr int P = (STAGE * 4 <= CVSR_LT_STAGE_KB * 1024) ? 3 : 2;
-    static constexpr size_t RAW = (size_t)P * STAGE * 4 + P * 8 + (size_t)LT_CH * DC * 4;
+    // degree <= 2 checks of codes with DC >= 6 (MET type-A checks): the stages are re-cut into NS2
+    // slots of 2 posterior + 2 message lines, so a warp has NS2 such checks in flight, and a warp
+    // takes LT_CH2 of them
+    static constexpr bool PAIRS = DC >= 6;
+    static constexpr int NS2 = PAIRS ? P * DC / 2 : 0;
+    static constexpr int NB = NS2 > P ? NS2 : P;  // mbarriers per warp
+    static constexpr int VIDX = LT_CH * DC > 2 * LT_CH2 ? LT_CH * DC : 2 * LT_CH2;
+    static constexpr size_t RAW = (size_t)P * STAGE * 4 + NB * 8 + (size_t)VIDX * 4;
     static constexpr size_t WARP_BYTES = (RAW + 127) & ~(size_t)127;
     static constexpr size_t BLOCK_BYTES = WARP_BYTES * lt_warps(S);
     // blocks per SM the shared memory allows (228 KB per SM, 1 KB reserved per block), at most 4
@@ -303,21 +317,130 @@ __device__ __forceinline__ void lt_check(float *__restrict__ sp, int deg, uint32
 #ifndef CVSR_LT_EXACT_MAXDC
 #define CVSR_LT_EXACT_MAXDC 5
 #endif
+// k_layer_tma's pipeline for a chunk of nc <= LT_CH2 degree <= 2 checks (layer positions g0 ..):
+// NS2 slots of 2 posterior + 2 message lines cut from the warp's stages, one mbarrier each.  Same
+// per-check steps and arithmetic as the general path (lt_check<2, ...>), so results are identical;
+// only more checks are in flight per warp and a warp's prologue is shared by LT_CH2 checks.
+template <int DC, int S>
+__device__ __forceinline__ void lt_pairs(const CodeDev &cd, const DecState &ds, int g0, int nc, int ti, int lane,
+                                         unsigned char *wb, float qmax2, int first, int early) {
+    using LY = LtLayout<DC, S>;
+    constexpr int LINE = LY::LINE;
+    constexpr int NS = LY::NS2;
+    constexpr int SLOT = 4 * LINE;  // floats
+    float *stage = reinterpret_cast<float *>(wb);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(wb + (size_t)LY::P * LY::STAGE * 4);
+    int *vidx = reinterpret_cast<int *>(bar + LY::NB);
+    int4 dsc = make_int4(0, 0, 0, 0);
+    if (nc > 0) {
+        if (lane == 0) {
+#pragma unroll
+            for (int p = 0; p < NS; ++p) mbar_init(&bar[p], 1);
+            mbar_init_fence();
+        }
+        if (lane < nc) dsc = cd.layer_desc[g0 + lane];
+        for (int f = lane; f < 2 * LT_CH2; f += LANES)
+            vidx[f] = (f >> 1) < nc ? cd.layer_col[(size_t)(g0 + (f >> 1)) * DC + (f & 1)] : 0;
+        __syncwarp();
+    }
+    const int mylo = dsc.x, myhi = dsc.x + dsc.y;
+    const int npre = min(NS, nc);
+    int t = 0;
+    uint4 act = make_uint4(0u, 0u, 0u, 0u), mys = make_uint4(0u, 0u, 0u, 0u);
+    const float *Lt = nullptr, *mt = nullptr;
+    auto issue_msg = [&](int i, int p) {
+        const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
+        if (lane == 0 && deg > 0 && !first) {
+            mbar_expect_tx(&bar[p], (uint32_t)deg * LINE * 4u);
+            bulk_g2s(stage + (size_t)p * SLOT + 2 * LINE, mt + (size_t)lo * LINE, (uint32_t)deg * LINE * 4, &bar[p]);
+        }
+    };
+    auto issue_post = [&](int i, int p) {
+        const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
+        float *sp = stage + (size_t)p * SLOT;
+        const int *vr = vidx + i * 2;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+            if (k < deg) cp_async_g2s<4 * S>(sp + k * LINE + lane * S, Lt + (size_t)vr[k] * LINE + lane * S);
+        cp_async_mbar_arrive(&bar[p]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar[p]);
+    };
+    auto tile_meta = [&]() -> bool {
+        if (ti >= ds.counts[0] || nc <= 0) return false;
+        t = ds.active_list[ti];
+        act = ds.tile_active[t];
+        if (lane < nc) mys = ds.st[(size_t)t * cd.M + g0 + lane];
+        Lt = ds.L + (size_t)t * cd.n * LINE;
+        mt = ds.msg + (size_t)t * cd.E * LINE;
+        return true;
+    };
+    bool live = true;
+    if (early) {
+        live = tile_meta();
+        if (live)
+            for (int i = 0; i < npre; ++i) issue_msg(i, i);
+    }
+    griddep_wait();
+    griddep_launch_dependents();
+    if (!early) {
+        live = tile_meta();
+        if (live)
+            for (int i = 0; i < npre; ++i) issue_msg(i, i);
+    }
+    if (!live) return;
+    for (int i = 0; i < npre; ++i) issue_post(i, i);
+    const uint32_t al = lane_act<S>(act, lane);
+    uint32_t *hbt = reinterpret_cast<uint32_t *>(ds.hb + (size_t)t * cd.n);
+    float *Lw = ds.L + (size_t)t * cd.n * LINE + lane * S;
+    float *mw = ds.msg + (size_t)t * cd.E * LINE + lane * S;
+    uint32_t phase = 0u;
+    for (int i = 0; i < nc; ++i) {
+        const int p = i % NS;
+        mbar_wait(&bar[p], (phase >> p) & 1u);
+        phase ^= 1u << p;
+        const int lo = __shfl_sync(FULL, mylo, i), deg = __shfl_sync(FULL, myhi, i) - lo;
+        uint4 sw;
+        sw.x = __shfl_sync(FULL, mys.x, i);
+        sw.y = (S > 1) ? __shfl_sync(FULL, mys.y, i) : 0u;
+        sw.z = (S > 2) ? __shfl_sync(FULL, mys.z, i) : 0u;
+        sw.w = (S > 2) ? __shfl_sync(FULL, mys.w, i) : 0u;
+        const uint32_t sb = lane_act<S>(sw, lane);
+        lt_check<2, 2, S, false>(stage + (size_t)p * SLOT, deg, sb, lane, qmax2, first != 0, lo, vidx + i * 2, al, act,
+                                 mw, Lw, hbt);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (i + NS < nc) {
+            issue_msg(i + NS, p);
+            issue_post(i + NS, p);
+        }
+    }
+}
+
 template <int DC, int S>
 __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
-    k_layer_tma(CodeDev cd, DecState ds, int lbeg, int lcnt, float qmax2, int first, int exact, int early) {
+    k_layer_tma(CodeDev cd, DecState ds, int lbeg, int lcnt, int nbig, int ch2, float qmax2, int first, int early) {
     using LY = LtLayout<DC, S>;
     constexpr int LINE = LY::LINE;
     constexpr int P = LY::P;
     extern __shared__ __align__(128) unsigned char lt_smem[];
     const int ti = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i0 = (blockIdx.x * lt_warps(S) + warp) * LT_CH;
-    const int nc = min(LT_CH, lcnt - i0);
+    const int gw = blockIdx.x * lt_warps(S) + warp;  // the warp's chunk in the layer
+    const int nch = (nbig + LT_CH - 1) / LT_CH;      // chunks of degree > 2 checks
     unsigned char *wb = lt_smem + (size_t)warp * LY::WARP_BYTES;
+    if constexpr (LY::PAIRS) {
+        if (gw >= nch) {  // warp-uniform: a chunk of the layer's degree <= 2 tail
+            const int j0 = nbig + (gw - nch) * ch2;
+            lt_pairs<DC, S>(cd, ds, lbeg + j0, min(ch2, lcnt - j0), ti, lane, wb, qmax2, first, early);
+            return;
+        }
+    }
+    const int i0 = gw * LT_CH;
+    const int nc = min(LT_CH, nbig - i0);
     float *stage = reinterpret_cast<float *>(wb);
     uint64_t *bar = reinterpret_cast<uint64_t *>(wb + (size_t)P * LY::STAGE * 4);
-    int *vidx = reinterpret_cast<int *>(bar + P);
+    int *vidx = reinterpret_cast<int *>(bar + LY::NB);
     // Prologue (it may overlap the previous layer's grid when launched as a programmatic
     // dependent): the chunk's descriptors {row start, degree, check id} and padded column indices,
     // independent coalesced loads (layer_desc / layer_col in layer order).  When `early` (the
@@ -413,7 +536,6 @@ __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
         // exact-degree bodies for the two largest degrees (the irregular codes' checks take two
         // consecutive degrees; no padded dummy edges, no degree predicates), the 2-edge body for
         // MET type-A checks, and the padded body otherwise
-        (void)exact;
         if constexpr (CVSR_LT_EXACT && DC <= CVSR_LT_EXACT_MAXDC) {
             if (deg == DC)
                 lt_check<DC, DC, S, true>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
@@ -849,6 +971,15 @@ static bool layer_pdl_enabled() {
     return v != 0;
 }
 
+// degree <= 2 layer tails in LT_CH2-check chunks with NS2 slots (CVSR_LAYER_PAIRS=0: LT_CH chunks)
+static bool layer_pairs_enabled() {
+    static const int v = [] {
+        const char *e = getenv("CVSR_LAYER_PAIRS");
+        return (e && *e) ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 // message lines of the first stages fetched before the dependency wait (CVSR_LAYER_EARLY=0: after)
 static bool layer_early_enabled() {
     static const int v = [] {
@@ -859,7 +990,7 @@ static bool layer_early_enabled() {
 }
 
 template <int DC, int S>
-static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,
+static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, int grid_tiles, int l, float q2,
                                int first, int early, cudaStream_t s) {
     static bool attr = false;
     constexpr size_t smem = LtLayout<DC, S>::BLOCK_BYTES;
@@ -867,9 +998,28 @@ static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, dim3 grid,
         cudaFuncSetAttribute(k_layer_tma<DC, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    const int exact = DC <= CVSR_LT_EXACT_MAXDC ? 1 : 0;
+    const int lbeg = cd.layer_off[l], lcnt = cd.layer_off[l + 1] - lbeg;
+    // degree <= 2 tail in LT_CH2-check chunks (codes with DC >= 6), the rest in LT_CH-check chunks
+    const int nbig = (LtLayout<DC, S>::PAIRS && layer_pairs_enabled()) ? cd.layer_nbig[l] : lcnt;
+    // chunk length of the tail: LT_CH2 while that leaves at least 4 waves of warps (resident warps
+    // per GPU from the occupancy of this instantiation), else shorter (C3's many small MET layers:
+    // 12-check chunks left 1.3 waves, 11.7 -> 12.8 ms per step)
+    static int resident = 0;
+    if (!resident) {
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_layer_tma<DC, S>, lt_warps(S) * 32,
+                                                      LtLayout<DC, S>::BLOCK_BYTES);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        resident = std::max(1, per_sm * lt_warps(S) * sms);
+    }
+    int ch2 = LT_CH2;
+    const int64_t tail = (int64_t)(lcnt - nbig) * grid_tiles;
+    while (ch2 > LT_CH && tail < (int64_t)4 * resident * ch2) ch2 -= LT_CH;
+    const int chunks = (nbig + LT_CH - 1) / LT_CH + (lcnt - nbig + ch2 - 1) / ch2;
+    const dim3 grid((chunks + lt_warps(S) - 1) / lt_warps(S), grid_tiles);
     if (!layer_pdl_enabled()) {
-        k_layer_tma<DC, S><<<grid, lt_warps(S) * 32, smem, s>>>(cd, ds, lbeg, lcnt, q2, first, exact, 0);
+        k_layer_tma<DC, S><<<grid, lt_warps(S) * 32, smem, s>>>(cd, ds, lbeg, lcnt, nbig, ch2, q2, first, 0);
         return;
     }
     // programmatic dependent launch: the grid is launched while the previous layer's last wave
@@ -884,23 +1034,23 @@ static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, dim3 grid,
     lc.stream = s;
     lc.attrs = at;
     lc.numAttrs = 1;
-    cudaLaunchKernelEx(&lc, k_layer_tma<DC, S>, cd, ds, lbeg, lcnt, q2, first, exact, early);
+    cudaLaunchKernelEx(&lc, k_layer_tma<DC, S>, cd, ds, lbeg, lcnt, nbig, ch2, q2, first, early);
 }
 
 template <int S>
-static bool launch_layer_tma_s(const CodeDev &cd, const DecState &ds, dim3 grid, int lbeg, int lcnt, float q2,
-                               int first, int early, cudaStream_t s) {
+static bool launch_layer_tma_s(const CodeDev &cd, const DecState &ds, int grid_tiles, int l, float q2, int first,
+                               int early, cudaStream_t s) {
     switch (cd.max_dc) {
-        case 1: case 2: launch_layer_tma_t<2, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
-        case 3: launch_layer_tma_t<3, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
-        case 4: launch_layer_tma_t<4, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
-        case 5: launch_layer_tma_t<5, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
-        case 6: launch_layer_tma_t<6, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
-        case 7: launch_layer_tma_t<7, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
-        case 8: launch_layer_tma_t<8, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
-        case 9: launch_layer_tma_t<9, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
-        case 10: launch_layer_tma_t<10, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
-        case 11: case 12: launch_layer_tma_t<12, S>(cd, ds, grid, lbeg, lcnt, q2, first, early, s); return true;
+        case 1: case 2: launch_layer_tma_t<2, S>(cd, ds, grid_tiles, l, q2, first, early, s); return true;
+        case 3: launch_layer_tma_t<3, S>(cd, ds, grid_tiles, l, q2, first, early, s); return true;
+        case 4: launch_layer_tma_t<4, S>(cd, ds, grid_tiles, l, q2, first, early, s); return true;
+        case 5: launch_layer_tma_t<5, S>(cd, ds, grid_tiles, l, q2, first, early, s); return true;
+        case 6: launch_layer_tma_t<6, S>(cd, ds, grid_tiles, l, q2, first, early, s); return true;
+        case 7: launch_layer_tma_t<7, S>(cd, ds, grid_tiles, l, q2, first, early, s); return true;
+        case 8: launch_layer_tma_t<8, S>(cd, ds, grid_tiles, l, q2, first, early, s); return true;
+        case 9: launch_layer_tma_t<9, S>(cd, ds, grid_tiles, l, q2, first, early, s); return true;
+        case 10: launch_layer_tma_t<10, S>(cd, ds, grid_tiles, l, q2, first, early, s); return true;
+        case 11: case 12: launch_layer_tma_t<12, S>(cd, ds, grid_tiles, l, q2, first, early, s); return true;
         default: return false;
     }
 }
@@ -981,9 +1131,9 @@ int launch_layers(const CodeDev &cd, const DecState &ds, int grid_tiles, float q
             // the tile lists / messages may be read before the dependency wait only when the
             // previous kernel of the stream is the layer kernel launched just above
             const int early = (l > 0 && layer_pdl_enabled() && layer_early_enabled()) ? 1 : 0;
-            if (ds.subs == 4) launch_layer_tma_s<4>(cd, ds, grid, lbeg, lcnt, q2, f, early, s);
-            else if (ds.subs == 2) launch_layer_tma_s<2>(cd, ds, grid, lbeg, lcnt, q2, f, early, s);
-            else launch_layer_tma_s<1>(cd, ds, grid, lbeg, lcnt, q2, f, early, s);
+            if (ds.subs == 4) launch_layer_tma_s<4>(cd, ds, grid_tiles, l, q2, f, early, s);
+            else if (ds.subs == 2) launch_layer_tma_s<2>(cd, ds, grid_tiles, l, q2, f, early, s);
+            else launch_layer_tma_s<1>(cd, ds, grid_tiles, l, q2, f, early, s);
             continue;
         }
         if (ds.subs == 4) launch_layer_s<4>(cd, ds, grid, lbeg, lcnt, q2, s);
