@@ -192,6 +192,9 @@ constexpr int LT_CH = CVSR_LT_CH;  // checks per warp
 #define CVSR_LT_CH2 12
 #endif
 constexpr int LT_CH2 = CVSR_LT_CH2;  // degree <= 2 checks per warp (codes with DC >= 6)
+#ifndef CVSR_LT_CH2_WAVES
+#define CVSR_LT_CH2_WAVES 4  // shorter tail chunks below this many waves of warps
+#endif
 static_assert(LT_CH <= 32 && LT_CH2 <= 32, "a chunk's descriptors are held one per lane");
 
 template <int DC, int S>
@@ -1015,7 +1018,7 @@ static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, int grid_t
     }
     int ch2 = LT_CH2;
     const int64_t tail = (int64_t)(lcnt - nbig) * grid_tiles;
-    while (ch2 > LT_CH && tail < (int64_t)4 * resident * ch2) ch2 -= LT_CH;
+    while (ch2 > LT_CH && tail < (int64_t)CVSR_LT_CH2_WAVES * resident * ch2) ch2 -= LT_CH;
     const int chunks = (nbig + LT_CH - 1) / LT_CH + (lcnt - nbig + ch2 - 1) / ch2;
     const dim3 grid((chunks + lt_warps(S) - 1) / lt_warps(S), grid_tiles);
     if (!layer_pdl_enabled()) {
