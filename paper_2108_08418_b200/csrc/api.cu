@@ -250,6 +250,18 @@ double compact_frac() {
     return v;
 }
 
+// compaction only when it frees at least this many tiles: at C4 (125 frames, 2 tiles) the 2 -> 1
+// compaction moved 1.1 GB per slice to save half of a few tail iterations whose cost is mostly
+// per-launch (C4 99.7 ms with, 98.6 ms without; C2's 32 tiles still gain: 41.8 vs 44.9 ms)
+int compact_min_free() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("CVSR_COMPACT_MIN_FREE");  // tuning switch
+        v = e ? atoi(e) : 2;
+    }
+    return v;
+}
+
 // second arena for frame compaction (see bp_kernels.cu "frame compaction")
 struct CompactArena {
     float *msg = nullptr, *L = nullptr;
@@ -371,7 +383,8 @@ cvsr_status run_decode(cvsr_ctx *ctx, const cvsr_code *code, const DecState &ds0
         if (lanes == 0) return false;
         bound = std::min(bound, std::max(na, 1));
         // compaction: the active frames fill at most compact_frac of the active tiles
-        if (ca && k < max_iter && na >= 2 && (double)lanes <= compact_frac() * (double)na * T) {
+        if (ca && k < max_iter && na >= 2 && (double)lanes <= compact_frac() * (double)na * T &&
+            na - (lanes + T - 1) / T >= compact_min_free()) {
             DecState dst = ds;
             if (arena == 0) {
                 dst.msg = ca->msg;
@@ -1006,7 +1019,7 @@ cvsr_status cvsr_decode(cvsr_ctx *ctx, const cvsr_code *code, const float *llr, 
     const bool layered = layered_requested(opts->flags) && layered_supported(cd);
     const int subs = pick_subs(frames, cd.E, layered, cd.max_dc);
     const int tiles = tiles_for(frames, subs);
-    const bool comp = compact_enabled() && tiles >= 2;
+    const bool comp = compact_enabled() && tiles >= 1 + compact_min_free();
     char *base;
     if (cvsr_status st = scratch_reserve(ctx, decstate_bytes(tiles, frames, subs, cd.n, cd.M, cd.E) +
                                                   (comp ? compact_bytes(tiles, subs, cd.n, cd.M, cd.E) : 0),
@@ -1136,7 +1149,7 @@ cvsr_status cvsr_reconcile(cvsr_ctx *ctx, int32_t m, const cvsr_code *const *cod
         lay_j[j] = want_layered && layered_supported(cd);
         subs_j[j] = pick_subs(frames, cd.E, lay_j[j], cd.max_dc);
         tiles_j[j] = tiles_for(frames, subs_j[j]);
-        comp_j[j] = compact_enabled() && tiles_j[j] >= 2;
+        comp_j[j] = compact_enabled() && tiles_j[j] >= 1 + compact_min_free();
         size_t b = decstate_bytes(tiles_j[j], frames, subs_j[j], n, cd.M, cd.E);
         if (comp_j[j]) b += compact_bytes(tiles_j[j], subs_j[j], n, cd.M, cd.E);
         dec_bytes = std::max(dec_bytes, b);
