@@ -51,7 +51,8 @@
  *    (persistent k_layer_tmap), CVSR_LAYER_PDL [1] (layer kernels launched as
  *    programmatic dependents), CVSR_LAYER_EARLY [1] (tile lists and first
  *    message lines read before the dependency wait), CVSR_LAYER_PAIRS [1]
- *    (degree <= 2 layer tails in longer chunks), CVSR_SYND_TEST_W [1]
+ *    (degree <= 2 layer tails in longer chunks; CVSR_LAYER_CH2_WAVES [4]: 12-check
+ *    chunks only above that many waves of warps), CVSR_SYND_TEST_W [1]
  *    (syndrome test from the padded layer rows, two tiles per thread);
  *    CVSR_SYND_SLICED [1]: cvsr_syndrome through bit-sliced 32-frame words.
  *  - Layouts.  "frame-major" arrays are [frames][n] row-major.  Packed bit

@@ -1018,7 +1018,11 @@ static void launch_layer_tma_t(const CodeDev &cd, const DecState &ds, int grid_t
     }
     int ch2 = LT_CH2;
     const int64_t tail = (int64_t)(lcnt - nbig) * grid_tiles;
-    while (ch2 > LT_CH && tail < (int64_t)CVSR_LT_CH2_WAVES * resident * ch2) ch2 -= LT_CH;
+    static const int waves = [] {
+        const char *e = getenv("CVSR_LAYER_CH2_WAVES");  // test / tuning switch (0: always LT_CH2)
+        return (e && *e) ? atoi(e) : CVSR_LT_CH2_WAVES;
+    }();
+    while (ch2 > LT_CH && tail < (int64_t)waves * resident * ch2) ch2 -= LT_CH;
     const int chunks = (nbig + LT_CH - 1) / LT_CH + (lcnt - nbig + ch2 - 1) / ch2;
     const dim3 grid((chunks + lt_warps(S) - 1) / lt_warps(S), grid_tiles);
     if (!layer_pdl_enabled()) {

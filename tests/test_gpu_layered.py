@@ -293,8 +293,9 @@ def test_layered_variants_bit_identical(tmp_path):
     the persistent k_layer_tmap (CVSR_LAYER_PERSIST=1), frame compaction off (CVSR_COMPACT=0),
     plain stream-ordered layer launches (CVSR_LAYER_PDL=0), no reads before the dependency wait
     (CVSR_LAYER_EARLY=0), the thread-per-(check, tile) syndrome test (CVSR_SYND_TEST_W=0) and
-    Bob's per-frame syndrome kernels (CVSR_SYND_SLICED=0) and degree <= 2 checks in 4-check chunks
-    (CVSR_LAYER_PAIRS=0) give bit-identical labels, flags and iteration counts on a multi-tile C4-structure and C2
+    Bob's per-frame syndrome kernels (CVSR_SYND_SLICED=0), degree <= 2 checks in 4-check chunks
+    (CVSR_LAYER_PAIRS=0) or always in 12-check chunks (CVSR_LAYER_CH2_WAVES=0; at these sizes the
+    default takes 4) give bit-identical labels, flags and iteration counts on a multi-tile C4-structure and C2
     reconcile."""
     prog = r'''
 import sys, numpy as np, torch
@@ -321,7 +322,8 @@ np.savez(sys.argv[1], **out)
                      ("reg", {"CVSR_LAYER_TMA": "0"}), ("persist", {"CVSR_LAYER_PERSIST": "1"}),
                      ("nocompact", {"CVSR_COMPACT": "0"}), ("nopdl", {"CVSR_LAYER_PDL": "0"}),
                      ("noearly", {"CVSR_LAYER_EARLY": "0"}), ("synd_test_thread", {"CVSR_SYND_TEST_W": "0"}),
-                     ("bob_synd_per_frame", {"CVSR_SYND_SLICED": "0"}), ("nopairs", {"CVSR_LAYER_PAIRS": "0"})):
+                     ("bob_synd_per_frame", {"CVSR_SYND_SLICED": "0"}), ("nopairs", {"CVSR_LAYER_PAIRS": "0"}),
+                     ("pairs12", {"CVSR_LAYER_CH2_WAVES": "0"})):
         path = str(tmp_path / f"{tag}.npz")
         res = subprocess.run([sys.executable, "-c", prog, path], cwd=ROOT, env=dict(os.environ, **env),
                              capture_output=True, text=True, timeout=900)
