@@ -33,9 +33,12 @@
 //   The syndrome test H xhat = s of iteration k-1 is fused into CN pass k.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "vec.cuh"
+
 #include "bp_device.cuh"
 
 namespace cvsr {
@@ -784,27 +787,32 @@ __global__ void __launch_bounds__(1024) k_list(DecState ds, int32_t *host_counts
 }
 
 // Write the hard decisions of retired frames as packed bits (32x32 bit transposes by ballots).
+// Grid-stride over (retired tile, block of WARPS_PER_BLOCK words): most iterations retire no tile,
+// and a grid sized for every tile's words was ~8k blocks that only read the count and exit.
 __global__ void __launch_bounds__(BLOCK) k_retire(DecState ds, int32_t n, uint32_t *bits_out) {
-    const int ti = blockIdx.y;
-    if (ti >= ds.counts[1]) return;
-    const int t = ds.retire_list[ti];
-    const uint4 newly = ds.tile_newly[t];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nr = ds.counts[1];
     const int Wn = words_of(n);
-    const int w = blockIdx.x * WARPS_PER_BLOCK + warp;
-    if (w >= Wn) return;
-    const int v = w * 32 + lane;
-    const uint4 word = (v < n) ? ds.hb[(size_t)t * n + v] : make_uint4(0u, 0u, 0u, 0u);
+    const int nwb = (Wn + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t item = blockIdx.x; item < (int64_t)nr * nwb; item += gridDim.x) {
+        const int ti = (int)(item / nwb);
+        const int w = (int)(item - (int64_t)ti * nwb) * WARPS_PER_BLOCK + warp;
+        if (w >= Wn) continue;  // warp-uniform
+        const int t = ds.retire_list[ti];
+        const uint4 newly = ds.tile_newly[t];
+        const int v = w * 32 + lane;
+        const uint4 word = (v < n) ? ds.hb[(size_t)t * n + v] : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-    for (int s = 0; s < SUBS; ++s) {
-        const uint32_t ns = cmpu(newly, s);
-        if (!ns) continue;
-        // lane i holds bit f = decision of variable 32 w + i for frame lane f; lane f needs the
-        // word over the 32 variables: a 32 x 32 bit transpose (5 shuffle rounds of block swaps)
-        const uint32_t mine = transpose32(cmpu(word, s), lane);
-        const int slot = t * ds.tile_frames + s * LANES + lane;
-        const int frame = ds.slot_frame ? ds.slot_frame[slot] : slot;
-        if (((ns >> lane) & 1u) && frame >= 0 && frame < ds.frames) bits_out[(size_t)frame * Wn + w] = mine;
+        for (int s = 0; s < SUBS; ++s) {
+            const uint32_t ns = cmpu(newly, s);
+            if (!ns) continue;
+            // lane i holds bit f = decision of variable 32 w + i for frame lane f; lane f needs the
+            // word over the 32 variables: a 32 x 32 bit transpose (5 shuffle rounds of block swaps)
+            const uint32_t mine = transpose32(cmpu(word, s), lane);
+            const int slot = t * ds.tile_frames + s * LANES + lane;
+            const int frame = ds.slot_frame ? ds.slot_frame[slot] : slot;
+            if (((ns >> lane) & 1u) && frame >= 0 && frame < ds.frames) bits_out[(size_t)frame * Wn + w] = mine;
+        }
     }
 }
 
@@ -1382,8 +1390,8 @@ void launch_status(const DecState &ds, int k, int max_iter, int final_pass, int3
 
 void launch_retire(const DecState &ds, int32_t n, int grid_tiles, uint32_t *bits_out, cudaStream_t s) {
     if (grid_tiles <= 0) return;
-    dim3 grid((words_of(n) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK, grid_tiles);
-    k_retire<<<grid, BLOCK, 0, s>>>(ds, n, bits_out);
+    const int64_t items = (int64_t)((words_of(n) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK) * grid_tiles;
+    k_retire<<<(unsigned)std::min<int64_t>(items, 148 * 8), BLOCK, 0, s>>>(ds, n, bits_out);
 }
 
 void launch_to_interleaved(const float *src, float *dst, int32_t F, int64_t rows, int tiles, int subs, float scale,
