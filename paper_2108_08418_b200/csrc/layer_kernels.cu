@@ -316,9 +316,11 @@ __device__ __forceinline__ void lt_check(float *__restrict__ sp, int deg, uint32
 #define CVSR_LT_EXACT 1
 #endif
 // exact-degree bodies are used up to this maximum check degree: measured faster on C2 (degrees 4/5:
-// 43.8 vs 46.6 ms per step) and slower on C4 (6/7, 8/9: 86.0 vs 84.3 ms; more i-cache misses)
+// 43.8 vs 46.6 ms per step); on C4 (6/7, 8/9) slower with 8-warp blocks (86.0 vs 84.3 ms, i-cache)
+// and faster with the final 4-warp blocks and MET tail chunks (96.0 vs 97.4 ms; C4fast 74.2 vs 75.2;
+// C3 11.5 vs 11.3: its degree-6 core checks are few and the kernel's registers rise 76 -> 96)
 #ifndef CVSR_LT_EXACT_MAXDC
-#define CVSR_LT_EXACT_MAXDC 5
+#define CVSR_LT_EXACT_MAXDC 12
 #endif
 // k_layer_tma's pipeline for a chunk of nc <= LT_CH2 degree <= 2 checks (layer positions g0 ..):
 // NS2 slots of 2 posterior + 2 message lines cut from the warp's stages, one mbarrier each.  Same
@@ -539,7 +541,9 @@ __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
         // exact-degree bodies for the two largest degrees (the irregular codes' checks take two
         // consecutive degrees; no padded dummy edges, no degree predicates), the 2-edge body for
         // MET type-A checks, and the padded body otherwise
-        if constexpr (CVSR_LT_EXACT && DC <= CVSR_LT_EXACT_MAXDC) {
+        if (DC >= 6 && deg <= 2) {
+            lt_check<2, DC, S, false>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
+        } else if constexpr (CVSR_LT_EXACT && DC <= CVSR_LT_EXACT_MAXDC) {
             if (deg == DC)
                 lt_check<DC, DC, S, true>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
             else if (DC > 3 && deg == DC - 1)
@@ -548,10 +552,7 @@ __global__ void __launch_bounds__(lt_warps(S) * 32, LtLayout<DC, S>::BLOCKS)
             else
                 lt_check<DC, DC, S, false>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
         } else {
-            if (DC >= 6 && deg <= 2)
-                lt_check<2, DC, S, false>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
-            else
-                lt_check<DC, DC, S, false>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
+            lt_check<DC, DC, S, false>(sp, deg, sb, lane, qmax2, f1, lo, vrow, al, act, mw, Lw, hbt);
         }
         fence_proxy_async_smem();
         __syncwarp();
