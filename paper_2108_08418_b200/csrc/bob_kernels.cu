@@ -457,12 +457,22 @@ struct HashKeys {
     unsigned long long k[CVSR_HASH_KEYS];
 };
 
+// One block per frame, FH_T threads: thread t runs Horner over its words i = t + k T with K = key^T
+// (6 independent chains for 2 labels x 3 keys), so h_t = sum_k w_{t+kT} key^{kT}; the block sums
+// h_t key^{t+1} = sum_i w_i key^{i+1} (independent of T).  1024 threads: the chains are
+// latency-bound 64-bit multiplies: with fewer frames than 2 blocks per SM and long frames (C4: 125
+// frames of 250k words) 1024 threads per block (hash check 0.63 -> 0.38 ms per step); otherwise
+// 256, since each thread's powers of the keys cost about as much as 16 words (C2: 0.39 vs 0.68 ms).
+constexpr int FH_T = 1024;
+static int frame_hash_threads(int32_t F, int32_t n) {
+    return (F < 2 * 148 && (n + 3) / 4 >= 64 * FH_T) ? FH_T : 256;
+}
 template <int NL, int NK>
-__global__ void __launch_bounds__(256) k_frame_hash(const uint8_t *__restrict__ label_a,
-                                                   const uint8_t *__restrict__ label_b, int32_t n, HashKeys keys,
-                                                   unsigned long long *__restrict__ out_a,
-                                                   unsigned long long *__restrict__ out_b,
-                                                   const uint8_t *__restrict__ ok_in, uint8_t *__restrict__ ok_out) {
+__global__ void __launch_bounds__(FH_T) k_frame_hash(const uint8_t *__restrict__ label_a,
+                                                    const uint8_t *__restrict__ label_b, int32_t n, HashKeys keys,
+                                                    unsigned long long *__restrict__ out_a,
+                                                    unsigned long long *__restrict__ out_b,
+                                                    const uint8_t *__restrict__ ok_in, uint8_t *__restrict__ ok_out) {
     const int f = blockIdx.x, T = blockDim.x, t = threadIdx.x;
     const int W = (n + 3) / 4;
     const bool aligned = (n & 3) == 0;
@@ -486,32 +496,43 @@ __global__ void __launch_bounds__(256) k_frame_hash(const uint8_t *__restrict__ 
             if (NL == 2) h[NL - 1][q] = addmod61(mulmod61(h[NL - 1][q], K[q]), wb);
         }
     }
-    __shared__ unsigned long long s[NL * NK][256];
+    // h_t key^{t+1}, summed over the warp by shuffles, then over the warps
+    __shared__ unsigned long long sw[NL * NK][FH_T / 32];
+    const int lane = t & 31, warp = t >> 5;
 #pragma unroll
     for (int q = 0; q < NK; ++q) {
         const unsigned long long kt = powmod61(keys.k[q], (unsigned long long)(t + 1));
 #pragma unroll
-        for (int l = 0; l < NL; ++l) s[l * NK + q][t] = mulmod61(h[l][q], kt);
+        for (int l = 0; l < NL; ++l) {
+            unsigned long long v = mulmod61(h[l][q], kt);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v = addmod61(v, __shfl_xor_sync(0xffffffffu, v, o));
+            if (lane == 0) sw[l * NK + q][warp] = v;
+        }
     }
     __syncthreads();
-    for (int o = T / 2; o > 0; o >>= 1) {
-        if (t < o) {
+    if (warp == 0) {
+        const int nw = T / 32;
+        unsigned long long tot[NL * NK];
 #pragma unroll
-            for (int r = 0; r < NL * NK; ++r) s[r][t] = addmod61(s[r][t], s[r][t + o]);
+        for (int r = 0; r < NL * NK; ++r) {
+            unsigned long long v = lane < nw ? sw[r][lane] : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v = addmod61(v, __shfl_xor_sync(0xffffffffu, v, o));
+            tot[r] = v;
         }
-        __syncthreads();
-    }
-    if (t == 0) {
-        bool eq = true;
+        if (lane == 0) {
+            bool eq = true;
 #pragma unroll
-        for (int q = 0; q < NK; ++q) {
-            if (out_a) out_a[(size_t)f * NK + q] = s[q][0];
-            if (NL == 2) {
-                if (out_b) out_b[(size_t)f * NK + q] = s[NK + q][0];
-                eq = eq && s[q][0] == s[NK + q][0];
+            for (int q = 0; q < NK; ++q) {
+                if (out_a) out_a[(size_t)f * NK + q] = tot[q];
+                if (NL == 2) {
+                    if (out_b) out_b[(size_t)f * NK + q] = tot[NK + q];
+                    eq = eq && tot[q] == tot[NK + q];
+                }
             }
+            if (NL == 2) ok_out[f] = (uint8_t)(ok_in[f] && eq);
         }
-        if (NL == 2) ok_out[f] = (uint8_t)(ok_in[f] && eq);
     }
 }
 
@@ -519,7 +540,7 @@ void launch_frame_hash(const uint8_t *label, int32_t F, int32_t n, unsigned long
                        cudaStream_t s) {
     HashKeys k{};
     k.k[0] = key;
-    k_frame_hash<1, 1><<<F, 256, 0, s>>>(label, nullptr, n, k, out, nullptr, nullptr, nullptr);
+    k_frame_hash<1, 1><<<F, frame_hash_threads(F, n), 0, s>>>(label, nullptr, n, k, out, nullptr, nullptr, nullptr);
 }
 
 void launch_verify(const uint8_t *label_a, const uint8_t *label_b, const uint8_t *ok_in, int32_t F, int32_t n,
@@ -527,7 +548,8 @@ void launch_verify(const uint8_t *label_a, const uint8_t *label_b, const uint8_t
                    cudaStream_t s) {
     HashKeys k{};
     for (int q = 0; q < CVSR_HASH_KEYS; ++q) k.k[q] = keys[q];
-    k_frame_hash<2, CVSR_HASH_KEYS><<<F, 256, 0, s>>>(label_a, label_b, n, k, ha, hb, ok_in, ok_out);
+    k_frame_hash<2, CVSR_HASH_KEYS><<<F, frame_hash_threads(F, n), 0, s>>>(label_a, label_b, n, k, ha, hb, ok_in,
+                                                                            ok_out);
 }
 
 }  // namespace cvsr

@@ -466,10 +466,11 @@ def test_compaction_switch_subprocess():
 
 
 # ----------------------------------------------------------------- verification hash (R-6)
-@pytest.mark.parametrize("n", [1, 3, 5, 255, 1024, 4097, 65536])
+@pytest.mark.parametrize("n", [1, 3, 5, 255, 1024, 4097, 65536, 262147])
 def test_frame_hash_and_verify_bitexact(cv, ctx, n):
     """cvsr_frame_hash / cvsr_verify equal the oracle's polynomial hash bit for bit (aligned and
-    ragged n); verified = frame_ok AND equal hashes; a single flipped label bit is caught."""
+    ragged n; n = 262147 takes the 1024-thread blocks used for few long frames); verified =
+    frame_ok AND equal hashes; a single flipped label bit is caught."""
     from oracle import verify
     rng = np.random.default_rng(n)
     F = 6 if n < 65536 else 3
